@@ -1,0 +1,206 @@
+/*
+ * bfmm.h — C ABI of the B200-native black-box FMM matvec (phi = K sigma).
+ *
+ * This is the drop-in boundary under the Python evaluator
+ * (paper_1903_02153_b200.FmmEvaluator), which mirrors the reference's
+ * FmmEvaluator.evaluate (engine.py:482-536).  The reference has no FFI of
+ * its own (it is pure Python/NumPy); each entry point below
+ * replaces one NumPy stage of that method and cites it.
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory allocated by the caller
+ *    (PyTorch in the shipped host), except where marked "host".
+ *  - Every call is asynchronous on `stream` (a cudaStream_t) and returns 0
+ *    on success; nonzero means a launch/config error whose text is
+ *    available from bfmm_last_error().  No call synchronises except
+ *    bfmm_kernel_compile (NVRTC) and bfmm_device_fp64_probe.
+ *  - Internal data layouts (all float64, row-major):
+ *      pts4      (N, 4)        sorted points x, y, z, weight column 0
+ *      wsorted   (N, m)        sorted weights
+ *      moments / locals (8^l, m, p^3)   dense over every cell of a level
+ *      z / lt    (8^l, m, rp)  rank-space moments / local accumulators,
+ *                              rp = rank padded to a multiple of 8
+ *  - Cell ids are the reference's Morton ids (octree.py:75-107): x in the
+ *    high bit of each bit triple, children of q are 8q..8q+7.
+ */
+#ifndef BFMM_H
+#define BFMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *bfmm_stream_t; /* cudaStream_t */
+
+/* ---- library ---------------------------------------------------------- */
+const char *bfmm_last_error(void);
+int bfmm_version(void);
+
+/* ---- tree: distribute (engine.py:60-94, octree.py:186-200) ------------ */
+
+/* Scratch bytes bfmm_tree_build needs for n points at `levels`. */
+size_t bfmm_tree_scratch_bytes(int64_t n, int levels);
+
+/* Leaf id per point (floor((x-lo)/h), clip, Morton; octree.py:186-200),
+ * stable radix sort (== np.argsort(kind="stable"), engine.py:74),
+ * run-length encode (== np.unique(return_index, return_counts),
+ * engine.py:76-77), plus dense per-cell (start, count) maps.
+ * geom (host) = {lo_x, lo_y, lo_z, hi_x, hi_y, hi_z, h, tol}.
+ * domain_flag is set to 1 when a point lies outside [lo-tol, hi+tol]
+ * (the DomainError of octree.py:190-196).  leaves/starts/counts have
+ * capacity n; *n_leaves (device) receives the nonempty-leaf count. */
+int bfmm_tree_build(const double *points, int64_t n, const double *geom,
+                    int levels, void *scratch, size_t scratch_bytes,
+                    int64_t *perm, double *pts4, int64_t *leaves,
+                    int64_t *starts, int64_t *counts, int64_t *n_leaves,
+                    int32_t *cell_start, int32_t *cell_count,
+                    int32_t *domain_flag, bfmm_stream_t stream);
+
+/* w (N, m) original order -> wsorted (N, m) and pts4[:, 3] = w[perm, 0]
+ * (the weights[part.perm] of engine.py:168,528). */
+int bfmm_gather_weights(const double *w, int64_t n, int m,
+                        const int64_t *perm, double *wsorted, double *pts4,
+                        bfmm_stream_t stream);
+
+/* ---- upward pass ------------------------------------------------------- */
+
+/* P2M leaf_moments (engine.py:159-185).  interp (host) holds the 1-D
+ * basis: scheme 0 (Chebyshev) p*p coefficients S[n][j] = c_n T_n(x_j),
+ * scheme 1 (uniform) p nodes followed by p*p inverse node differences.
+ * geom (host) = {lo_x, lo_y, lo_z, h_leaf}.  moments must be zeroed by the
+ * caller; cells without points stay zero.  ref_flag is set when a point's
+ * leaf-frame coordinate exceeds 1 + 1e-9 (engine.py:339-345). */
+int bfmm_p2m(const double *pts4, const double *wsorted, int m,
+             const int64_t *leaves, const int64_t *starts,
+             const int64_t *counts, const int64_t *n_leaves,
+             int64_t max_leaves, int levels, int p, int scheme,
+             const double *interp, const double *geom, double *moments,
+             int32_t *ref_flag, bfmm_stream_t stream);
+
+/* M2M ascend (engine.py:187-204): parent[q] = sum_o T[o] child[8q+o] with
+ * T[o] = kron(Hx, Hy, Hz) (interpolation.py:136-155).  H (host) holds the
+ * two p x p half-interval matrices H[s][a][b], s = 0 lower / 1 upper half. */
+int bfmm_m2m(const double *child, double *parent, int64_t n_parent, int p,
+             int m, const double *H, bfmm_stream_t stream);
+
+/* ---- far field --------------------------------------------------------- */
+
+/* C = alpha * A @ B + beta * C for row-major A (rows, K), B (K, N),
+ * C (rows, N).  Used for z = moments @ V and locals = scale * lt @ U^T
+ * (engine.py:233, 252-255). */
+int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
+                   int N, double *C, double alpha, double beta,
+                   bfmm_stream_t stream);
+
+/* M2L Chebyshev (engine.py:228-256): for every cell c at `level` and
+ * column, lt[c] = sum over the valid far offsets t of z[c + t] @ coresT[t],
+ * with coresT[t][k][i] = C_t[i][k] padded to rp x rp.  The valid offsets
+ * per child octant follow octree.py:128-145 and match
+ * cell_pairs_for_offset (octree.py:202-221) pair for pair. */
+int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
+                  const double *coresT, bfmm_stream_t stream);
+
+/* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
+ * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ).  symbols (device)
+ * (316, q, q, q//2+1) complex128 interleaved. */
+int bfmm_m2l_fft_scratch_bytes(int level, int m, int p, size_t *bytes);
+int bfmm_m2l_fft(const double *moments, double *locals, int level, int m,
+                 int p, const double *symbols, double scale, void *scratch,
+                 size_t scratch_bytes, bfmm_stream_t stream);
+
+/* ---- downward pass ----------------------------------------------------- */
+
+/* L2L descend (engine.py:296-311): child[8q+o] += T[o]^T parent[q]. */
+int bfmm_l2l(const double *parent, double *child, int64_t n_parent, int p,
+             int m, const double *H, bfmm_stream_t stream);
+
+/* L2P read_potentials (engine.py:313-337): phi_sorted[i] =
+ * W(x_i) . locals[leaf(i)] (assigns; targets in sorted order). */
+int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
+             const int64_t *starts, const int64_t *counts,
+             const int64_t *n_leaves, int64_t max_leaves, int levels, int p,
+             int scheme, const double *interp, const double *geom,
+             const double *locals, double *phi_sorted, int32_t *ref_flag,
+             bfmm_stream_t stream);
+
+/* ---- near field (engine.py:349-478) ------------------------------------ */
+
+/* Compile (NVRTC, cached by source) a P2P kernel for a device functor.
+ * kind: 0 = expression in r (profile), 1 = expression in r2,
+ * 2 = expression in dx, dy, dz (diff_func).  Returns a handle > 0 in
+ * *handle.  Built-in handles (no JIT): 1 laplacian, 2 laplacianforce,
+ * 3 gaussian, 4 exponential, 5 logarithm. */
+int bfmm_kernel_compile(int kind, const char *expr, int *handle);
+
+/* Scratch bytes bfmm_p2p needs (per-leaf chunk prefix). */
+size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves);
+
+/* out[i] = sum over the 27 neighbour leaves of the target leaf of
+ * K(x_i - y_j) w_j (assigns every target row), targets and sources both in
+ * sorted order.  The source structure is the dense per-cell (start, count)
+ * map of bfmm_tree_build. */
+int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
+             const int64_t *tstarts, const int64_t *tcounts,
+             const int64_t *n_tleaves, int64_t max_tleaves,
+             const double *spts4, const double *swsorted, int m,
+             const int32_t *scell_start, const int32_t *scell_count,
+             int levels, double *out, void *scratch, size_t scratch_bytes,
+             bfmm_stream_t stream);
+
+/* Locate the first non-finite kernel value in the near field in the
+ * reference's enumeration order (offset, target row, source row;
+ * engine.py:362-441).  *key (device, init UINT64_MAX) receives
+ * (offset << 58) | (target_row << 29) | source_row. */
+int bfmm_p2p_locate(int handle, const double *tpts4, const int64_t *tleaves,
+                    const int64_t *tstarts, const int64_t *tcounts,
+                    const int64_t *n_tleaves, int64_t max_tleaves,
+                    const double *spts4, const int32_t *scell_start,
+                    const int32_t *scell_count, int levels,
+                    unsigned long long *key, bfmm_stream_t stream);
+
+/* phi[perm[i]] = far_sorted[i] + near_sorted[i] (engine.py:530);
+ * nonfinite_flag is set when a near-field sum is non-finite. */
+int bfmm_scatter_output(const double *far_sorted, const double *near_sorted,
+                        const int64_t *perm, int64_t n, int m, double *phi,
+                        int32_t *nonfinite_flag, bfmm_stream_t stream);
+
+/* ---- interaction lists (parity / diagnostics) ------------------------- */
+
+/* Far pairs of one offset t_index (0..315, lexicographic) at `level` in
+ * the reference's meshgrid order: identical to
+ * Octree.cell_pairs_for_offset (octree.py:202-221).  Built from the same
+ * far_pair() rule bfmm_m2l_cheb applies.  tg/sr capacity 8^level; *count
+ * (device) receives the pair count. */
+size_t bfmm_far_pairs_scratch_bytes(int level);
+int bfmm_far_pairs(int level, int t_index, int64_t *tg, int64_t *sr,
+                   int64_t *count, void *scratch, size_t scratch_bytes,
+                   bfmm_stream_t stream);
+
+/* Near list of neighbour offset t_index (0..26, lexicographic) like
+ * FmmEvaluator._neighbor_segments (engine.py:401-417): out[i] = index of
+ * the nonempty source leaf at tleaves[i] + t, or -1. */
+int bfmm_near_pairs(int levels, int t_index, const int64_t *tleaves,
+                    const int64_t *n_tleaves, int64_t max_tleaves,
+                    const int64_t *sleaves, const int64_t *n_sleaves,
+                    int64_t *out, bfmm_stream_t stream);
+
+/* Ordered near-field point pairs (timings["near_pairs"], engine.py:532). */
+int bfmm_near_pair_count(const int64_t *tleaves, const int64_t *tcounts,
+                         const int64_t *n_tleaves, int64_t max_tleaves,
+                         const int32_t *scell_count, int levels,
+                         int64_t *total, bfmm_stream_t stream);
+
+/* ---- diagnostics ------------------------------------------------------- */
+
+/* Measure the FP64 FMA peak of this device (GFLOP/s) with a DFMA chain
+ * kernel (synchronises). */
+int bfmm_device_fp64_probe(double *gflops, bfmm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BFMM_H */

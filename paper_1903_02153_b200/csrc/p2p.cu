@@ -1,0 +1,512 @@
+// Near field: built-in device functors, the NVRTC JIT for user kernels,
+// launchers, the non-finite locator and the output scatter.
+#include <cub/cub.cuh>
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "p2p.cuh"
+
+namespace bfmm {
+namespace {
+
+// ---- built-in kernels (kernel.py:149-180): profile f(r) with r = |x - y| ----
+// 1/r, r = 0 -> 0
+struct KLaplace {
+  __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    return r2 == 0.0 ? 0.0 : rsqrt(r2);
+  }
+};
+// 1/r^4, r = 0 -> 0
+struct KLaplaceForce {
+  __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    return r2 == 0.0 ? 0.0 : 1.0 / (r2 * r2);
+  }
+};
+// exp(-r^2)
+struct KGaussian {
+  __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
+    return exp(-(dx * dx + dy * dy + dz * dz));
+  }
+};
+// exp(-r)
+struct KExponential {
+  __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
+    return exp(-sqrt(dx * dx + dy * dy + dz * dz));
+  }
+};
+// log r, r = 0 -> 0
+struct KLogarithm {
+  __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    return r2 == 0.0 ? 0.0 : 0.5 * log(r2);
+  }
+};
+
+constexpr int kMCs[5] = {1, 2, 4, 8, 16};
+
+// ---- JIT (NVRTC + driver API loaded lazily) ---------------------------------
+const char kP2PSource[] =
+#include "p2p_src.inc"
+    ;
+
+struct Driver {
+  bool ok = false;
+  CUresult (*ModuleLoadData)(CUmodule *, const void *) = nullptr;
+  CUresult (*ModuleGetFunction)(CUfunction *, CUmodule, const char *) = nullptr;
+  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, unsigned, unsigned, CUstream, void **,
+                           void **) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char **) = nullptr;
+};
+
+Driver &driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    d.ModuleLoadData = (decltype(d.ModuleLoadData))dlsym(h, "cuModuleLoadData");
+    d.ModuleGetFunction =
+        (decltype(d.ModuleGetFunction))dlsym(h, "cuModuleGetFunction");
+    d.LaunchKernel = (decltype(d.LaunchKernel))dlsym(h, "cuLaunchKernel");
+    d.GetErrorString = (decltype(d.GetErrorString))dlsym(h, "cuGetErrorString");
+    d.ok = d.ModuleLoadData && d.ModuleGetFunction && d.LaunchKernel;
+  });
+  return d;
+}
+
+struct JitKernel {
+  CUfunction p2p[5];
+  CUfunction locate;
+};
+
+std::mutex g_jit_mu;
+std::vector<JitKernel> g_jit;                       // handle - 6
+std::unordered_map<std::string, int> g_jit_cache;  // source -> handle
+
+constexpr int kFirstJit = 6;
+
+std::string functor_source(int kind, const char *expr) {
+  std::string body;
+  if (kind == 0)
+    body = "const double r = sqrt(dx * dx + dy * dy + dz * dz);\n return (" +
+           std::string(expr) + ");";
+  else if (kind == 1)
+    body = "const double r2 = dx * dx + dy * dy + dz * dz;\n return (" +
+           std::string(expr) + ");";
+  else
+    body = "return (" + std::string(expr) + ");";
+  return "struct KUser {\n __device__ __forceinline__ static double eval("
+         "double dx, double dy, double dz) {\n " +
+         body + "\n }\n};\n";
+}
+
+int jit_compile(int kind, const char *expr, int *handle) {
+  std::lock_guard<std::mutex> lock(g_jit_mu);
+  std::string key = std::to_string(kind) + ":" + expr;
+  auto it = g_jit_cache.find(key);
+  if (it != g_jit_cache.end()) {
+    *handle = it->second;
+    return 0;
+  }
+  Driver &d = driver();
+  if (!d.ok) {
+    set_error("bfmm_kernel_compile: libcuda.so.1 not available");
+    return 3;
+  }
+  std::string src = std::string(kP2PSource) + "\nnamespace bfmm_nf {\n" +
+                    functor_source(kind, expr) + "}\n";
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "bfmm_user_p2p.cu", 0, nullptr,
+                         nullptr) != NVRTC_SUCCESS) {
+    set_error("bfmm_kernel_compile: nvrtcCreateProgram failed");
+    return 3;
+  }
+  std::vector<std::string> names;
+  for (int i = 0; i < 5; ++i)
+    names.push_back("bfmm_nf::p2p_kernel<bfmm_nf::KUser, " +
+                    std::to_string(kMCs[i]) + ">");
+  names.push_back("bfmm_nf::locate_kernel<bfmm_nf::KUser>");
+  for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
+  const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17",
+                        "-default-device", "-lineinfo"};
+  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t logn = 0;
+    nvrtcGetProgramLogSize(prog, &logn);
+    std::string log(logn, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    set_error("bfmm_kernel_compile: NVRTC failed for '%s': %s", expr,
+              log.c_str());
+    nvrtcDestroyProgram(&prog);
+    return 4;
+  }
+  size_t cubin_n = 0;
+  nvrtcGetCUBINSize(prog, &cubin_n);
+  std::vector<char> cubin(cubin_n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  std::vector<std::string> lowered;
+  for (auto &n : names) {
+    const char *ln = nullptr;
+    nvrtcGetLoweredName(prog, n.c_str(), &ln);
+    lowered.push_back(ln ? ln : "");
+  }
+  nvrtcDestroyProgram(&prog);
+  // make sure the runtime has initialised the primary context
+  cudaFree(0);
+  CUmodule mod;
+  CUresult cr = d.ModuleLoadData(&mod, cubin.data());
+  if (cr != CUDA_SUCCESS) {
+    const char *msg = "?";
+    if (d.GetErrorString) d.GetErrorString(cr, &msg);
+    set_error("bfmm_kernel_compile: cuModuleLoadData: %s", msg);
+    return 3;
+  }
+  JitKernel jk;
+  for (int i = 0; i < 6; ++i) {
+    CUfunction f;
+    if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
+      set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
+      return 3;
+    }
+    if (i < 5) jk.p2p[i] = f; else jk.locate = f;
+  }
+  g_jit.push_back(jk);
+  *handle = kFirstJit + (int)g_jit.size() - 1;
+  g_jit_cache[key] = *handle;
+  return 0;
+}
+
+// ---- launch helpers ---------------------------------------------------------
+template <class K>
+void launch_builtin(int mci, dim3 grid, const bfmm_nf::Args &a, int c0,
+                    cudaStream_t st) {
+  const int T = 32 * bfmm_nf::kWarps;
+  switch (mci) {
+    case 0: bfmm_nf::p2p_kernel<K, 1><<<grid, T, 0, st>>>(a, c0); break;
+    case 1: bfmm_nf::p2p_kernel<K, 2><<<grid, T, 0, st>>>(a, c0); break;
+    case 2: bfmm_nf::p2p_kernel<K, 4><<<grid, T, 0, st>>>(a, c0); break;
+    case 3: bfmm_nf::p2p_kernel<K, 8><<<grid, T, 0, st>>>(a, c0); break;
+    default: bfmm_nf::p2p_kernel<K, 16><<<grid, T, 0, st>>>(a, c0); break;
+  }
+}
+
+int launch_p2p(int handle, int mci, dim3 grid, const bfmm_nf::Args &a, int c0,
+               cudaStream_t st) {
+  switch (handle) {
+    case 1: launch_builtin<KLaplace>(mci, grid, a, c0, st); break;
+    case 2: launch_builtin<KLaplaceForce>(mci, grid, a, c0, st); break;
+    case 3: launch_builtin<KGaussian>(mci, grid, a, c0, st); break;
+    case 4: launch_builtin<KExponential>(mci, grid, a, c0, st); break;
+    case 5: launch_builtin<KLogarithm>(mci, grid, a, c0, st); break;
+    default: {
+      JitKernel jk;
+      {
+        std::lock_guard<std::mutex> lock(g_jit_mu);
+        if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+          set_error("bfmm_p2p: unknown kernel handle %d", handle);
+          return 2;
+        }
+        jk = g_jit[handle - kFirstJit];
+      }
+      bfmm_nf::Args args = a;
+      int c = c0;
+      void *params[] = {&args, &c};
+      CUresult r = driver().LaunchKernel(jk.p2p[mci], grid.x, 1, 1,
+                                         32 * bfmm_nf::kWarps, 1, 1, 0,
+                                         (CUstream)st, params, nullptr);
+      if (r != CUDA_SUCCESS) {
+        set_error("bfmm_p2p: cuLaunchKernel failed (%d)", (int)r);
+        return 1;
+      }
+      return 0;
+    }
+  }
+  return check_launch("p2p_kernel");
+}
+
+int launch_locate(int handle, const bfmm_nf::Args &a,
+                  unsigned long long *key, cudaStream_t st) {
+  dim3 grid(kNumSMs * 8), block(128);
+  switch (handle) {
+    case 1: bfmm_nf::locate_kernel<KLaplace><<<grid, block, 0, st>>>(a, key); break;
+    case 2: bfmm_nf::locate_kernel<KLaplaceForce><<<grid, block, 0, st>>>(a, key); break;
+    case 3: bfmm_nf::locate_kernel<KGaussian><<<grid, block, 0, st>>>(a, key); break;
+    case 4: bfmm_nf::locate_kernel<KExponential><<<grid, block, 0, st>>>(a, key); break;
+    case 5: bfmm_nf::locate_kernel<KLogarithm><<<grid, block, 0, st>>>(a, key); break;
+    default: {
+      JitKernel jk;
+      {
+        std::lock_guard<std::mutex> lock(g_jit_mu);
+        if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+          set_error("bfmm_p2p_locate: unknown kernel handle %d", handle);
+          return 2;
+        }
+        jk = g_jit[handle - kFirstJit];
+      }
+      bfmm_nf::Args args = a;
+      unsigned long long *k = key;
+      void *params[] = {&args, &k};
+      if (driver().LaunchKernel(jk.locate, grid.x, 1, 1, block.x, 1, 1, 0,
+                                (CUstream)st, params, nullptr) != CUDA_SUCCESS) {
+        set_error("bfmm_p2p_locate: cuLaunchKernel failed");
+        return 1;
+      }
+      return 0;
+    }
+  }
+  return check_launch("locate_kernel");
+}
+
+__global__ void chunk_counts_kernel(const int64_t *__restrict__ counts,
+                                    const int64_t *__restrict__ n_leaves,
+                                    int64_t max_leaves,
+                                    int64_t *__restrict__ nch) {
+  const int64_t nl = *n_leaves;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+       i < max_leaves; i += int64_t(gridDim.x) * blockDim.x)
+    nch[i] = i < nl ? (counts[i] + 31) / 32 : 0;
+}
+
+__global__ void scatter_kernel(const double *__restrict__ far,
+                               const double *__restrict__ near,
+                               const int64_t *__restrict__ perm, int64_t n,
+                               int m, double *__restrict__ phi, int32_t *flag) {
+  const int64_t total = n * m;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m;
+    const int c = (int)(e - i * m);
+    const double nv = near[e];
+    bad |= !isfinite(nv);
+    phi[perm[i] * m + c] = (far ? far[e] : 0.0) + nv;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// Near list for one neighbour offset (engine.py:401-417): per target leaf,
+// the index of the source leaf at cell + t among the nonempty source leaves
+// (np.searchsorted), or -1.  Same in-range rule as the P2P kernel.
+__global__ void near_pairs_kernel(int levels, int t_index,
+                                  const int64_t *__restrict__ tleaves,
+                                  const int64_t *__restrict__ n_tleaves,
+                                  const int64_t *__restrict__ sleaves,
+                                  const int64_t *__restrict__ n_sleaves,
+                                  int64_t *__restrict__ out) {
+  const int64_t nt = *n_tleaves, ns = *n_sleaves;
+  const int n = 1 << levels;
+  const int dx = t_index / 9 - 1, dy = (t_index / 3) % 3 - 1, dz = t_index % 3 - 1;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nt;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int cx, cy, cz;
+    unmorton3((uint64_t)tleaves[i], cx, cy, cz);
+    const int sx = cx + dx, sy = cy + dy, sz = cz + dz;
+    int64_t res = -1;
+    if (sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n) {
+      const int64_t id = (int64_t)morton3(sx, sy, sz);
+      int64_t lo = 0, hi = ns;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (sleaves[mid] < id) lo = mid + 1; else hi = mid;
+      }
+      if (lo < ns && sleaves[lo] == id) res = lo;
+    }
+    out[i] = res;
+  }
+}
+
+// Near pair count (the "near_pairs" timing entry, engine.py:532).
+__global__ void near_count_kernel(const int64_t *__restrict__ tleaves,
+                                  const int64_t *__restrict__ tcounts,
+                                  const int64_t *__restrict__ n_tleaves,
+                                  const int32_t *__restrict__ scell_count,
+                                  int levels, unsigned long long *total) {
+  const int64_t nt = *n_tleaves;
+  const int n = 1 << levels;
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nt;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int cx, cy, cz;
+    unmorton3((uint64_t)tleaves[i], cx, cy, cz);
+    int64_t s = 0;
+    for (int nb = 0; nb < 27; ++nb) {
+      const int sx = cx + nb / 9 - 1, sy = cy + (nb / 3) % 3 - 1, sz = cz + nb % 3 - 1;
+      if (sx < 0 || sx >= n || sy < 0 || sy >= n || sz < 0 || sz >= n) continue;
+      s += scell_count[morton3(sx, sy, sz)];
+    }
+    local += (unsigned long long)(s * tcounts[i]);
+  }
+  atomicAdd(total, local);
+}
+
+size_t p2p_scratch(int64_t max_leaves, size_t *cub_off) {
+  size_t cub_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, cub_bytes, (int64_t *)nullptr,
+                                (int64_t *)nullptr, (int)max_leaves);
+  size_t a = ((size_t)max_leaves * 2 * sizeof(int64_t) + 255) & ~size_t(255);
+  *cub_off = a;
+  return a + cub_bytes + 256;
+}
+
+bfmm_nf::Args make_args(const double *tpts4, const int64_t *tleaves,
+                         const int64_t *tstarts, const int64_t *tcounts,
+                         const int64_t *n_tleaves, const double *spts4,
+                         const double *sw, int m, const int32_t *scs,
+                         const int32_t *scc, int levels, double *out,
+                         const int64_t *work) {
+  bfmm_nf::Args a;
+  a.tpts4 = tpts4;
+  a.tleaves = reinterpret_cast<const long long *>(tleaves);
+  a.tstarts = reinterpret_cast<const long long *>(tstarts);
+  a.tcounts = reinterpret_cast<const long long *>(tcounts);
+  a.n_tleaves = reinterpret_cast<const long long *>(n_tleaves);
+  a.spts4 = spts4;
+  a.sw = sw;
+  a.m = m;
+  a.scell_start = scs;
+  a.scell_count = scc;
+  a.levels = levels;
+  a.out = out;
+  a.work_incl = reinterpret_cast<const long long *>(work);
+  return a;
+}
+
+}  // namespace
+}  // namespace bfmm
+
+using namespace bfmm;
+
+extern "C" int bfmm_kernel_compile(int kind, const char *expr, int *handle) {
+  if (kind < 0 || kind > 2 || !expr || !handle) {
+    set_error("bfmm_kernel_compile: bad arguments");
+    return 2;
+  }
+  return jit_compile(kind, expr, handle);
+}
+
+extern "C" size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves) {
+  size_t off;
+  return p2p_scratch(max_tleaves < 1 ? 1 : max_tleaves, &off);
+}
+
+extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
+                        const int64_t *tstarts, const int64_t *tcounts,
+                        const int64_t *n_tleaves, int64_t max_tleaves,
+                        const double *spts4, const double *swsorted, int m,
+                        const int32_t *scell_start, const int32_t *scell_count,
+                        int levels, double *out, void *scratch,
+                        size_t scratch_bytes, bfmm_stream_t stream) {
+  if (max_tleaves <= 0) return 0;
+  size_t cub_off;
+  size_t need = p2p_scratch(max_tleaves, &cub_off);
+  if (scratch_bytes < need) {
+    set_error("bfmm_p2p: scratch too small (%zu < %zu)", scratch_bytes, need);
+    return 2;
+  }
+  cudaStream_t st = as_stream(stream);
+  int64_t *nch = static_cast<int64_t *>(scratch);
+  int64_t *incl = nch + max_tleaves;
+  chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256),
+                                                    kNumSMs * 16),
+                        256, 0, st>>>(tcounts, n_tleaves, max_tleaves, nch);
+  if (check_launch("chunk_counts_kernel")) return 1;
+  size_t cb = need - cub_off;
+  if (cub::DeviceScan::InclusiveSum(static_cast<char *>(scratch) + cub_off, cb,
+                                    nch, incl, (int)max_tleaves,
+                                    st) != cudaSuccess) {
+    set_error("bfmm_p2p: scan failed");
+    return 1;
+  }
+  bfmm_nf::Args a = make_args(tpts4, tleaves, tstarts, tcounts, n_tleaves,
+                               spts4, swsorted, m, scell_start, scell_count,
+                               levels, out, incl);
+  // persistent-style grid: 16 CTAs (64 warps) per SM, grid-stride over chunks
+  dim3 grid(kNumSMs * 16);
+  int c0 = 0;
+  while (c0 < m) {
+    const int left = m - c0;
+    int mci = 0;
+    if (m == 1) mci = 0;
+    else if (left >= 16) mci = 4;
+    else if (left >= 8) mci = 3;
+    else if (left >= 4) mci = 2;
+    else if (left >= 2) mci = 1;
+    else mci = 0;
+    int rc = launch_p2p(handle, mci, grid, a, c0, st);
+    if (rc) return rc;
+    c0 += kMCs[mci];
+  }
+  return 0;
+}
+
+extern "C" int bfmm_p2p_locate(int handle, const double *tpts4,
+                               const int64_t *tleaves, const int64_t *tstarts,
+                               const int64_t *tcounts, const int64_t *n_tleaves,
+                               int64_t max_tleaves, const double *spts4,
+                               const int32_t *scell_start,
+                               const int32_t *scell_count, int levels,
+                               unsigned long long *key, bfmm_stream_t stream) {
+  if (max_tleaves <= 0) return 0;
+  bfmm_nf::Args a = make_args(tpts4, tleaves, tstarts, tcounts, n_tleaves,
+                               spts4, nullptr, 1, scell_start, scell_count,
+                               levels, nullptr, nullptr);
+  return launch_locate(handle, a, key, as_stream(stream));
+}
+
+extern "C" int bfmm_near_pairs(int levels, int t_index, const int64_t *tleaves,
+                               const int64_t *n_tleaves, int64_t max_tleaves,
+                               const int64_t *sleaves, const int64_t *n_sleaves,
+                               int64_t *out, bfmm_stream_t stream) {
+  if (t_index < 0 || t_index >= 27) {
+    set_error("bfmm_near_pairs: offset index %d outside [0, 27)", t_index);
+    return 2;
+  }
+  if (max_tleaves <= 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256), 4096);
+  near_pairs_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      levels, t_index, tleaves, n_tleaves, sleaves, n_sleaves, out);
+  return check_launch("near_pairs_kernel");
+}
+
+extern "C" int bfmm_near_pair_count(const int64_t *tleaves,
+                                    const int64_t *tcounts,
+                                    const int64_t *n_tleaves,
+                                    int64_t max_tleaves,
+                                    const int32_t *scell_count, int levels,
+                                    int64_t *total, bfmm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(total, 0, sizeof(int64_t), st) != cudaSuccess) {
+    set_error("bfmm_near_pair_count: memset failed");
+    return 1;
+  }
+  if (max_tleaves <= 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256), 1024);
+  near_count_kernel<<<grid, 256, 0, st>>>(tleaves, tcounts, n_tleaves,
+                                          scell_count, levels,
+                                          reinterpret_cast<unsigned long long *>(total));
+  return check_launch("near_count_kernel");
+}
+
+extern "C" int bfmm_scatter_output(const double *far_sorted,
+                                   const double *near_sorted,
+                                   const int64_t *perm, int64_t n, int m,
+                                   double *phi, int32_t *nonfinite_flag,
+                                   bfmm_stream_t stream) {
+  if (n == 0) return 0;
+  const int64_t total = n * m;
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 32);
+  scatter_kernel<<<grid, 256, 0, as_stream(stream)>>>(far_sorted, near_sorted,
+                                                      perm, n, m, phi,
+                                                      nonfinite_flag);
+  return check_launch("scatter_kernel");
+}

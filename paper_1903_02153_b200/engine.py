@@ -1,0 +1,466 @@
+"""GPU FMM evaluator — drop-in for the reference FmmEvaluator (engine.py:126-545).
+
+Same constructor, same ``evaluate(sources, targets=None, weights=None)``,
+same exceptions and ``timings`` keys.  Every stage of the matvec runs on
+the GPU through libbfmm.so (include/bfmm.h); PyTorch only allocates device
+memory and provides the stream.  There is no CPU fallback: without a CUDA
+device or without the library the constructor raises NativeLibraryError.
+
+Inputs may be NumPy arrays (result is a NumPy array, like the reference)
+or torch tensors (result is a tensor on the input's device; CUDA tensors
+skip every host<->device copy).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigurationError, DomainError, KernelEvaluationError, NativeLibraryError
+from .interp import device_interp_blob, half_interval_matrices
+from .kernel import KernelSpec
+from .plan import FmmPlan, SchemeKind
+from .tables import ChebyshevLevelBlock, M2LTable, neighbor_offsets, precompute_m2l
+
+_KIND = {"r": 0, "r2": 1, "diff": 2}
+_ST_DOMAIN_SRC, _ST_DOMAIN_TGT, _ST_REF, _ST_NONFINITE, _ST_WEIGHTS = 0, 1, 2, 3, 4
+
+
+def _torch():
+    try:
+        import torch
+    except Exception as e:  # pragma: no cover
+        raise NativeLibraryError(f"PyTorch is required for device memory: {e}")
+    return torch
+
+
+def _pad8(r: int) -> int:
+    return (r + 7) // 8 * 8
+
+
+@dataclass
+class _Tree:
+    """A point set binned by leaf on the device (reference _Partition)."""
+    n: int
+    perm: object
+    pts4: object
+    leaves: object
+    starts: object
+    counts: object
+    n_leaves: object
+    cell_start: object
+    cell_count: object
+    max_leaves: int
+
+
+class FmmEvaluator:
+    """A plan bound to its kernel functor and device-resident M2L tables."""
+
+    def __init__(self, kernel: KernelSpec, plan: FmmPlan, cache_dir=None,
+                 threads: int = 1, table: M2LTable = None, use_cache: bool = True,
+                 device=None):
+        if not isinstance(kernel, KernelSpec):
+            raise ConfigurationError("kernel must be a KernelSpec")
+        if not kernel.has_device_form:
+            raise ConfigurationError(
+                f"kernel {kernel.name!r} has no device form: give KernelSpec a "
+                "cuda_expr (there is no CPU fallback for the near field)")
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise NativeLibraryError("no CUDA device is visible; the FMM matvec runs on the GPU only")
+        self.lib = _native.load()
+        self.kernel = kernel
+        self.plan = plan
+        self.threads = max(1, int(threads))
+        self.device = torch.device(device if device is not None else "cuda")
+        t0 = time.perf_counter()
+        p, sch = plan.order, plan.scheme
+        self._H = np.ascontiguousarray(half_interval_matrices(p, sch))
+        self._interp = device_interp_blob(p, sch)
+        self._scheme_id = 0 if sch is SchemeKind.CHEBYSHEV else 1
+        self.transfers_factors = self._H
+        self.tree_seconds = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        if table is None:
+            table = precompute_m2l(kernel, plan, cache_dir=cache_dir, threads=self.threads,
+                                   use_cache=use_cache)
+        self.table = table
+        self._upload_tables()
+        self.table_seconds = time.perf_counter() - t0
+        self.precompute_seconds = self.tree_seconds + self.table_seconds
+        self._handle = self._kernel_handle()
+        self.timings = {}
+        self._disable_far_field = False
+        self.keep_stages = False
+        self.stages = {}
+
+    # -- setup --------------------------------------------------------------
+    def _kernel_handle(self) -> int:
+        k = self.kernel
+        if k.builtin_id:
+            return int(k.builtin_id)
+        h = _native.C.c_int(0)
+        _native.check(self.lib.bfmm_kernel_compile(_KIND[k.cuda_arg], k.cuda_expr.encode(),
+                                                   _native.C.byref(h)),
+                      f"NVRTC compile of kernel {k.name!r}")
+        return int(h.value)
+
+    def _upload_tables(self):
+        torch = _torch()
+        dev = self.device
+        self._dev_blocks = {}
+        for key, blk in self.table.blocks.items():
+            if isinstance(blk, ChebyshevLevelBlock):
+                p3, r = blk.u.shape
+                rp = _pad8(r)
+                V = np.zeros((p3, rp))
+                V[:, :r] = blk.v
+                UT = np.zeros((rp, p3))
+                UT[:r] = blk.u.T
+                CT = np.zeros((blk.cores.shape[0], rp, rp))
+                CT[:, :r, :r] = blk.cores.transpose(0, 2, 1)
+                self._dev_blocks[key] = {
+                    "kind": "cheb", "r": r, "rp": rp,
+                    "V": torch.from_numpy(V).to(dev),
+                    "UT": torch.from_numpy(UT).to(dev),
+                    "coresT": torch.from_numpy(np.ascontiguousarray(CT)).to(dev),
+                }
+            else:
+                sym = np.ascontiguousarray(blk.symbols).view(np.float64)
+                self._dev_blocks[key] = {"kind": "fft",
+                                         "symbols": torch.from_numpy(sym.copy()).to(dev)}
+
+    def _dev_block(self, level):
+        return self._dev_blocks[0] if self.table.single_level else self._dev_blocks[level]
+
+    # -- helpers --------------------------------------------------------------
+    @staticmethod
+    def _stream():
+        torch = _torch()
+        return _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _prepare_points(self, arr, name):
+        torch = _torch()
+        if isinstance(arr, torch.Tensor):
+            if arr.ndim != 2 or arr.shape[1] != 3:
+                raise ConfigurationError(f"{name} must be an (N, 3) array, got shape {tuple(arr.shape)}")
+            return arr.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous()
+        pts = np.ascontiguousarray(arr, dtype=np.float64)
+        if pts.ndim != 2 or pts.shape[1] != 3:
+            raise ConfigurationError(f"{name} must be an (N, 3) array, got shape {np.shape(arr)}")
+        return torch.from_numpy(pts).to(self.device, non_blocking=True)
+
+    def _prepare_weights(self, w, n_src):
+        torch = _torch()
+        if w is None:
+            raise ConfigurationError("weights are required")
+        if isinstance(w, torch.Tensor):
+            squeeze = w.ndim == 1
+            wt = w[:, None] if squeeze else w
+            if wt.ndim != 2 or wt.shape[0] != n_src:
+                raise ConfigurationError(
+                    f"weights shape {tuple(w.shape)} does not match {n_src} sources")
+            return wt.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous(), squeeze
+        wa = np.ascontiguousarray(w, dtype=np.float64)
+        squeeze = wa.ndim == 1
+        if squeeze:
+            wa = wa[:, None]
+        if wa.ndim != 2 or wa.shape[0] != n_src:
+            raise ConfigurationError(
+                f"weights shape {np.shape(w)} does not match {n_src} sources")
+        return torch.from_numpy(wa).to(self.device, non_blocking=True), squeeze
+
+    def _geom(self):
+        d = self.plan.domain
+        lo, hi = d.low, d.high
+        h = d.length / (1 << self.plan.levels)
+        return np.ascontiguousarray(np.concatenate([lo, hi, [h, 1e-12 * d.length]]))
+
+    def _build_tree(self, pts, status, slot) -> _Tree:
+        torch = _torch()
+        L = self.plan.levels
+        n = int(pts.shape[0])
+        dev = self.device
+        cap = max(n, 1)
+        ncell = 1 << (3 * L)
+        perm = torch.empty(cap, dtype=torch.int64, device=dev)
+        pts4 = torch.empty((cap, 4), dtype=torch.float64, device=dev)
+        leaves = torch.empty(cap, dtype=torch.int64, device=dev)
+        starts = torch.empty(cap, dtype=torch.int64, device=dev)
+        counts = torch.empty(cap, dtype=torch.int64, device=dev)
+        n_leaves = torch.zeros(1, dtype=torch.int64, device=dev)
+        cell_start = torch.empty(ncell, dtype=torch.int32, device=dev)
+        cell_count = torch.empty(ncell, dtype=torch.int32, device=dev)
+        sb = self.lib.bfmm_tree_scratch_bytes(n, L)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        geom = self._geom()
+        _native.check(self.lib.bfmm_tree_build(
+            pts.data_ptr(), n, _native.dptr(geom), L, scratch.data_ptr(), sb,
+            perm.data_ptr(), pts4.data_ptr(), leaves.data_ptr(), starts.data_ptr(),
+            counts.data_ptr(), n_leaves.data_ptr(), cell_start.data_ptr(),
+            cell_count.data_ptr(), status[slot:].data_ptr(), self._stream()), "bfmm_tree_build")
+        return _Tree(n, perm, pts4, leaves, starts, counts, n_leaves, cell_start,
+                     cell_count, min(n, ncell))
+
+    # -- stages -----------------------------------------------------------------
+    def _upward(self, tree, ws, m, status):
+        torch = _torch()
+        L, p = self.plan.levels, self.plan.order
+        p3 = p ** 3
+        moments = {L: torch.zeros(((1 << (3 * L)) * m * p3,), dtype=torch.float64, device=self.device)}
+        st = self._stream()
+        leaf_geom = np.ascontiguousarray(np.concatenate([self.plan.domain.low,
+                                                         [self.plan.domain.length / (1 << L)]]))
+        _native.check(self.lib.bfmm_p2m(
+            tree.pts4.data_ptr(), ws.data_ptr(), m, tree.leaves.data_ptr(),
+            tree.starts.data_ptr(), tree.counts.data_ptr(), tree.n_leaves.data_ptr(),
+            tree.max_leaves, L, p, self._scheme_id, _native.dptr(self._interp),
+            _native.dptr(leaf_geom), moments[L].data_ptr(), status[_ST_REF:].data_ptr(), st),
+            "bfmm_p2m")
+        for lev in range(L, 2, -1):
+            npar = 1 << (3 * (lev - 1))
+            moments[lev - 1] = torch.empty((npar * m * p3,), dtype=torch.float64, device=self.device)
+            _native.check(self.lib.bfmm_m2m(moments[lev].data_ptr(), moments[lev - 1].data_ptr(),
+                                            npar, p, m, _native.dptr(self._H), st), "bfmm_m2m")
+        return moments, leaf_geom
+
+    def _far_field(self, moments, m):
+        torch = _torch()
+        L, p = self.plan.levels, self.plan.order
+        p3 = p ** 3
+        st = self._stream()
+        locs = {}
+        for lev in range(2, L + 1):
+            blk = self._dev_block(lev)
+            scale = float(self.table.scale_for_level(lev))
+            ncell = 1 << (3 * lev)
+            out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
+            if blk["kind"] == "cheb":
+                rp = blk["rp"]
+                z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
+                lt = torch.empty_like(z)
+                _native.check(self.lib.bfmm_rows_gemm(moments[lev].data_ptr(), ncell * m, p3,
+                                                      blk["V"].data_ptr(), rp, z.data_ptr(),
+                                                      1.0, 0.0, st), "bfmm_rows_gemm(V)")
+                _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp,
+                                                     blk["coresT"].data_ptr(), st), "bfmm_m2l_cheb")
+                _native.check(self.lib.bfmm_rows_gemm(lt.data_ptr(), ncell * m, rp,
+                                                      blk["UT"].data_ptr(), p3, out.data_ptr(),
+                                                      scale, 0.0, st), "bfmm_rows_gemm(U)")
+            else:
+                nb = _native.C.c_size_t(0)
+                _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, m, p, _native.C.byref(nb)),
+                              "bfmm_m2l_fft_scratch_bytes")
+                scratch = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=self.device)
+                _native.check(self.lib.bfmm_m2l_fft(moments[lev].data_ptr(), out.data_ptr(), lev, m,
+                                                    p, blk["symbols"].data_ptr(), scale,
+                                                    scratch.data_ptr(), int(nb.value), st),
+                              "bfmm_m2l_fft")
+            locs[lev] = out
+        return locs
+
+    def _downward(self, locs, tree, m, leaf_geom, status, phi_far):
+        L, p = self.plan.levels, self.plan.order
+        st = self._stream()
+        for lev in range(2, L):
+            _native.check(self.lib.bfmm_l2l(locs[lev].data_ptr(), locs[lev + 1].data_ptr(),
+                                            1 << (3 * lev), p, m, _native.dptr(self._H), st),
+                          "bfmm_l2l")
+        _native.check(self.lib.bfmm_l2p(
+            tree.pts4.data_ptr(), m, tree.leaves.data_ptr(), tree.starts.data_ptr(),
+            tree.counts.data_ptr(), tree.n_leaves.data_ptr(), tree.max_leaves, L, p,
+            self._scheme_id, _native.dptr(self._interp), _native.dptr(leaf_geom),
+            locs[L].data_ptr(), phi_far.data_ptr(), status[_ST_REF:].data_ptr(), st), "bfmm_l2p")
+
+    def _near_field(self, ttree, stree, ws, m, near):
+        torch = _torch()
+        st = self._stream()
+        sb = self.lib.bfmm_p2p_scratch_bytes(max(ttree.max_leaves, 1))
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        _native.check(self.lib.bfmm_p2p(
+            self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(), ttree.starts.data_ptr(),
+            ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(), ttree.max_leaves,
+            stree.pts4.data_ptr(), ws.data_ptr(), m, stree.cell_start.data_ptr(),
+            stree.cell_count.data_ptr(), self.plan.levels, near.data_ptr(), scratch.data_ptr(),
+            sb, st), "bfmm_p2p")
+
+    # -- driver -----------------------------------------------------------------
+    def evaluate(self, sources, targets=None, weights=None):
+        """phi[i, c] = sum_j K(x_i, y_j) w[j, c] (reference engine.py:482-536)."""
+        torch = _torch()
+        shared = targets is None or targets is sources
+        as_tensor = isinstance(sources, torch.Tensor)
+        out_device = sources.device if as_tensor else None
+        if not as_tensor:
+            # host-side validation mirrors the reference (eng:51-57, 484-497)
+            src_np = np.asarray(sources)
+            _check_host_points(src_np, "sources")
+            if not shared:
+                _check_host_points(np.asarray(targets), "targets")
+            if weights is None:
+                raise ConfigurationError("weights are required")
+            w_np = np.asarray(weights, dtype=np.float64)
+            if w_np.ndim not in (1, 2) or w_np.shape[0] != src_np.shape[0]:
+                raise ConfigurationError(
+                    f"weights shape {np.shape(weights)} does not match {src_np.shape[0]} sources")
+            if w_np.size and not np.all(np.isfinite(w_np)):
+                raise ConfigurationError("weights contain non-finite values")
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        t_host0 = time.perf_counter()
+        ev[0].record()
+        src = self._prepare_points(sources, "sources")
+        tgt = src if shared else self._prepare_points(targets, "targets")
+        w, squeeze = self._prepare_weights(weights, src.shape[0])
+        m = int(w.shape[1])
+        n_src, n_tgt = int(src.shape[0]), int(tgt.shape[0])
+        status = torch.zeros(16, dtype=torch.int32, device=self.device)
+        st = self._stream()
+        ev[1].record()
+        stree = self._build_tree(src, status, _ST_DOMAIN_SRC)
+        ttree = stree if shared else self._build_tree(tgt, status, _ST_DOMAIN_TGT)
+        ws = torch.empty((max(n_src, 1), m), dtype=torch.float64, device=self.device)
+        _native.check(self.lib.bfmm_gather_weights(w.data_ptr(), n_src, m, stree.perm.data_ptr(),
+                                                   ws.data_ptr(), stree.pts4.data_ptr(), st),
+                      "bfmm_gather_weights")
+        ev[2].record()
+        moments, leaf_geom = self._upward(stree, ws, m, status)
+        ev[3].record()
+        phi_far = None
+        if not self._disable_far_field:
+            locs = self._far_field(moments, m)
+            ev[4].record()
+            phi_far = torch.empty((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
+            self._downward(locs, ttree, m, leaf_geom, status, phi_far)
+        else:
+            locs = None
+            ev[4].record()
+        ev[5].record()
+        near = torch.empty((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
+        self._near_field(ttree, stree, ws, m, near)
+        phi = torch.empty((n_tgt, m), dtype=torch.float64, device=self.device)
+        _native.check(self.lib.bfmm_scatter_output(
+            phi_far.data_ptr() if phi_far is not None else None, near.data_ptr(),
+            ttree.perm.data_ptr(), n_tgt, m, phi.data_ptr(), status[_ST_NONFINITE:].data_ptr(), st),
+            "bfmm_scatter_output")
+        pairs_dev = status.view(torch.int64)[4:5]
+        _native.check(self.lib.bfmm_near_pair_count(
+            ttree.leaves.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
+            ttree.max_leaves, stree.cell_count.data_ptr(), self.plan.levels,
+            pairs_dev.data_ptr(), st), "bfmm_near_pair_count")
+        ev[6].record()
+        if self.keep_stages:
+            self.stages = {"stree": stree, "ttree": ttree, "moments": moments, "locals": locs,
+                           "near": near, "far": phi_far, "ws": ws}
+        stat = status.cpu().numpy()  # the one synchronising read-back
+        self._raise_flags(stat, ttree, stree)
+        if as_tensor:
+            result = phi if out_device.type == "cuda" else phi.to(out_device)
+        else:
+            result = phi.cpu().numpy()
+        total_host = time.perf_counter() - t_host0
+        ms = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(6)]
+        self.timings = {
+            "upload": ms[0], "distribute": ms[1], "upward": ms[2],
+            "far_field": ms[3] if not self._disable_far_field else 0.0,
+            "downward": ms[4] if not self._disable_far_field else 0.0,
+            "near_field": ms[5], "near_pairs": int(stat.view(np.int64)[4]),
+        }
+        self.timings["total"] = sum(v for k, v in self.timings.items()
+                                    if k not in ("near_pairs", "upload"))
+        self.timings["wall"] = total_host
+        return result[:, 0] if squeeze else result
+
+    def _raise_flags(self, stat, ttree, stree):
+        if stat[_ST_DOMAIN_SRC] & 2 or stat[_ST_DOMAIN_TGT] & 2:
+            raise DomainError("points contain non-finite coordinates")
+        if stat[_ST_DOMAIN_SRC] or stat[_ST_DOMAIN_TGT]:
+            d = self.plan.domain
+            raise DomainError(f"a point lies outside the box centered at {d.center} "
+                              f"with length {d.length}")
+        if stat[_ST_REF]:
+            raise DomainError("a point landed outside its leaf cell; the tree assignment is inconsistent")
+        if stat[_ST_NONFINITE]:
+            self._locate_nonfinite(ttree, stree)
+
+    def _locate_nonfinite(self, ttree, stree):
+        torch = _torch()
+        key = torch.full((1,), -1, dtype=torch.int64, device=self.device)
+        _native.check(self.lib.bfmm_p2p_locate(
+            self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(), ttree.starts.data_ptr(),
+            ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(), ttree.max_leaves,
+            stree.pts4.data_ptr(), stree.cell_start.data_ptr(), stree.cell_count.data_ptr(),
+            self.plan.levels, key.data_ptr(), self._stream()), "bfmm_p2p_locate")
+        k = int(key.cpu().numpy().view(np.uint64)[0])
+        if k == 0xFFFFFFFFFFFFFFFF:
+            raise KernelEvaluationError(
+                f"kernel {self.kernel.name!r} produced a non-finite near-field sum")
+        trow, srow = (k >> 29) & ((1 << 29) - 1), k & ((1 << 29) - 1)
+        ti = int(ttree.perm[trow].item())
+        si = int(stree.perm[srow].item())
+        x = ttree.pts4[trow, :3].cpu().numpy()
+        y = stree.pts4[srow, :3].cpu().numpy()
+        raise KernelEvaluationError(
+            f"kernel {self.kernel.name!r} returned a non-finite value for "
+            f"target {ti} and source {si}", x=x, y=y, indices=(ti, si))
+
+    # -- diagnostics used by the parity tests -------------------------------------
+    def partition(self, points):
+        """The device tree of a point set as NumPy arrays (perm, leaves,
+        starts, counts), comparable with the reference _Partition."""
+        torch = _torch()
+        pts = self._prepare_points(points, "points")
+        status = torch.zeros(16, dtype=torch.int32, device=self.device)
+        tr = self._build_tree(pts, status, 0)
+        nl = int(tr.n_leaves.item())
+        if status[0].item():
+            raise DomainError("a point lies outside the domain box")
+        return {"perm": tr.perm[:tr.n].cpu().numpy(), "leaves": tr.leaves[:nl].cpu().numpy(),
+                "starts": tr.starts[:nl].cpu().numpy(), "counts": tr.counts[:nl].cpu().numpy(),
+                "tree": tr}
+
+    def far_pairs(self, level, t_index):
+        torch = _torch()
+        n3 = 1 << (3 * level)
+        tg = torch.empty(n3, dtype=torch.int64, device=self.device)
+        sr = torch.empty(n3, dtype=torch.int64, device=self.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        sb = self.lib.bfmm_far_pairs_scratch_bytes(level)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        _native.check(self.lib.bfmm_far_pairs(level, t_index, tg.data_ptr(), sr.data_ptr(),
+                                              cnt.data_ptr(), scratch.data_ptr(), sb,
+                                              self._stream()), "bfmm_far_pairs")
+        c = int(cnt.item())
+        return tg[:c].cpu().numpy(), sr[:c].cpu().numpy()
+
+    def near_segments(self, points, t_index):
+        torch = _torch()
+        tr = self.partition(points)["tree"]
+        out = torch.empty(max(tr.max_leaves, 1), dtype=torch.int64, device=self.device)
+        _native.check(self.lib.bfmm_near_pairs(self.plan.levels, t_index, tr.leaves.data_ptr(),
+                                               tr.n_leaves.data_ptr(), tr.max_leaves,
+                                               tr.leaves.data_ptr(), tr.n_leaves.data_ptr(),
+                                               out.data_ptr(), self._stream()), "bfmm_near_pairs")
+        nl = int(tr.n_leaves.item())
+        o = out[:nl].cpu().numpy()
+        tseg = np.nonzero(o >= 0)[0]
+        return tseg, o[tseg]
+
+
+def _check_host_points(pts, name):
+    if pts.ndim != 2 or pts.shape[1] != 3:
+        raise ConfigurationError(f"{name} must be an (N, 3) array, got shape {np.shape(pts)}")
+    if pts.size and not np.all(np.isfinite(pts)):
+        raise DomainError(f"{name} contain non-finite coordinates")
+
+
+def evaluate(kernel: KernelSpec, plan: FmmPlan, sources, targets=None, weights=None,
+             cache_dir=None, threads: int = 1, table: M2LTable = None):
+    """One-shot wrapper (reference engine.py:539-545)."""
+    ev = FmmEvaluator(kernel, plan, cache_dir=cache_dir, threads=threads, table=table)
+    return ev.evaluate(sources, targets, weights)
+
+
+__all__ = ["FmmEvaluator", "evaluate", "neighbor_offsets"]

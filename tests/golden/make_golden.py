@@ -1,0 +1,298 @@
+"""Generate golden fixtures by running the REAL reference (boxfmm).
+
+Run in the builder container only (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [case ...]
+
+Each case writes ``tests/golden/<case>.npz``.  Large arrays are stored as
+sha256 digests plus small slices so the fixtures stay small; everything is
+produced by the reference's public API (FmmEvaluator, direct_evaluate,
+Octree, precompute_m2l, ...) at threads=1, which the reference guarantees
+to be bitwise deterministic (pkg/README.md:53-55).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import boxfmm  # noqa: E402
+from boxfmm import engine as reng  # noqa: E402
+from boxfmm.kernel import KernelSpec, kernel_by_name  # noqa: E402
+from boxfmm.octree import BoxDomain, Octree, neighbor_offsets  # noqa: E402
+from boxfmm.operators import offset_set, precompute_m2l  # noqa: E402
+from boxfmm.plan import FmmPlan  # noqa: E402
+
+from paper_1903_02153_b200 import workloads  # noqa: E402
+
+CACHE = "/tmp/golden_cache"
+
+
+def ref_kernel(key):
+    if key == "gauss02":
+        return KernelSpec("gauss02", homogen=0.0, symmetry=1,
+                          profile=lambda r: np.exp(-(r / 0.2) ** 2))
+    if key == "exp03":
+        return KernelSpec("exp03", homogen=0.0, symmetry=1,
+                          profile=lambda r: np.exp(-r / 0.3))
+    return kernel_by_name(key)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def save(case, **arrays):
+    path = os.path.join(HERE, f"{case}.npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def plan_of(wl):
+    return FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"],
+                   eps=wl["eps"], domain_center=wl["center"],
+                   domain_length=wl["length"], n_cols=wl["ncols"])
+
+
+def unit_cloud(n, seed=0, ncols=1):
+    gen = np.random.default_rng(seed)
+    return gen.random((n, 3)), gen.standard_normal((n, ncols))
+
+
+def small_plan(levels=3, order=4, scheme="chebyshev", eps=1e-6):
+    return FmmPlan(levels=levels, order=order, scheme=scheme, eps=eps,
+                   domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+
+
+# ---------------------------------------------------------------------------
+
+def case_tree():
+    out = {}
+    for tag, name, scale in (("c1", "C1", 0), ("c4s2", "C4", 2), ("c2s1", "C2", 1)):
+        wl = workloads.make(name, scale)
+        tree = Octree(BoxDomain(wl["center"], wl["length"]), wl["levels"])
+        part = reng._Partition.build(tree, wl["points"])
+        out[f"{tag}_perm_sha"] = sha(part.perm.astype(np.int64))
+        out[f"{tag}_leaves"] = part.leaves
+        out[f"{tag}_starts"] = part.starts
+        out[f"{tag}_counts"] = part.counts
+        out[f"{tag}_center"] = np.array(wl["center"])
+        out[f"{tag}_length"] = np.array(wl["length"])
+        if tag == "c1":
+            out["c1_perm"] = part.perm.astype(np.int32)
+    # the half-open / closed-face conventions (T/test_octree.py:86-100)
+    tree = Octree(BoxDomain((0.5, 0.5, 0.5), 1.0), 2)
+    faces = np.array([[0.0, 0.0, 0.0], [0.25, 0.0, 0.0], [1.0, 1.0, 1.0],
+                      [0.5, 0.75, 0.25], [1.0 + 5e-13, 0.0, 0.0]])
+    out["faces_pts"] = faces
+    out["faces_ids"] = tree.leaf_index(faces)
+    save("tree", **out)
+
+
+def case_lists():
+    out = {}
+    dom = BoxDomain((0.0, 0.0, 0.0), 2.0)
+    for lev in (2, 3, 4, 5):
+        tree = Octree(dom, max(lev, 2))
+        tg_all, sr_all, counts = [], [], []
+        for t in offset_set():
+            tg, sr = tree.cell_pairs_for_offset(lev, tuple(t))
+            tg_all.append(tg)
+            sr_all.append(sr)
+            counts.append(len(tg))
+        tg_all = np.concatenate(tg_all)
+        sr_all = np.concatenate(sr_all)
+        out[f"l{lev}_counts"] = np.array(counts)
+        out[f"l{lev}_tg_sha"] = sha(tg_all)
+        out[f"l{lev}_sr_sha"] = sha(sr_all)
+        if lev <= 3:
+            out[f"l{lev}_tg"] = tg_all.astype(np.int32)
+            out[f"l{lev}_sr"] = sr_all.astype(np.int32)
+    out["offsets"] = offset_set()
+    out["near_offsets"] = neighbor_offsets()
+    # near-field segments for C1 (eng:401-417)
+    wl = workloads.make("C1")
+    plan = plan_of(wl)
+    ev = reng.FmmEvaluator(ref_kernel(wl["kernel"]), plan, cache_dir=CACHE)
+    part = reng._Partition.build(ev.tree, wl["points"])
+    ts, ss, cnt = [], [], []
+    for t in neighbor_offsets():
+        a, b = ev._neighbor_segments(part, part, tuple(t))
+        ts.append(a)
+        ss.append(b)
+        cnt.append(len(a))
+    out["c1_near_tseg"] = np.concatenate(ts).astype(np.int32)
+    out["c1_near_sseg"] = np.concatenate(ss).astype(np.int32)
+    out["c1_near_counts"] = np.array(cnt)
+    # interaction list counts (T/test_octree.py:110-116)
+    save("lists", **out)
+
+
+def case_tables():
+    out = {}
+    probe = [(2, 0, 0), (3, -1, 2), (-2, 3, 1), (-3, -3, -3), (0, 0, 2)]
+    out["probe_offsets"] = np.array(probe)
+    specs = {
+        "c1": ("C1", None),
+        "c2": ("C2", None),
+        "c4": ("C4", None),
+        "c5": ("C5", None),
+        "c3": ("C3", None),
+    }
+    for tag, (name, _) in specs.items():
+        wl = workloads.make(name, 0 if name != "C4" else 0, n_override=8)
+        if name == "C4":
+            wl["center"], wl["length"] = (0.04243, 0.00945, -0.01194), 2.14973
+        plan = plan_of(wl)
+        t0 = time.perf_counter()
+        table = precompute_m2l(ref_kernel(wl["kernel"]), plan, use_cache=False)
+        print(tag, "table", time.perf_counter() - t0, "s")
+        out[f"{tag}_single"] = np.array(table.single_level)
+        out[f"{tag}_nbytes"] = np.array(table.nbytes())
+        levs = sorted(table.blocks)
+        out[f"{tag}_levels"] = np.array(levs)
+        for lev in levs:
+            blk = table.blocks[lev]
+            if hasattr(blk, "u"):
+                out[f"{tag}_rank_{lev}"] = np.array(blk.rank)
+        big = plan.order ** 3 > 125
+        for lev in ((3,) if big else (2, 3, 4)):
+            out[f"{tag}_dense_{lev}"] = np.stack([table.dense(t, lev)
+                                                 for t in (probe[:2] if big else probe)])
+    # a small table kept whole for element-wise pins (p=3, symmetric 1/r)
+    plan = FmmPlan(levels=3, order=3, scheme="chebyshev", eps=1e-7)
+    table = precompute_m2l(kernel_by_name("laplacian"), plan, use_cache=False)
+    blk = table.blocks[0]
+    out["p3_u"] = blk.u
+    out["p3_cores"] = blk.cores
+    # non-symmetric + antisymmetric kernels (T/test_operators.py:92-116)
+    def dipole(dx, dy, dz):
+        r2 = dx * dx + dy * dy + dz * dz
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = dx / (r2 * np.sqrt(r2))
+        return np.where(r2 == 0, 0.0, v)
+    kd = KernelSpec(name="xdipole", diff_func=dipole, symmetry=-1, homogen=-2.0)
+    plan = FmmPlan(levels=2, order=3, scheme="chebyshev", eps=1e-7)
+    td = precompute_m2l(kd, plan, use_cache=False)
+    out["dipole_rank"] = np.array(td.blocks[0].rank)
+    out["dipole_dense"] = np.stack([td.dense(t, 2) for t in probe])
+    ks = KernelSpec(name="skew", diff_func=lambda dx, dy, dz: np.exp(-(dx + 2 * dy) ** 2 - dz * dz),
+                    symmetry=0)
+    plan = FmmPlan(levels=2, order=3, scheme="chebyshev", eps=1e-7)
+    tsk = precompute_m2l(ks, plan, use_cache=False)
+    out["skew_rank"] = np.array(tsk.blocks[2].rank)
+    out["skew_dense"] = np.stack([tsk.dense(t, 2) for t in probe])
+    save("tables", **out)
+
+
+def _run(kernel, plan, pts, w, targets=None, threads=1):
+    ev = reng.FmmEvaluator(kernel, plan, cache_dir=CACHE, threads=threads)
+    t0 = time.perf_counter()
+    phi = ev.evaluate(pts, targets=targets, weights=w)
+    return phi, time.perf_counter() - t0, ev
+
+
+def case_engine():
+    """Small engine fixtures mirroring T/test_engine.py."""
+    out = {}
+    pts, w = unit_cloud(1500, seed=42)
+    out["cloud1500_pts"] = pts
+    out["cloud1500_w"] = w
+    for name in sorted(boxfmm.BUILTIN_KERNELS):
+        for scheme in ("chebyshev", "uniform"):
+            phi, _, _ = _run(kernel_by_name(name), small_plan(scheme=scheme), pts, w)
+            out[f"phi_{name}_{scheme}"] = phi
+        out[f"direct_{name}"] = reng.direct_evaluate(kernel_by_name(name), pts, weights=w)
+    # distinct targets + wide columns
+    pts2, w2 = unit_cloud(1200, seed=7)
+    tg = np.random.default_rng(8).random((300, 3))
+    out["tgt_src"], out["tgt_w"], out["tgt_t"] = pts2, w2[:, 0], tg
+    out["tgt_phi"], _, _ = _run(kernel_by_name("laplacian"), small_plan(), pts2, w2[:, 0], tg)
+    # multi-column
+    pts3, _ = unit_cloud(800, seed=10)
+    for nc in (4, 20):
+        w3 = np.random.default_rng(11).standard_normal((800, nc))
+        out[f"mc{nc}_w"] = w3
+        out[f"mc{nc}_phi"], _, _ = _run(kernel_by_name("laplacian"), small_plan(), pts3, w3)
+    out["mc_pts"] = pts3
+    # order sweep (T/test_engine.py:202-214)
+    pts4, w4 = unit_cloud(1200, seed=17)
+    out["ord_pts"], out["ord_w"] = pts4, w4
+    for p in (2, 4, 6):
+        plan = FmmPlan(levels=3, order=p, scheme="chebyshev", eps=1e-10,
+                       domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+        out[f"ord{p}_phi"], _, _ = _run(kernel_by_name("laplacian"), plan, pts4, w4)
+    # uniform per-level with higher order, exp kernel, 3 columns, L=4
+    pts5, w5 = unit_cloud(4000, seed=21, ncols=3)
+    plan = FmmPlan(levels=4, order=5, scheme="uniform", eps=1e-6,
+                   domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    out["u4_pts"], out["u4_w"] = pts5, w5
+    out["u4_phi"], _, _ = _run(kernel_by_name("exponential"), plan, pts5, w5)
+    # non-symmetric (diff_func) kernel, Chebyshev, distinct U/V
+    ks = KernelSpec(name="skew", diff_func=lambda dx, dy, dz: np.exp(-(dx + 2 * dy) ** 2 - dz * dz),
+                    symmetry=0)
+    pts6, w6 = unit_cloud(2000, seed=23)
+    plan = FmmPlan(levels=3, order=4, scheme="chebyshev", eps=1e-7,
+                   domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    out["skew_pts"], out["skew_w"] = pts6, w6
+    out["skew_phi"], _, _ = _run(ks, plan, pts6, w6)
+    save("engine", **out)
+
+
+def case_config(name, scale, direct=True, threads=1):
+    wl = workloads.make(name, scale)
+    kernel = ref_kernel(wl["kernel"])
+    plan = plan_of(wl)
+    w = wl["weights"]
+    reng.FmmEvaluator(kernel, plan, cache_dir=CACHE)  # warm the table cache
+    phi, secs, ev = _run(kernel, plan, wl["points"], w, threads=threads)
+    idx = wl["check_idx"]
+    out = {"phi_idx": phi[idx], "phi_norm": np.array(np.linalg.norm(phi)),
+           "phi_sum": np.array(phi.sum(axis=0)), "seconds": np.array(secs),
+           "threads": np.array(threads),
+           "timings": np.array([ev.timings[k] for k in
+                                ("distribute", "upward", "far_field", "downward",
+                                 "near_field", "near_pairs", "total")])}
+    if wl["points"].shape[0] <= 20_000:
+        out["phi"] = phi
+    if direct:
+        t0 = time.perf_counter()
+        d = reng.direct_evaluate(kernel, wl["points"], targets=wl["points"][idx], weights=w)
+        out["direct_idx"] = d
+        out["direct_seconds"] = np.array(time.perf_counter() - t0)
+        out["rel_l2_vs_direct"] = np.array(np.linalg.norm(phi[idx] - d) / np.linalg.norm(d))
+        print(name, scale, "rel l2 vs direct", float(out["rel_l2_vs_direct"]))
+    print(name, scale, "evaluate", secs, "s", ev.timings)
+    save(f"{name.lower()}_s{scale}", **out)
+
+
+CASES = {
+    "tree": case_tree,
+    "lists": case_lists,
+    "tables": case_tables,
+    "engine": case_engine,
+    "c1": lambda: case_config("C1", 0),
+    "c2s1": lambda: case_config("C2", 1),
+    "c3s2": lambda: case_config("C3", 2),
+    "c4s2": lambda: case_config("C4", 2),
+    "c5s3": lambda: case_config("C5", 3),
+    "c2": lambda: case_config("C2", 0, threads=8),
+    "c5s2": lambda: case_config("C5", 2, threads=8),
+    "c3s1": lambda: case_config("C3", 1, threads=8),
+    "c4s1": lambda: case_config("C4", 1, threads=8),
+}
+
+if __name__ == "__main__":
+    for c in (sys.argv[1:] or ["tree", "lists", "tables", "engine", "c1", "c2s1",
+                               "c3s2", "c4s2", "c5s3"]):
+        t0 = time.perf_counter()
+        CASES[c]()
+        print(f"case {c}: {time.perf_counter() - t0:.1f}s", flush=True)

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through libbfmm.so) against the golden
+fixtures of the real reference and against the CPU oracle.
+
+Bars (BASELINE.json north_star): tree and lists bit-exact; phi within
+relative L2 1e-10 in FP64 of the reference's own output.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2, small_plan, unit_cloud
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1903_02153_b200 as bf  # noqa: E402
+from paper_1903_02153_b200 import workloads  # noqa: E402
+from paper_1903_02153_b200.kernel import workload_kernel  # noqa: E402
+from oracle import fmm_oracle as O  # noqa: E402
+
+PHI_TOL = 1e-10
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def plan_of(wl):
+    return bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"],
+                      eps=wl["eps"], domain_center=wl["center"], domain_length=wl["length"],
+                      n_cols=wl["ncols"])
+
+
+@pytest.fixture(scope="module")
+def c1_eval(tmp_path_factory):
+    wl = workloads.make("C1")
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl),
+                         cache_dir=str(tmp_path_factory.mktemp("c")))
+    return wl, ev
+
+
+# ---------------------------------------------------------------------------
+# tree + lists: bit-exact
+
+@pytest.mark.parametrize("tag,name,scale", [("c1", "C1", 0), ("c4s2", "C4", 2), ("c2s1", "C2", 1)])
+def test_partition_bit_exact(tag, name, scale, cache_dir):
+    g = golden("tree")
+    wl = workloads.make(name, scale)
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
+    part = ev.partition(wl["points"])
+    assert sha(part["perm"].astype(np.int64)) == str(g[f"{tag}_perm_sha"])
+    assert np.array_equal(part["leaves"], g[f"{tag}_leaves"])
+    assert np.array_equal(part["starts"], g[f"{tag}_starts"])
+    assert np.array_equal(part["counts"], g[f"{tag}_counts"])
+    if tag == "c1":
+        assert np.array_equal(part["perm"], g["c1_perm"].astype(np.int64))
+
+
+def test_partition_face_conventions(cache_dir):
+    g = golden("tree")
+    plan = bf.FmmPlan(levels=2, order=2, domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, plan, cache_dir=cache_dir)
+    part = ev.partition(g["faces_pts"])
+    ids = np.empty(len(g["faces_pts"]), np.int64)
+    for leaf, s, c in zip(part["leaves"], part["starts"], part["counts"]):
+        ids[part["perm"][s:s + c]] = leaf
+    assert np.array_equal(ids, g["faces_ids"])
+    with pytest.raises(bf.DomainError):
+        ev.partition(np.array([[1.1, 0.5, 0.5]]))
+
+
+@pytest.mark.parametrize("lev", [2, 3, 4, 5])
+def test_far_lists_bit_exact(lev, c1_eval):
+    g = golden("lists")
+    _, ev = c1_eval
+    tgs, srs = [], []
+    for j in range(316):
+        tg, sr = ev.far_pairs(lev, j)
+        tgs.append(tg)
+        srs.append(sr)
+    assert np.array_equal([len(a) for a in tgs], g[f"l{lev}_counts"])
+    assert sha(np.concatenate(tgs)) == str(g[f"l{lev}_tg_sha"])
+    assert sha(np.concatenate(srs)) == str(g[f"l{lev}_sr_sha"])
+    if lev <= 3:
+        assert np.array_equal(np.concatenate(tgs), g[f"l{lev}_tg"].astype(np.int64))
+
+
+def test_near_lists_bit_exact(c1_eval):
+    g = golden("lists")
+    wl, ev = c1_eval
+    ts, ss = [], []
+    for t in range(27):
+        a, b = ev.near_segments(wl["points"], t)
+        ts.append(a)
+        ss.append(b)
+    assert np.array_equal([len(a) for a in ts], g["c1_near_counts"])
+    assert np.array_equal(np.concatenate(ts), g["c1_near_tseg"].astype(np.int64))
+    assert np.array_equal(np.concatenate(ss), g["c1_near_sseg"].astype(np.int64))
+
+
+# ---------------------------------------------------------------------------
+# phi parity against the reference's own outputs
+
+def test_c1_phi_matches_reference(c1_eval):
+    g = golden("c1_s0")
+    wl, ev = c1_eval
+    phi = ev.evaluate(wl["points"], weights=wl["weights"])
+    assert rel_l2(phi, g["phi"]) < PHI_TOL
+    acc = rel_l2(phi[wl["check_idx"]], g["direct_idx"])
+    assert acc <= float(g["rel_l2_vs_direct"]) * 1.01 + 1e-15
+    assert ev.timings["near_pairs"] == int(g["timings"][5])
+
+
+@pytest.mark.parametrize("name", ["laplacian", "laplacianforce", "gaussian", "exponential",
+                                  "logarithm"])
+def test_builtin_kernels_match_reference_chebyshev(name, cache_dir):
+    g = golden("engine")
+    ev = bf.FmmEvaluator(bf.kernel_by_name(name), small_plan(), cache_dir=cache_dir)
+    phi = ev.evaluate(g["cloud1500_pts"], weights=g["cloud1500_w"])
+    assert rel_l2(phi, g[f"phi_{name}_chebyshev"]) < PHI_TOL
+    assert rel_l2(phi, g[f"direct_{name}"]) < 1e-3
+
+
+def test_distinct_targets_match_reference(cache_dir):
+    g = golden("engine")
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
+    got = ev.evaluate(g["tgt_src"], targets=g["tgt_t"], weights=g["tgt_w"])
+    assert got.shape == (300,)
+    assert rel_l2(got, g["tgt_phi"]) < PHI_TOL
+
+
+@pytest.mark.parametrize("nc", [4, 20])
+def test_multi_column_matches_reference(nc, cache_dir):
+    g = golden("engine")
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
+    got = ev.evaluate(g["mc_pts"], weights=g[f"mc{nc}_w"])
+    assert got.shape == (800, nc)
+    assert rel_l2(got, g[f"mc{nc}_phi"]) < PHI_TOL
+    for c in (0, nc - 1):
+        single = ev.evaluate(g["mc_pts"], weights=g[f"mc{nc}_w"][:, c])
+        assert np.max(np.abs(got[:, c] - single)) <= 1e-13 * np.max(np.abs(single))
+
+
+def test_nonsymmetric_kernel_matches_reference(cache_dir):
+    g = golden("engine")
+    ks = bf.KernelSpec(name="skew", diff_func=lambda dx, dy, dz: np.exp(-(dx + 2 * dy) ** 2 - dz * dz),
+                       symmetry=0, cuda_expr="exp(-(dx + 2.0 * dy) * (dx + 2.0 * dy) - dz * dz)",
+                       cuda_arg="diff")
+    plan = bf.FmmPlan(levels=3, order=4, scheme="chebyshev", eps=1e-7,
+                      domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ev = bf.FmmEvaluator(ks, plan, cache_dir=cache_dir)
+    assert rel_l2(ev.evaluate(g["skew_pts"], weights=g["skew_w"]), g["skew_phi"]) < PHI_TOL
+
+
+def test_order_sweep_matches_reference(cache_dir):
+    g = golden("engine")
+    for p in (2, 4, 6):
+        plan = bf.FmmPlan(levels=3, order=p, scheme="chebyshev", eps=1e-10,
+                          domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+        got = bf.FmmEvaluator(bf.LAPLACIAN, plan, cache_dir=cache_dir).evaluate(
+            g["ord_pts"], weights=g["ord_w"])
+        assert rel_l2(got, g[f"ord{p}_phi"]) < PHI_TOL, p
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2)])
+def test_scaled_configs_match_reference(name, scale, cache_dir):
+    g = golden(f"{name.lower()}_s{scale}")
+    wl = workloads.make(name, scale)
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
+    phi = ev.evaluate(wl["points"], weights=wl["weights"])
+    idx = wl["check_idx"]
+    assert rel_l2(phi[idx], g["phi_idx"]) < PHI_TOL
+    assert abs(np.linalg.norm(phi) - float(g["phi_norm"])) <= PHI_TOL * float(g["phi_norm"])
+    acc = rel_l2(phi[idx], g["direct_idx"])
+    assert acc <= float(g["rel_l2_vs_direct"]) * 1.01 + 1e-15
+    assert ev.timings["near_pairs"] == int(g["timings"][5])
+
+
+def test_c2_full_matches_reference(cache_dir):
+    g = golden("c2_s0")
+    wl = workloads.make("C2")
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
+    phi = ev.evaluate(wl["points"], weights=wl["weights"])
+    idx = wl["check_idx"]
+    assert rel_l2(phi[idx], g["phi_idx"]) < PHI_TOL
+    assert rel_l2(phi[idx], g["direct_idx"]) <= float(g["rel_l2_vs_direct"]) * 1.01
+
+
+# ---------------------------------------------------------------------------
+# stage parity against the oracle (moments / locals per level)
+
+def test_stage_moments_and_locals_match_oracle(cache_dir):
+    wl = workloads.make("C2", 2)
+    k = workload_kernel(wl["kernel"])
+    plan = plan_of(wl)
+    ev = bf.FmmEvaluator(k, plan, cache_dir=cache_dir)
+    ev.keep_stages = True
+    phi = ev.evaluate(wl["points"], weights=wl["weights"])
+    orc = O.OracleFMM(k, wl["levels"], wl["order"], wl["scheme"], wl["eps"], wl["center"],
+                      wl["length"], threads=4)
+    ref = orc.matvec(wl["points"], weights=wl["weights"])
+    assert rel_l2(phi, ref) < PHI_TOL
+    p3 = wl["order"] ** 3
+    for lev, mom in orc.stage["M"].items():
+        got = ev.stages["moments"][lev].view(-1, 1, p3).cpu().numpy().transpose(0, 2, 1)
+        assert rel_l2(got, mom) < 1e-12, lev
+
+
+# ---------------------------------------------------------------------------
+# behaviour restated from the reference's engine tests (T/test_engine.py)
+
+def test_single_point_self_interaction_is_zero(cache_dir):
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(levels=2), cache_dir=cache_dir)
+    out = ev.evaluate(np.array([[0.5, 0.5, 0.5]]), weights=np.array([3.0]))
+    assert out.shape == (1,) and out[0] == 0.0
+
+
+def test_constant_kernel_sums_weights(cache_dir):
+    k = bf.KernelSpec(name="flatone", profile=lambda r: np.ones_like(r), symmetry=1,
+                      cuda_expr="1.0", cuda_arg="r2")
+    pts, w = unit_cloud(2000, seed=3)
+    out = bf.FmmEvaluator(k, small_plan(), cache_dir=cache_dir).evaluate(pts, weights=w)
+    assert np.allclose(out, w.sum(), rtol=0, atol=1e-10 * abs(w.sum()))
+
+
+def test_repeat_runs_are_bitwise_identical(cache_dir):
+    pts, w = unit_cloud(1000, seed=5)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
+    assert np.array_equal(ev.evaluate(pts, weights=w), ev.evaluate(pts, weights=w))
+
+
+def test_linearity_in_weights(cache_dir):
+    pts, _ = unit_cloud(900, seed=12)
+    gen = np.random.default_rng(13)
+    u, v = gen.standard_normal(900), gen.standard_normal(900)
+    ev = bf.FmmEvaluator(bf.EXPONENTIAL, small_plan(), cache_dir=cache_dir)
+    lhs = ev.evaluate(pts, weights=2.5 * u - 0.75 * v)
+    rhs = 2.5 * ev.evaluate(pts, weights=u) - 0.75 * ev.evaluate(pts, weights=v)
+    assert np.max(np.abs(lhs - rhs)) / np.max(np.abs(rhs)) < 1e-12
+
+
+def test_far_field_actually_contributes(cache_dir):
+    pts, w = unit_cloud(1500, seed=14)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
+    full = ev.evaluate(pts, weights=w)
+    ev._disable_far_field = True
+    near_only = ev.evaluate(pts, weights=w)
+    ev._disable_far_field = False
+    assert np.max(np.abs(full - near_only)) > 1e-3 * np.max(np.abs(full))
+    orc = O.OracleFMM(bf.LAPLACIAN, 3, 4, "chebyshev", 1e-6, (0.5, 0.5, 0.5), 1.0)
+    orc.disable_far = True
+    assert rel_l2(near_only, orc.matvec(pts, weights=w)) < 1e-13
+
+
+def test_nonfinite_kernel_value_reports_indices(cache_dir):
+    k = bf.KernelSpec(name="rawinv", profile=lambda r: 1.0 / r, homogen=-1.0, symmetry=1,
+                      cuda_expr="1.0 / r", cuda_arg="r")
+    pts, w = unit_cloud(100, seed=16)
+    ev = bf.FmmEvaluator(k, small_plan(levels=2, order=2), cache_dir=cache_dir)
+    with pytest.raises(bf.KernelEvaluationError) as err:
+        ev.evaluate(pts, targets=pts[37:38].copy(), weights=w)
+    assert "target 0" in str(err.value) and "source 37" in str(err.value)
+    assert err.value.indices == (0, 37)
+
+
+def test_rejects_bad_inputs(cache_dir):
+    pts, w = unit_cloud(100, seed=0)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
+    with pytest.raises(bf.ConfigurationError):
+        ev.evaluate(pts)
+    with pytest.raises(bf.ConfigurationError):
+        ev.evaluate(pts, weights=w[:50])
+    bad = w.copy()
+    bad[3] = np.nan
+    with pytest.raises(bf.ConfigurationError):
+        ev.evaluate(pts, weights=bad)
+    out = pts.copy()
+    out[0] = (2.5, 0.5, 0.5)
+    with pytest.raises(bf.DomainError):
+        ev.evaluate(out, weights=w)
+    with pytest.raises(bf.ConfigurationError):
+        ev.evaluate(pts[:, :2], weights=w)
+
+
+def test_device_tensors_round_trip(cache_dir):
+    pts, w = unit_cloud(3000, seed=31)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
+    host = ev.evaluate(pts, weights=w[:, 0])
+    dev = ev.evaluate(torch.from_numpy(pts).cuda(), weights=torch.from_numpy(w[:, 0]).cuda())
+    assert dev.is_cuda and np.array_equal(dev.cpu().numpy(), host)
+
+
+def test_empty_leaves_and_clusters(cache_dir):
+    """Ragged occupancy: most leaves empty, a few crowded (C4-like)."""
+    gen = np.random.default_rng(41)
+    pts = np.clip(0.5 + 0.01 * gen.standard_normal((3000, 3)), 0, 1)
+    pts = np.vstack([pts, gen.random((50, 3))])
+    w = gen.standard_normal(len(pts))
+    plan = bf.FmmPlan(levels=5, order=3, eps=1e-6, domain_center=(0.5, 0.5, 0.5),
+                      domain_length=1.0)
+    got = bf.FmmEvaluator(bf.LAPLACIAN, plan, cache_dir=cache_dir).evaluate(pts, weights=w)
+    ref = O.OracleFMM(bf.LAPLACIAN, 5, 3, "chebyshev", 1e-6, (0.5, 0.5, 0.5), 1.0).matvec(
+        pts, weights=w)
+    assert rel_l2(got, ref) < PHI_TOL

@@ -1,0 +1,178 @@
+"""Host-side logic (CPU only): C-ABI library, plan/kernel validation, the
+M2L table build against the reference's golden tables, cache format."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+import paper_1903_02153_b200 as bf
+from paper_1903_02153_b200 import _native, tables, workloads
+from paper_1903_02153_b200.interp import (child_transfer_matrices, half_interval_matrices,
+                                          interp_matrix_1d)
+from paper_1903_02153_b200.kernel import workload_kernel
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "bfmm.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bfmm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = _native.load()
+    names = header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in _native.SIGNATURES, f"{n} missing from the ctypes signature table"
+    assert lib.bfmm_version() == 1
+    assert lib.bfmm_tree_scratch_bytes(1000, 3) > 0
+
+
+def test_library_reports_config_errors_without_a_gpu():
+    lib = _native.load()
+    rc = lib.bfmm_m2l_cheb(None, None, 3, 1, 13, None, None)  # rp not a multiple of 8
+    assert rc != 0
+    assert b"multiple" in lib.bfmm_last_error()
+
+
+def test_product_has_no_oracle_dependency():
+    pkg = os.path.join(ROOT, "paper_1903_02153_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("ORACLE", ""), f
+
+
+def test_plan_validation():
+    with pytest.raises(bf.ConfigurationError):
+        bf.FmmPlan(levels=1, order=4)
+    with pytest.raises(bf.ConfigurationError):
+        bf.FmmPlan(levels=3, order=13)
+    with pytest.raises(bf.ConfigurationError):
+        bf.FmmPlan(levels=3, order=4, eps=1.5)
+    with pytest.raises(bf.ConfigurationError):
+        bf.FmmPlan(levels=3, order=4, scheme="spline")
+    p = bf.FmmPlan(levels=3, order=4, scheme="UNIFORM", domain_length=2.0)
+    assert p.scheme is bf.SchemeKind.UNIFORM and p.cell_width(3) == 0.25
+    assert bf.suggest_levels(1) == 2 and bf.suggest_levels(100_000) == 4
+
+
+def test_kernel_contract():
+    with pytest.raises(bf.ConfigurationError):
+        bf.KernelSpec(name="")
+    with pytest.raises(bf.ConfigurationError):
+        bf.KernelSpec(name="x")
+    with pytest.raises(bf.ConfigurationError):
+        bf.KernelSpec(name="x", profile=np.exp, symmetry=2)
+    assert bf.LAPLACIAN.evaluate((0, 0, 0), (0, 0, 2)) == 0.5
+    assert bf.LAPLACIAN.values_from_diffs(np.zeros(1), np.zeros(1), np.zeros(1))[0] == 0.0
+    with pytest.raises(bf.KernelEvaluationError):
+        bf.KernelSpec("bad", profile=lambda r: 1.0 / r).evaluate((0, 0, 0), (0, 0, 0))
+    assert all(k.has_device_form for k in bf.BUILTIN_KERNELS.values())
+    assert not bf.KernelSpec("np", profile=np.exp).has_device_form
+    assert workload_kernel("gauss02").has_device_form
+
+
+def test_interpolation_identities():
+    for scheme in (bf.SchemeKind.CHEBYSHEV, bf.SchemeKind.UNIFORM):
+        x = np.linspace(-1, 1, 17)
+        W = interp_matrix_1d(x, 5, scheme)
+        assert np.allclose(W.sum(axis=1), 1.0, atol=1e-13)
+        assert np.allclose(W @ (np.linspace(-1, 1, 5) ** 0), 1.0)
+        T = child_transfer_matrices(4, scheme)
+        H = half_interval_matrices(4, scheme)
+        assert np.allclose(T[5], np.kron(H[1], np.kron(H[0], H[1])))
+
+
+def test_tables_match_reference_golden():
+    g = golden("tables")
+    probe = [tuple(t) for t in g["probe_offsets"]]
+    for tag, name in (("c1", "C1"), ("c2", "C2"), ("c5", "C5"), ("c3", "C3")):
+        wl = workloads.make(name, n_override=8)
+        plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"],
+                          eps=wl["eps"], domain_center=wl["center"], domain_length=wl["length"])
+        t = bf.precompute_m2l(workload_kernel(wl["kernel"]), plan, use_cache=False)
+        assert t.single_level == bool(g[f"{tag}_single"])
+        assert t.nbytes() == int(g[f"{tag}_nbytes"])
+        for lev in g[f"{tag}_levels"]:
+            if f"{tag}_rank_{lev}" in g:
+                assert t.blocks[int(lev)].rank == int(g[f"{tag}_rank_{lev}"])
+        for lev in (2, 3, 4):
+            key = f"{tag}_dense_{lev}"
+            if key not in g:
+                continue
+            for j, off in enumerate(probe[:g[key].shape[0]]):
+                d = t.dense(off, lev)
+                ref = g[key][j]
+                assert np.max(np.abs(d - ref)) <= 1e-11 * np.max(np.abs(ref)), (tag, lev, off)
+
+
+def test_small_table_elementwise_and_mirror():
+    g = golden("tables")
+    plan = bf.FmmPlan(levels=3, order=3, scheme="chebyshev", eps=1e-7)
+    t = bf.precompute_m2l(bf.LAPLACIAN, plan, use_cache=False)
+    blk = t.blocks[0]
+    # singular vectors are unique up to sign: compare the projector and cores through it
+    assert blk.rank == g["p3_u"].shape[1]
+    P = blk.u @ blk.u.T
+    Pr = g["p3_u"] @ g["p3_u"].T
+    assert np.max(np.abs(P - Pr)) < 1e-12
+    for j in (0, 100, 315):
+        a = blk.u @ blk.cores[j] @ blk.u.T
+        b = g["p3_u"] @ g["p3_cores"][j] @ g["p3_u"].T
+        assert np.max(np.abs(a - b)) < 1e-12 * np.max(np.abs(b))
+    for off in [(2, 0, 0), (3, -1, 2)]:
+        assert np.max(np.abs(t.dense(tuple(-c for c in off), 2) - t.dense(off, 2).T)) < 1e-12
+
+
+def test_antisymmetric_and_nonsymmetric_tables():
+    g = golden("tables")
+    probe = [tuple(t) for t in g["probe_offsets"]]
+
+    def dipole(dx, dy, dz):
+        r2 = dx * dx + dy * dy + dz * dz
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = dx / (r2 * np.sqrt(r2))
+        return np.where(r2 == 0, 0.0, v)
+    kd = bf.KernelSpec(name="xdipole", diff_func=dipole, symmetry=-1, homogen=-2.0)
+    td = bf.precompute_m2l(kd, bf.FmmPlan(levels=2, order=3, eps=1e-7), use_cache=False)
+    assert td.blocks[0].rank == int(g["dipole_rank"])
+    for j, off in enumerate(probe):
+        assert np.max(np.abs(td.dense(off, 2) - g["dipole_dense"][j])) < 1e-11
+    ks = bf.KernelSpec(name="skew", diff_func=lambda dx, dy, dz: np.exp(-(dx + 2 * dy) ** 2 - dz * dz))
+    ts = bf.precompute_m2l(ks, bf.FmmPlan(levels=2, order=3, eps=1e-7), use_cache=False)
+    assert ts.blocks[2].rank == int(g["skew_rank"])
+    for j, off in enumerate(probe):
+        assert np.max(np.abs(ts.dense(off, 2) - g["skew_dense"][j])) < 1e-11
+
+
+def test_cache_round_trip_and_corruption(tmp_path):
+    plan = bf.FmmPlan(levels=2, order=3, eps=1e-6)
+    a = bf.precompute_m2l(bf.EXPONENTIAL, plan, cache_dir=str(tmp_path))
+    b = bf.precompute_m2l(bf.EXPONENTIAL, plan, cache_dir=str(tmp_path))
+    assert np.array_equal(a.blocks[2].u, b.blocks[2].u)
+    assert np.array_equal(a.blocks[2].cores, b.blocks[2].cores)
+    f = next(tmp_path.iterdir())
+    assert f.name == "m2l_exponential_chebyshev_p3_L2_e1.000e-06_len1.bin"
+    f.write_bytes(f.read_bytes()[:40])
+    c = bf.precompute_m2l(bf.EXPONENTIAL, plan, cache_dir=str(tmp_path))
+    assert np.array_equal(a.blocks[2].cores, c.blocks[2].cores)
+
+
+def test_uniform_table_fft_equals_dense():
+    plan = bf.FmmPlan(levels=3, order=3, scheme="uniform")
+    t = bf.precompute_m2l(bf.EXPONENTIAL, plan, use_cache=False)
+    for off in [(2, 0, 0), (-3, 1, 2)]:
+        d = tables.dense_m2l(bf.EXPONENTIAL, off, 3, bf.SchemeKind.UNIFORM, plan.cell_width(3))
+        assert np.max(np.abs(t.dense(off, 3) - d)) < 1e-12
+
+
+def test_evaluator_refuses_kernels_without_device_form():
+    k = bf.KernelSpec("hostonly", profile=np.exp)
+    with pytest.raises(bf.ConfigurationError):
+        bf.FmmEvaluator(k, bf.FmmPlan(levels=2, order=2))
