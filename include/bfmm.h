@@ -89,19 +89,25 @@ int bfmm_m2m(const double *child, double *parent, int64_t n_parent, int p,
 /* ---- far field --------------------------------------------------------- */
 
 /* C = alpha * A @ B + beta * C for row-major A (rows, K), B (K, N),
- * C (rows, N).  Used for z = moments @ V and locals = scale * lt @ U^T
- * (engine.py:233, 252-255). */
+ * C (rows, N).  A may be stored as a_splits blocks of K per row
+ * (rows, a_splits, K) that are summed in order on load.  Used for
+ * z = moments @ V and locals = scale * lt @ U^T (engine.py:233, 252-255). */
 int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
-                   int N, double *C, double alpha, double beta,
+                   int N, double *C, double alpha, double beta, int a_splits,
                    bfmm_stream_t stream);
 
 /* M2L Chebyshev (engine.py:228-256): for every cell c at `level` and
- * column, lt[c] = sum over the valid far offsets t of z[c + t] @ coresT[t],
- * with coresT[t][k][i] = C_t[i][k] padded to rp x rp.  The valid offsets
- * per child octant follow octree.py:128-145 and match
- * cell_pairs_for_offset (octree.py:202-221) pair for pair. */
+ * column, lt[c][i] = sum over the valid far offsets t of
+ * sum_k cores[t][i][k] z[c + t][k], cores = C_t zero-padded to rp x rp.
+ * The valid pairs follow octree.py:128-145 and match
+ * cell_pairs_for_offset (octree.py:202-221) pair for pair.  FP64 tensor
+ * cores (mma.sync m8n8k4 f64).  The 189 offsets of each cell are split into
+ * nsplit contiguous ranges written to separate column blocks:
+ * lt has layout (8^level, m, nsplit, rp) and the caller sums the blocks
+ * (bfmm_rows_gemm with a_splits = nsplit does it while projecting). */
+int bfmm_m2l_cheb_splits(int level, int m, int rp);
 int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
-                  const double *coresT, bfmm_stream_t stream);
+                  int nsplit, const double *cores, bfmm_stream_t stream);
 
 /* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
  * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ).  symbols (device)
@@ -198,6 +204,9 @@ int bfmm_near_pair_count(const int64_t *tleaves, const int64_t *tcounts,
 /* Measure the FP64 FMA peak of this device (GFLOP/s) with a DFMA chain
  * kernel (synchronises). */
 int bfmm_device_fp64_probe(double *gflops, bfmm_stream_t stream);
+
+/* Same for the FP64 tensor-core MMA (mma.sync m8n8k4 f64 -> DMMA). */
+int bfmm_device_dmma_probe(double *gflops, bfmm_stream_t stream);
 
 #ifdef __cplusplus
 }

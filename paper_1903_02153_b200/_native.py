@@ -31,8 +31,10 @@ SIGNATURES = {
     "bfmm_gather_weights": (_I, [_P, _I64, _I, _P, _P, _P, _P]),
     "bfmm_p2m": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_m2m": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
-    "bfmm_rows_gemm": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _P]),
-    "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _P, _P]),
+    "bfmm_rows_gemm": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P]),
+    "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I]),
+    "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
+    "bfmm_device_dmma_probe": (_I, [_DP, _P]),
     "bfmm_m2l_fft_scratch_bytes": (_I, [_I, _I, _I, C.POINTER(_SZ)]),
     "bfmm_m2l_fft": (_I, [_P, _P, _I, _I, _I, _P, _D, _P, _SZ, _P]),
     "bfmm_l2l": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),

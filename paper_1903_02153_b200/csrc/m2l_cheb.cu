@@ -6,13 +6,16 @@
 //    child octant.  Every target cell c of octant o needs exactly the 189
 //    offsets t whose +/-3 components match c's coordinate parity
 //    (octree.py:128-145); so per octant the operation is
-//        lt[c, :] = sum_{t in valid(o)} z[c + t, :] @ coresT[t]
+//        lt[c, i] = sum_{t in valid(o)} sum_k z[c + t, k] * C_t[i, k]
 //    i.e. a GEMM with K = 189 * rp whose A operand is gathered on the fly
-//    (rows of z at the shifted cells; zero when the source leaves the grid,
-//    exactly the pairs cell_pairs_for_offset omits, octree.py:202-221).
+//    (rows of z at the shifted cells; zero-filled when the source leaves the
+//    grid, exactly the pairs cell_pairs_for_offset omits, octree.py:202-221).
+//    The MMA is the FP64 tensor-core instruction (DMMA, mma.sync m8n8k4 f64;
+//    tcgen05 has no f64 kind), operands staged by a 3-stage cp.async ring.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -22,18 +25,18 @@ namespace {
 constexpr int TM = 64, TN = 64, KC = 8, kThreads = 256;
 
 // ----------------------------------------------------------------------------
-// Generic tiled DGEMM for row-major (rows x K) @ (K x N).
+// Generic tiled DGEMM for row-major (rows x K) @ (K x N); the A operand may
+// be stored as a_splits blocks per row that are summed on load.
 __global__ void __launch_bounds__(kThreads)
 rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
-                 const double *__restrict__ B, int N, double *__restrict__ C,
-                 double alpha, double beta) {
+                 int a_splits, const double *__restrict__ B, int N,
+                 double *__restrict__ C, double alpha, double beta) {
   __shared__ double As[2][KC][TM];
   __shared__ double Bs[2][KC][TN];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t r0 = int64_t(blockIdx.x) * TM;
   const int n0 = blockIdx.y * TN;
   double acc[4][4] = {};
-  // loader mapping: A tile TM x KC -> thread loads 2 elements
   const int la_r = threadIdx.x >> 2, la_k = (threadIdx.x & 3) * 2;
   const int lb_k = threadIdx.x >> 5, lb_n = (threadIdx.x & 31) * 2;
   double ra[2], rb[2];
@@ -42,7 +45,13 @@ rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int k = k0 + la_k + u;
-      ra[u] = (r < rows && k < K) ? A[r * K + k] : 0.0;
+      double v = 0.0;
+      if (r < rows && k < K) {
+        // logical A[r][k] = sum_s A[r][s][k] (M2L split blocks, fixed order)
+        const double *a = A + (r * a_splits) * K + k;
+        for (int sp = 0; sp < a_splits; ++sp) v += a[(int64_t)sp * K];
+      }
+      ra[u] = v;
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -97,19 +106,21 @@ rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
 }
 
 // ----------------------------------------------------------------------------
-// 316 far offsets in the reference's lexicographic order (octree.py:110-119).
+// 316 far offsets in the reference's lexicographic order (octree.py:110-119)
+// and, per child octant, the 189 of them its parity admits (in that order).
 __constant__ signed char c_offsets[316][3];
+__constant__ short c_valid[8][189];
 bool g_offsets_ready = false;
 
 void ensure_offsets() {
   if (g_offsets_ready) return;
   signed char h[316][3];
+  short v[8][189];
   int n = 0;
   for (int a = -3; a <= 3; ++a)
     for (int b = -3; b <= 3; ++b)
       for (int c = -3; c <= 3; ++c) {
-        int mx = abs(a) > abs(b) ? abs(a) : abs(b);
-        mx = mx > abs(c) ? mx : abs(c);
+        int mx = std::max(abs(a), std::max(abs(b), abs(c)));
         if (mx >= 2) {
           h[n][0] = (signed char)a;
           h[n][1] = (signed char)b;
@@ -117,132 +128,51 @@ void ensure_offsets() {
           ++n;
         }
       }
+  for (int o = 0; o < 8; ++o) {
+    int k = 0;
+    const int bit[3] = {(o >> 2) & 1, (o >> 1) & 1, o & 1};
+    for (int t = 0; t < 316; ++t) {
+      bool ok = true;
+      for (int a = 0; a < 3; ++a) {
+        // the parity half of far_axis_ok: +3 needs even, -3 needs odd
+        if (h[t][a] == 3 && bit[a]) ok = false;
+        if (h[t][a] == -3 && !bit[a]) ok = false;
+      }
+      if (ok) v[o][k++] = (short)t;
+    }
+  }
   cudaMemcpyToSymbol(c_offsets, h, sizeof(h));
+  cudaMemcpyToSymbol(c_valid, v, sizeof(v));
   g_offsets_ready = true;
 }
 
-__device__ inline bool offset_valid_for_octant(int o, int t0, int t1, int t2) {
-  // +3 needs an even coordinate (octant bit 0), -3 an odd one (bit 1)
-  const int bx = (o >> 2) & 1, by = (o >> 1) & 1, bz = o & 1;
-  if (t0 == 3 && bx) return false;
-  if (t0 == -3 && !bx) return false;
-  if (t1 == 3 && by) return false;
-  if (t1 == -3 && !by) return false;
-  if (t2 == 3 && bz) return false;
-  if (t2 == -3 && !bz) return false;
-  return true;
+// ---- DMMA helpers -------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a,
+                                           double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+      "{%0, %1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
-// Implicit-GEMM M2L.  Grid: (row tiles, column tiles, 8 octants).
-// Rows are (target cell of octant o, weight column) pairs.
-__global__ void __launch_bounds__(kThreads)
-m2l_cheb_kernel(const double *__restrict__ z, double *__restrict__ lt,
-                int level, int m, int rp, const double *__restrict__ coresT) {
-  __shared__ double As[2][KC][TM];
-  __shared__ double Bs[2][KC][TN];
-  const int o = blockIdx.z;
-  const int n = 1 << level;
-  const int64_t ncell = int64_t(1) << (3 * level);
-  const int64_t rows = (ncell >> 3) * m;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t r0 = int64_t(blockIdx.x) * TM;
-  const int n0 = blockIdx.y * TN;
-
-  // loader: A tile TM rows x KC -> each thread one double2 (row, k pair)
-  const int la_r = threadIdx.x >> 2, la_k = (threadIdx.x & 3) * 2;
-  const int lb_k = threadIdx.x >> 5, lb_n = (threadIdx.x & 31) * 2;
-  const int64_t my_row = r0 + la_r;
-  int cx = 0, cy = 0, cz = 0, col = 0;
-  const bool row_ok = my_row < rows;
-  if (row_ok) {
-    const int64_t q = my_row / m;
-    col = (int)(my_row - q * m);
-    unmorton3((uint64_t)(8 * q + o), cx, cy, cz);
-  }
-  const int kchunks = rp / KC;
-
-  double acc[4][4] = {};
-  double2 ra;
-  double rb[2];
-  // iterate over (offset, k-chunk) steps
-  int t = -1, kc = kchunks;  // current step
-  int64_t src_base = -1;
-  auto advance = [&]() -> bool {
-    ++kc;
-    if (kc >= kchunks) {
-      kc = 0;
-      for (++t; t < 316; ++t)
-        if (offset_valid_for_octant(o, c_offsets[t][0], c_offsets[t][1],
-                                    c_offsets[t][2]))
-          break;
-      if (t >= 316) return false;
-      const int t0 = c_offsets[t][0], t1 = c_offsets[t][1], t2 = c_offsets[t][2];
-      if (row_ok && far_pair(n, cx, cy, cz, t0, t1, t2))
-        src_base =
-            ((int64_t)morton3(cx + t0, cy + t1, cz + t2) * m + col) * rp;
-      else
-        src_base = -1;
-    }
-    return true;
-  };
-  auto load = [&]() {
-    const int k = kc * KC;
-    if (src_base >= 0)
-      ra = *reinterpret_cast<const double2 *>(z + src_base + k + la_k);
-    else
-      ra = make_double2(0.0, 0.0);
-    const double *bt = coresT + ((int64_t)t * rp + k + lb_k) * rp;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int nn = n0 + lb_n + u;
-      rb[u] = nn < rp ? bt[nn] : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-    As[buf][la_k][la_r] = ra.x;
-    As[buf][la_k + 1][la_r] = ra.y;
-    Bs[buf][lb_k][lb_n] = rb[0];
-    Bs[buf][lb_k][lb_n + 1] = rb[1];
-  };
-  if (!advance()) return;
-  load();
-  store(0);
-  __syncthreads();
-  int buf = 0;
-  while (true) {
-    const bool more = advance();
-    if (more) load();
-#pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    if (!more) break;
-    store(buf ^ 1);
-    __syncthreads();
-    buf ^= 1;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + ty + 16 * i;
-    if (r >= rows) continue;
-    const int64_t q = r / m;
-    const int c = (int)(r - q * m);
-    double *dst = lt + ((8 * q + o) * m + c) * rp;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int nn = n0 + tx + 16 * j;
-      if (nn < rp) dst[nn] = acc[i][j];
-    }
-  }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem,
+                                           bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s),
+               "l"(gmem), "r"(n));
 }
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+#include "m2l_dmma.cuh"
+#include "m2l_ws.cuh"
 
 // ----------------------------------------------------------------------------
 // Explicit far list for one offset, in the reference's meshgrid(ij) order
@@ -325,26 +255,58 @@ extern "C" int bfmm_far_pairs(int level, int t_index, int64_t *tg, int64_t *sr,
 
 extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
                               const double *B, int N, double *C, double alpha,
-                              double beta, bfmm_stream_t stream) {
+                              double beta, int a_splits, bfmm_stream_t stream) {
   if (rows <= 0 || N <= 0) return 0;
+  if (a_splits < 1) {
+    set_error("bfmm_rows_gemm: a_splits=%d < 1", a_splits);
+    return 2;
+  }
   dim3 grid((unsigned)ceil_div(rows, TM), (unsigned)ceil_div(N, TN));
-  rows_gemm_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(A, rows, K, B, N,
-                                                             C, alpha, beta);
+  rows_gemm_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(
+      A, rows, K, a_splits, B, N, C, alpha, beta);
   return check_launch("rows_gemm_kernel");
 }
 
+extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp) {
+  // about three CTA slots' worth of work per SM; every split keeps >= 8 offsets
+  const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
+  const M2LConfig c = m2l_config(level, m, rp);
+  const int64_t ctas =
+      ceil_div(rows, rows <= 64 ? 64 : 128) * ceil_div(rp, 8 * c.nt8) * 8;
+  // pick the split count whose last wave (2 CTAs per SM) is fullest, with a
+  // small penalty per split for the extra lt traffic
+  const double slots = 2.0 * kNumSMs;
+  int best = 1;
+  double best_score = -1e30;
+  for (int s = 1; s <= 189 / 8; ++s) {
+    const double waves = ctas * s / slots;
+    const double score = waves / std::ceil(waves) - 0.004 * s;
+    if (score > best_score + 1e-12) {
+      best_score = score;
+      best = s;
+    }
+  }
+  return best;
+}
+
 extern "C" int bfmm_m2l_cheb(const double *z, double *lt, int level, int m,
-                             int rp, const double *coresT,
+                             int rp, int nsplit, const double *cores,
                              bfmm_stream_t stream) {
-  if (rp % KC != 0 || level < 2 || level > 10) {
-    set_error("bfmm_m2l_cheb: rp=%d must be a multiple of %d, level=%d", rp, KC,
-              level);
+  if (rp % 8 != 0 || rp <= 0 || level < 2 || level > 10) {
+    set_error("bfmm_m2l_cheb: rp=%d must be a positive multiple of 8, level=%d",
+              rp, level);
+    return 2;
+  }
+  if (nsplit < 1 || nsplit > 189) {
+    set_error("bfmm_m2l_cheb: nsplit=%d outside [1, 189]", nsplit);
     return 2;
   }
   ensure_offsets();
+  const M2LConfig c = m2l_config(level, m, rp);
+  static const char *which = getenv("BFMM_M2L_KERNEL");
+  if (which && which[0] == 's')  // "sync": CTA-barrier pipeline variant
+    return dispatch_m2l(c, z, lt, level, m, rp, nsplit, cores, as_stream(stream));
   const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
-  dim3 grid((unsigned)ceil_div(rows, TM), (unsigned)ceil_div(rp, TN), 8);
-  m2l_cheb_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(z, lt, level, m, rp,
-                                                            coresT);
-  return check_launch("m2l_cheb_kernel");
+  return dispatch_ws(rows <= 64 ? 1 : 2, c.nt8, z, lt, level, m, rp, nsplit, cores,
+                     as_stream(stream));
 }

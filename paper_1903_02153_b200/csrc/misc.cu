@@ -33,10 +33,121 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double *out, int iters,
   if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
 }
 
+// Eight independent m8n8k4 f64 MMA chains per warp (FP64 tensor cores).
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double *out, int iters) {
+  double c[8][2];
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 0.999999;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) c[u][0] = c[u][1] = u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      asm volatile(
+          "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, "
+          "{%3}, {%0, %1};\n"
+          : "+d"(c[u][0]), "+d"(c[u][1])
+          : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += c[u][0] + c[u][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+// C independent m8n8k4 chains per warp (microarchitecture sweep).
+template <int C>
+__global__ void dmma_chain_kernel(double *out, int iters) {
+  double c[C][2];
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 0.999999;
+#pragma unroll
+  for (int u = 0; u < C; ++u) c[u][0] = c[u][1] = u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < C; ++u)
+      asm volatile(
+          "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, "
+          "{%3}, {%0, %1};\n"
+          : "+d"(c[u][0]), "+d"(c[u][1])
+          : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < C; ++u) s += c[u][0] + c[u][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <class F>
+float best_ms(F launch, cudaStream_t st) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  launch();
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, st);
+    launch();
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+
 }  // namespace
 }  // namespace bfmm
 
 using namespace bfmm;
+
+// Diagnostics: DMMA throughput with `warps_per_sm` resident warps (one CTA
+// of that many warps per SM) each running `chains` independent chains.
+extern "C" int bfmm_device_dmma_sweep(int warps_per_sm, int chains,
+                                      double *gflops, bfmm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  double *out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return 1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int iters = (1 << 13) / chains;
+  dim3 grid(sms), block(32 * warps_per_sm);
+  float ms = 0.f;
+  switch (chains) {
+    case 1: ms = best_ms([&] { dmma_chain_kernel<1><<<grid, block, 0, st>>>(out, iters); }, st); break;
+    case 2: ms = best_ms([&] { dmma_chain_kernel<2><<<grid, block, 0, st>>>(out, iters); }, st); break;
+    case 4: ms = best_ms([&] { dmma_chain_kernel<4><<<grid, block, 0, st>>>(out, iters); }, st); break;
+    case 8: ms = best_ms([&] { dmma_chain_kernel<8><<<grid, block, 0, st>>>(out, iters); }, st); break;
+    default: ms = best_ms([&] { dmma_chain_kernel<16><<<grid, block, 0, st>>>(out, iters); }, st); chains = 16; break;
+  }
+  cudaFree(out);
+  if (check_launch("dmma_chain_kernel")) return 1;
+  *gflops = 512.0 * chains * iters * double(grid.x) * warps_per_sm / (ms * 1e-3) / 1e9;
+  return 0;
+}
+
+extern "C" int bfmm_device_dmma_probe(double *gflops, bfmm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  double *out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) {
+    set_error("bfmm_device_dmma_probe: cudaMalloc failed");
+    return 1;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int iters = 1 << 12;
+  dim3 grid(sms * 4), block(256);
+  float ms = best_ms([&] { dmma_probe_kernel<<<grid, block, 0, st>>>(out, iters); }, st);
+  cudaFree(out);
+  if (check_launch("dmma_probe_kernel")) return 1;
+  // 8 chains x 256 FMA (512 flops) per warp per iteration
+  const double flops = 512.0 * 8 * iters * double(grid.x) * (block.x / 32);
+  *gflops = flops / (ms * 1e-3) / 1e9;
+  return 0;
+}
 
 extern "C" const char *bfmm_last_error(void) { return g_err; }
 

@@ -41,6 +41,13 @@ def _pad8(r: int) -> int:
     return (r + 7) // 8 * 8
 
 
+def _rank_interleave(rp: int) -> np.ndarray:
+    """Storage position of rank index k: 2*(k%4) + (k//4)%2 inside its group
+    of 8, so an MMA lane finds the k of two consecutive k4 steps adjacent."""
+    k = np.arange(rp)
+    return (k // 8) * 8 + 2 * (k % 4) + (k // 4) % 2
+
+
 @dataclass
 class _Tree:
     """A point set binned by leaf on the device (reference _Partition)."""
@@ -116,17 +123,20 @@ class FmmEvaluator:
             if isinstance(blk, ChebyshevLevelBlock):
                 p3, r = blk.u.shape
                 rp = _pad8(r)
+                # rank index k of z and of the cores' k axis is interleaved inside
+                # groups of 8 (csrc/m2l_dmma.cuh); the contraction is unchanged
+                kpos = _rank_interleave(rp)[:r]
                 V = np.zeros((p3, rp))
-                V[:, :r] = blk.v
+                V[:, kpos] = blk.v
                 UT = np.zeros((rp, p3))
                 UT[:r] = blk.u.T
-                CT = np.zeros((blk.cores.shape[0], rp, rp))
-                CT[:, :r, :r] = blk.cores.transpose(0, 2, 1)
+                CP = np.zeros((blk.cores.shape[0], rp, rp))
+                CP[:, :r, kpos] = blk.cores  # [t][i][k], k contiguous
                 self._dev_blocks[key] = {
                     "kind": "cheb", "r": r, "rp": rp,
                     "V": torch.from_numpy(V).to(dev),
                     "UT": torch.from_numpy(UT).to(dev),
-                    "coresT": torch.from_numpy(np.ascontiguousarray(CT)).to(dev),
+                    "cores": torch.from_numpy(CP).to(dev),
                 }
             else:
                 sym = np.ascontiguousarray(blk.symbols).view(np.float64)
@@ -240,16 +250,17 @@ class FmmEvaluator:
             out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
             if blk["kind"] == "cheb":
                 rp = blk["rp"]
+                ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp))
                 z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
-                lt = torch.empty_like(z)
+                lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
                 _native.check(self.lib.bfmm_rows_gemm(moments[lev].data_ptr(), ncell * m, p3,
                                                       blk["V"].data_ptr(), rp, z.data_ptr(),
-                                                      1.0, 0.0, st), "bfmm_rows_gemm(V)")
-                _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp,
-                                                     blk["coresT"].data_ptr(), st), "bfmm_m2l_cheb")
+                                                      1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+                _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
+                                                     blk["cores"].data_ptr(), st), "bfmm_m2l_cheb")
                 _native.check(self.lib.bfmm_rows_gemm(lt.data_ptr(), ncell * m, rp,
                                                       blk["UT"].data_ptr(), p3, out.data_ptr(),
-                                                      scale, 0.0, st), "bfmm_rows_gemm(U)")
+                                                      scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
             else:
                 nb = _native.C.c_size_t(0)
                 _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, m, p, _native.C.byref(nb)),

@@ -164,7 +164,7 @@ def case_tables():
             if hasattr(blk, "u"):
                 out[f"{tag}_rank_{lev}"] = np.array(blk.rank)
         big = plan.order ** 3 > 125
-        for lev in ((3,) if big else (2, 3, 4)):
+        for lev in [l for l in ((3,) if big else (2, 3, 4)) if l <= plan.levels]:
             out[f"{tag}_dense_{lev}"] = np.stack([table.dense(t, lev)
                                                  for t in (probe[:2] if big else probe)])
     # a small table kept whole for element-wise pins (p=3, symmetric 1/r)
