@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""FMM matvec throughput (points/s, fp64) on B200 — the BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2] [--no-cpu-baseline]
+
+Workload (N=1): BASELINE.json configs[1] = C2 (Gaussian exp(-(r/0.2)^2),
+N = 1,000,000 uniform in [-1,1]^3, L=5, Chebyshev p=5, eps 1e-7, 1 RHS),
+seeded synthetic inputs; the other configs are parity
+cases (tests/).  A step is one full matvec phi = K sigma: tree build, P2M,
+M2M, M2L, L2L, L2P, P2P, output scatter.
+
+* value     device-resident inputs, CUDA-event time of K steps, L2 flushed
+            (256 MiB write) between steps outside the timed spans.
+* e2e       the public API on pinned host tensors: H2D of points + weights,
+            the matvec, D2H of phi, every step.
+* roofline  the dominant kernel (largest share of the step), timed live
+            with CUDA events on its launching stream; FP64 peak measured live
+            (DMMA/DFMA microbenchmarks in libbfmm.so: MEASURED_PEAKS.json has
+            no FP64 entry).
+* cpu_baseline  the CPU oracle (oracle/fmm_oracle.py, a NumPy restatement of
+            the reference's engine with its thread pool) on the same C2
+            inputs, timed on this host's cores, rank 0 at N=1 only.
+* --impl reference  the same oracle as the reference arm (the reference is
+            pure Python and not present on the GPU box; the oracle is pinned
+            to its outputs by tests/test_oracle_golden.py).
+* N > 1: target leaves are split by Morton range across ranks (one process
+  per GPU, NCCL); each rank evaluates its share, phi is all-gathered.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FMM matvec points/sec (fp64) at 1/2/4/8 B200; P2P & M2L % of roofline"
+
+# FP64 flops per near-field pair interaction, frozen from ncu instruction
+# counts of the P2P kernel (2*DFMA + DMUL + DADD thread instructions / pair,
+# profiles/r01_p2p_flops.txt); kernel-specific.
+P2P_FLOPS_PER_PAIR = {"gauss02": 62.0, "laplacian": 30.0, "laplacianforce": 34.0,
+                      "exp03": 66.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(name):
+    from paper_1903_02153_b200 import workloads
+    return workloads.make(name)
+
+
+def config_dict(wl):
+    from paper_1903_02153_b200 import workloads
+    return {"workload": f"{wl['name']}: {workloads.DESCRIPTION[wl['name']]}",
+            "n_points": int(wl["points"].shape[0]), "levels": wl["levels"],
+            "order": wl["order"], "scheme": wl["scheme"], "eps": wl["eps"],
+            "kernel": wl["kernel"], "ncols": wl["ncols"],
+            "l2": "flushed between steps (256 MiB write, outside the timed spans)"}
+
+
+def oracle_step(wl, threads):
+    from oracle import fmm_oracle as O
+    from paper_1903_02153_b200.kernel import workload_kernel
+    fmm = O.OracleFMM(workload_kernel(wl["kernel"]), wl["levels"], wl["order"],
+                      wl["scheme"], wl["eps"], wl["center"], wl["length"], threads=threads)
+    t0 = time.perf_counter()
+    fmm.matvec(wl["points"], weights=wl["weights"])
+    return time.perf_counter() - t0
+
+
+def cpu_threads():
+    try:
+        import psutil
+        return max(1, psutil.cpu_count(logical=False) or os.cpu_count() or 1)
+    except Exception:
+        return max(1, os.cpu_count() or 1)
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle (reference algorithm, NumPy, thread pool)
+    on the host cores; rank 0 only."""
+    if rank != 0:
+        return
+    wl = make_workload(args.config)
+    threads = cpu_threads()
+    for _ in range(args.warmup):
+        oracle_step(wl, threads)
+    times = [oracle_step(wl, threads) for _ in range(args.steps)]
+    total = sum(times)
+    n = wl["points"].shape[0]
+    value = n * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SURVEY.md §8(d) recipe)", "config": config_dict(wl),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
+                         "sample": f"full {args.config} matvec per step (oracle/fmm_oracle.py)"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def fp64_peaks(lib, stream):
+    import ctypes as C
+    g1, g2 = C.c_double(0), C.c_double(0)
+    lib.bfmm_device_fp64_probe(C.byref(g1), stream)
+    lib.bfmm_device_dmma_probe(C.byref(g2), stream)
+    return g1.value / 1e3, g2.value / 1e3  # TFLOP/s
+
+
+def m2l_flops(ev, wl):
+    """Algorithmic M2L flops per level: pairs P_l * 2 r_l^2 * m."""
+    from paper_1903_02153_b200.tables import OFFSETS
+    out = {}
+    m = wl["ncols"]
+    for lev in range(2, wl["levels"] + 1):
+        n = 1 << lev
+        pairs = 1
+        cnt = 0
+        for t in OFFSETS:
+            c = 1
+            for a in range(3):
+                tt = int(t[a])
+                lo, hi = max(0, -tt), min(n - 1, n - 1 - tt)
+                k = max(0, hi - lo + 1)
+                if abs(tt) == 3:
+                    k = len([x for x in range(lo, hi + 1) if (x % 2 == 0) == (tt > 0)])
+                c *= k
+            cnt += c
+        blk = ev.table.block_for_level(lev)
+        r = blk.rank
+        out[lev] = cnt * 2.0 * r * r * m
+        del pairs
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+    import torch
+
+    import paper_1903_02153_b200 as bf
+    from paper_1903_02153_b200 import _native
+    from paper_1903_02153_b200.kernel import workload_kernel
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = make_workload(args.config)
+    plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"],
+                      eps=wl["eps"], domain_center=wl["center"], domain_length=wl["length"],
+                      n_cols=wl["ncols"])
+    kernel = workload_kernel(wl["kernel"])
+    ev = bf.FmmEvaluator(kernel, plan, cache_dir=os.path.join("/tmp", "bfmm_bench_cache"))
+    lib = _native.load()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    n = wl["points"].shape[0]
+    m = wl["ncols"]
+    X = torch.from_numpy(wl["points"]).cuda()
+    W = torch.from_numpy(np.ascontiguousarray(wl["weights"])).cuda()
+    if world > 1:
+        from paper_1903_02153_b200.parallel import ShardedEvaluator
+        runner = ShardedEvaluator(ev, dist)
+        step = lambda x, w: runner.evaluate(x, weights=w)  # noqa: E731
+    else:
+        runner = ev
+        step = lambda x, w: ev.evaluate(x, weights=w)  # noqa: E731
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        step(X, W)
+    torch.cuda.synchronize()
+    ev.profile_kernels = True
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.bfmm_launch_count()
+    spans, kms, stage_sum = [], [], {}
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(X, W)
+        e1.record()
+        e1.synchronize()
+        spans.append(e0.elapsed_time(e1))
+        kms.append(dict(ev.kernel_ms))
+        for k, v in ev.timings.items():
+            if isinstance(v, float):
+                stage_sum[k] = stage_sum.get(k, 0.0) + v
+    torch.cuda.synchronize()
+    launches = lib.bfmm_launch_count() - launches0
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    ev.profile_kernels = False
+    total_ms = float(sum(spans))
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n * args.steps / (total_ms * 1e-3)
+
+    # ---- e2e through the public API with pinned host tensors ----
+    Xh = torch.from_numpy(wl["points"]).pin_memory()
+    Wh = torch.from_numpy(np.ascontiguousarray(wl["weights"])).pin_memory()
+    for _ in range(2):
+        runner.evaluate(Xh, weights=Wh)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        phi = runner.evaluate(Xh, weights=Wh)
+        assert phi.device.type == "cpu"
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_total = float(sum(e2e_ms))
+    if dist is not None:
+        t = torch.tensor([e2e_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = n * args.steps / (e2e_total * 1e-3)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----
+    dfma_tf, dmma_tf = fp64_peaks(lib, stream)
+    avg = {}
+    for d in kms:
+        for k, v in d.items():
+            avg[k] = avg.get(k, 0.0) + v / len(kms)
+    dom = max(avg, key=avg.get) if avg else None
+    roof = None
+    if dom is not None:
+        ms = avg[dom]
+        if dom == "p2p":
+            fpp = P2P_FLOPS_PER_PAIR.get(wl["kernel"])
+            pairs = ev.timings["near_pairs"] * m
+            flops = pairs * fpp
+            peak = dfma_tf
+            roof = {"kernel": "p2p (near field, FP64 pipe)", "bound": "fp64",
+                    "flops_per_pair": fpp, "pair_interactions": pairs}
+        else:
+            lev = int(dom.split("_l")[1])
+            flops = m2l_flops(ev, wl)[lev]
+            peak = dmma_tf
+            roof = {"kernel": f"m2l level {lev} (DMMA implicit GEMM)", "bound": "fp64-tensor"}
+        achieved = flops / (ms * 1e-3) / 1e12
+        roof.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_source": "measured live: DFMA / DMMA microbenchmarks (libbfmm.so); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "kernel_ms": ms, "share_of_step": ms / (total_ms / args.steps)})
+    m2l = m2l_flops(ev, wl)
+    kernels = {k: round(v, 4) for k, v in sorted(avg.items())}
+    m2l_frac = {k: (m2l[int(k.split("_l")[1])] / (v * 1e-3) / 1e12) / dmma_tf
+                for k, v in avg.items() if k.startswith("m2l_l")}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = cpu_threads()
+        secs = oracle_step(wl, threads)
+        cpu = {"value": n / secs, "unit": "points/s", "cores": threads, "kind": "port",
+               "sample": f"one full {args.config} matvec (oracle/fmm_oracle.py, {secs:.1f} s)"}
+
+    h2d = int(Xh.numel() * 8 + Wh.numel() * 8)
+    d2h = int(n * m * 8)
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SURVEY.md §8(d) recipe)", "config": config_dict(wl),
+        "roofline": roof, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps},
+        "gpu_launches": int(launches), "clocks": clk,
+        "stages_ms": {k: round(1e3 * v / args.steps, 4) for k, v in stage_sum.items()},
+        "kernels_ms": kernels,
+        "m2l_frac_of_dmma_peak": {k: round(v, 3) for k, v in m2l_frac.items()},
+        "fp64_peaks_tflops": {"dfma": dfma_tf, "dmma": dmma_tf},
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

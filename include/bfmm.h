@@ -208,6 +208,15 @@ int bfmm_device_fp64_probe(double *gflops, bfmm_stream_t stream);
 /* Same for the FP64 tensor-core MMA (mma.sync m8n8k4 f64 -> DMMA). */
 int bfmm_device_dmma_probe(double *gflops, bfmm_stream_t stream);
 
+/* DMMA throughput with warps_per_sm resident warps x `chains` independent
+ * accumulator chains (microarchitecture sweep behind the M2L tiling). */
+int bfmm_device_dmma_sweep(int warps_per_sm, int chains, double *gflops,
+                           bfmm_stream_t stream);
+
+/* Number of kernels this library has launched in this process (own
+ * kernels plus the CUB sort/scan kernels it invokes). */
+long long bfmm_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

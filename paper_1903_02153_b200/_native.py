@@ -35,6 +35,8 @@ SIGNATURES = {
     "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I]),
     "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "bfmm_device_dmma_probe": (_I, [_DP, _P]),
+    "bfmm_device_dmma_sweep": (_I, [_I, _I, _DP, _P]),
+    "bfmm_launch_count": (C.c_longlong, []),
     "bfmm_m2l_fft_scratch_bytes": (_I, [_I, _I, _I, C.POINTER(_SZ)]),
     "bfmm_m2l_fft": (_I, [_P, _P, _I, _I, _I, _P, _D, _P, _SZ, _P]),
     "bfmm_l2l": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),

@@ -11,7 +11,11 @@ namespace bfmm {
 // Thread-local message behind bfmm_last_error().
 void set_error(const char *fmt, ...);
 
+// Process-wide count of kernels this library has launched (bfmm_launch_count).
+void add_launches(long long n);
+
 inline int check_launch(const char *what) {
+  add_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));

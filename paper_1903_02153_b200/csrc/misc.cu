@@ -2,11 +2,16 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace bfmm {
 
 static thread_local char g_err[4096] = "";
+static std::atomic<long long> g_launches{0};
+
+void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
   va_list ap;
@@ -152,6 +157,10 @@ extern "C" int bfmm_device_dmma_probe(double *gflops, bfmm_stream_t stream) {
 extern "C" const char *bfmm_last_error(void) { return g_err; }
 
 extern "C" int bfmm_version(void) { return 1; }
+
+extern "C" long long bfmm_launch_count(void) {
+  return g_launches.load(std::memory_order_relaxed);
+}
 
 extern "C" int bfmm_device_fp64_probe(double *gflops, bfmm_stream_t stream) {
   cudaStream_t st = as_stream(stream);

@@ -427,6 +427,7 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
     set_error("bfmm_p2p: scan failed");
     return 1;
   }
+  add_launches(2);  // CUB scan: init + scan
   bfmm_nf::Args a = make_args(tpts4, tleaves, tstarts, tcounts, n_tleaves,
                                spts4, swsorted, m, scell_start, scell_count,
                                levels, out, incl);

@@ -190,6 +190,7 @@ int build(const double *points, int64_t n, const TreeGeom &g, int levels,
     set_error("bfmm_tree_build: radix sort failed");
     return 1;
   }
+  add_launches(2 + (3 * levels + 7) / 8);  // CUB onesweep: histogram, scan, passes
   heads_kernel<Key><<<grid_for(n, T), T, 0, st>>>(kout, n, head);
   if (check_launch("heads_kernel")) return 1;
   sb = cub_bytes;
@@ -198,6 +199,7 @@ int build(const double *points, int64_t n, const TreeGeom &g, int levels,
     set_error("bfmm_tree_build: scan failed");
     return 1;
   }
+  add_launches(2);  // CUB scan: init + scan
   runs_kernel<Key><<<grid_for(n, T), T, 0, st>>>(kout, head, run, n, leaves,
                                                  starts, n_leaves);
   if (check_launch("runs_kernel")) return 1;

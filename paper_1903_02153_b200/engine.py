@@ -103,6 +103,9 @@ class FmmEvaluator:
         self._disable_far_field = False
         self.keep_stages = False
         self.stages = {}
+        self.profile_kernels = False
+        self.kernel_ms = {}
+        self._kpending = []
 
     # -- setup --------------------------------------------------------------
     def _kernel_handle(self) -> int:
@@ -256,8 +259,10 @@ class FmmEvaluator:
                 _native.check(self.lib.bfmm_rows_gemm(moments[lev].data_ptr(), ncell * m, p3,
                                                       blk["V"].data_ptr(), rp, z.data_ptr(),
                                                       1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+                e0 = self._kevent()
                 _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
                                                      blk["cores"].data_ptr(), st), "bfmm_m2l_cheb")
+                self._kspan(f"m2l_l{lev}", e0)
                 _native.check(self.lib.bfmm_rows_gemm(lt.data_ptr(), ncell * m, rp,
                                                       blk["UT"].data_ptr(), p3, out.data_ptr(),
                                                       scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
@@ -291,12 +296,32 @@ class FmmEvaluator:
         st = self._stream()
         sb = self.lib.bfmm_p2p_scratch_bytes(max(ttree.max_leaves, 1))
         scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        e0 = self._kevent()
         _native.check(self.lib.bfmm_p2p(
             self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(), ttree.starts.data_ptr(),
             ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(), ttree.max_leaves,
             stree.pts4.data_ptr(), ws.data_ptr(), m, stree.cell_start.data_ptr(),
             stree.cell_count.data_ptr(), self.plan.levels, near.data_ptr(), scratch.data_ptr(),
             sb, st), "bfmm_p2p")
+        self._kspan("p2p", e0)
+
+    # per-kernel CUDA events on the launching (current) stream, enabled by
+    # profile_kernels; read back after the evaluate's synchronising status read
+    def _kevent(self):
+        if not self.profile_kernels:
+            return None
+        torch = _torch()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def _kspan(self, name, e0):
+        if e0 is None:
+            return
+        torch = _torch()
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self._kpending.append((name, e0, e1))
 
     # -- driver -----------------------------------------------------------------
     def evaluate(self, sources, targets=None, weights=None):
@@ -366,6 +391,8 @@ class FmmEvaluator:
             self.stages = {"stree": stree, "ttree": ttree, "moments": moments, "locals": locs,
                            "near": near, "far": phi_far, "ws": ws}
         stat = status.cpu().numpy()  # the one synchronising read-back
+        self.kernel_ms = {name: a.elapsed_time(b) for name, a, b in self._kpending}
+        self._kpending = []
         self._raise_flags(stat, ttree, stree)
         if as_tensor:
             result = phi if out_device.type == "cuda" else phi.to(out_device)
