@@ -49,8 +49,7 @@ METRIC = "FMM matvec points/sec (fp64) at 1/2/4/8 B200; P2P & M2L % of roofline"
 # FP64 flops per near-field pair interaction, frozen from ncu instruction
 # counts of the P2P kernel (2*DFMA + DMUL + DADD thread instructions / pair,
 # profiles/r01_p2p_flops.txt); kernel-specific.
-P2P_FLOPS_PER_PAIR = {"gauss02": 62.0, "laplacian": 30.0, "laplacianforce": 34.0,
-                      "exp03": 66.0}
+P2P_FLOPS_PER_PAIR = {"gauss02": 40.0}
 
 
 def parse():

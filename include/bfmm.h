@@ -90,8 +90,9 @@ int bfmm_m2m(const double *child, double *parent, int64_t n_parent, int p,
 
 /* C = alpha * A @ B + beta * C for row-major A (rows, K), B (K, N),
  * C (rows, N).  A may be stored as a_splits blocks of K per row
- * (rows, a_splits, K) that are summed in order on load.  Used for
- * z = moments @ V and locals = scale * lt @ U^T (engine.py:233, 252-255). */
+ * (rows, a_splits, K); they are first summed in order IN PLACE into block 0
+ * (A is modified).  Used for z = moments @ V and
+ * locals = scale * lt @ U^T (engine.py:233, 252-255). */
 int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
                    int N, double *C, double alpha, double beta, int a_splits,
                    bfmm_stream_t stream);

@@ -45,13 +45,8 @@ rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int k = k0 + la_k + u;
-      double v = 0.0;
-      if (r < rows && k < K) {
-        // logical A[r][k] = sum_s A[r][s][k] (M2L split blocks, fixed order)
-        const double *a = A + (r * a_splits) * K + k;
-        for (int sp = 0; sp < a_splits; ++sp) v += a[(int64_t)sp * K];
-      }
-      ra[u] = v;
+      // row stride a_splits * K: split block 0 holds the reduced sum
+      ra[u] = (r < rows && k < K) ? A[(r * a_splits) * K + k] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -103,6 +98,39 @@ rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
       C[r * N + n] = v;
     }
   }
+}
+
+// A[r][0][k] = sum_s A[r][s][k] in place, fixed order (M2L split blocks).
+__global__ void reduce_splits_kernel(double *__restrict__ A, int64_t rows, int K,
+                                     int a_splits) {
+  const int64_t total = rows * K;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / K;
+    const int k = (int)(e - r * K);
+    double *a = A + r * a_splits * K + k;
+    double v = a[0];
+    for (int sp = 1; sp < a_splits; ++sp) v += a[(int64_t)sp * K];
+    a[0] = v;
+  }
+}
+
+// One thread per output for small (coarse-level) projections: a single 64-row
+// tile would serialise the whole K loop on one SM.
+__global__ void __launch_bounds__(128)
+small_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
+                  int a_splits, const double *__restrict__ B, int N,
+                  double *__restrict__ C, double alpha, double beta) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= rows * N) return;
+  const int64_t r = e / N;
+  const int n = (int)(e - r * N);
+  const double *a = A + r * a_splits * K;  // split block 0 holds the sum
+  double acc = 0.0;
+  for (int k = 0; k < K; ++k) acc = fma(a[k], B[(int64_t)k * N + n], acc);
+  double out = alpha * acc;
+  if (beta != 0.0) out += beta * C[e];
+  C[e] = out;
 }
 
 // ----------------------------------------------------------------------------
@@ -261,24 +289,38 @@ extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
     set_error("bfmm_rows_gemm: a_splits=%d < 1", a_splits);
     return 2;
   }
+  cudaStream_t st = as_stream(stream);
+  if (a_splits > 1) {
+    reduce_splits_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * K, 256), 4096), 256,
+                           0, st>>>(const_cast<double *>(A), rows, K, a_splits);
+    if (check_launch("reduce_splits_kernel")) return 1;
+  }
+  if (rows * N <= (int64_t(1) << 17)) {
+    // small problem (coarse tree levels): one thread per output, full K
+    small_gemm_kernel<<<(unsigned)ceil_div(rows * N, 128), 128, 0, st>>>(
+        A, rows, K, a_splits, B, N, C, alpha, beta);
+    return check_launch("small_gemm_kernel");
+  }
   dim3 grid((unsigned)ceil_div(rows, TM), (unsigned)ceil_div(N, TN));
-  rows_gemm_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(
-      A, rows, K, a_splits, B, N, C, alpha, beta);
+  rows_gemm_kernel<<<grid, kThreads, 0, st>>>(A, rows, K, a_splits, B, N, C,
+                                              alpha, beta);
   return check_launch("rows_gemm_kernel");
 }
 
 extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp) {
-  // about three CTA slots' worth of work per SM; every split keeps >= 8 offsets
   const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
   const M2LConfig c = m2l_config(level, m, rp);
   const int64_t ctas =
       ceil_div(rows, rows <= 64 ? 64 : 128) * ceil_div(rp, 8 * c.nt8) * 8;
-  // pick the split count whose last wave (2 CTAs per SM) is fullest, with a
-  // small penalty per split for the extra lt traffic
   const double slots = 2.0 * kNumSMs;
+  // coarse levels: too few tiles to fill the GPU, so split the 189 offsets
+  // finely (down to one per CTA) and let the U projection sum the blocks
+  if (ctas * 4 < slots) return (int)std::min<int64_t>(189, ceil_div(4 * (int64_t)slots, ctas));
+  // otherwise pick the split count whose last wave (2 CTAs per SM) is
+  // fullest, with a small penalty per split for the extra lt traffic
   int best = 1;
   double best_score = -1e30;
-  for (int s = 1; s <= 189 / 8; ++s) {
+  for (int s = 1; s <= 16; ++s) {
     const double waves = ctas * s / slots;
     const double score = waves / std::ceil(waves) - 0.004 * s;
     if (score > best_score + 1e-12) {

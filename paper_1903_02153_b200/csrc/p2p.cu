@@ -34,13 +34,13 @@ struct KLaplaceForce {
 // exp(-r^2)
 struct KGaussian {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
-    return exp(-(dx * dx + dy * dy + dz * dz));
+    return bfmm_nf::bfmm_exp(-(dx * dx + dy * dy + dz * dz));
   }
 };
 // exp(-r)
 struct KExponential {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
-    return exp(-sqrt(dx * dx + dy * dy + dz * dz));
+    return bfmm_nf::bfmm_exp(-sqrt(dx * dx + dy * dy + dz * dz));
   }
 };
 // log r, r = 0 -> 0
@@ -105,9 +105,10 @@ std::string functor_source(int kind, const char *expr) {
            std::string(expr) + ");";
   else
     body = "return (" + std::string(expr) + ");";
-  return "struct KUser {\n __device__ __forceinline__ static double eval("
-         "double dx, double dy, double dz) {\n " +
-         body + "\n }\n};\n";
+  // exp() in user expressions maps to the branch-free bfmm_exp (p2p.cuh)
+  return "#define exp(x) bfmm_exp(x)\nstruct KUser {\n __device__ __forceinline__ "
+         "static double eval(double dx, double dy, double dz) {\n " +
+         body + "\n }\n};\n#undef exp\n";
 }
 
 int jit_compile(int kind, const char *expr, int *handle) {
