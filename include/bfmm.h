@@ -111,9 +111,12 @@ int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
                   int nsplit, const double *cores, bfmm_stream_t stream);
 
 /* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
- * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ).  symbols (device)
- * (316, q, q, q//2+1) complex128 interleaved. */
-int bfmm_m2l_fft_scratch_bytes(int level, int m, int p, size_t *bytes);
+ * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ) over the valid far
+ * offsets t.  symbols (device) (316, q, q, q//2+1) complex128 interleaved
+ * (the reference's rfftn symbols, ops:156-159).  Scratch for a chunk of
+ * `cols` weight columns (X and Y spectra); bfmm_m2l_fft processes as many
+ * columns per pass as its scratch holds. */
+int bfmm_m2l_fft_scratch_bytes(int level, int cols, int p, size_t *bytes);
 int bfmm_m2l_fft(const double *moments, double *locals, int level, int m,
                  int p, const double *symbols, double scale, void *scratch,
                  size_t scratch_bytes, bfmm_stream_t stream);

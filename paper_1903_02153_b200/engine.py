@@ -267,8 +267,12 @@ class FmmEvaluator:
                                                       blk["UT"].data_ptr(), p3, out.data_ptr(),
                                                       scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
             else:
+                # spectra of a chunk of columns at a time (<= 16 GiB of scratch)
                 nb = _native.C.c_size_t(0)
-                _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, m, p, _native.C.byref(nb)),
+                _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, 1, p, _native.C.byref(nb)),
+                              "bfmm_m2l_fft_scratch_bytes")
+                cc = max(1, min(m, (16 << 30) // max(int(nb.value), 1)))
+                _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, cc, p, _native.C.byref(nb)),
                               "bfmm_m2l_fft_scratch_bytes")
                 scratch = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=self.device)
                 _native.check(self.lib.bfmm_m2l_fft(moments[lev].data_ptr(), out.data_ptr(), lev, m,

@@ -126,6 +126,26 @@ def test_builtin_kernels_match_reference_chebyshev(name, cache_dir):
     assert rel_l2(phi, g[f"direct_{name}"]) < 1e-3
 
 
+@pytest.mark.parametrize("name", ["laplacian", "laplacianforce", "gaussian", "exponential",
+                                  "logarithm"])
+def test_builtin_kernels_match_reference_uniform(name, cache_dir):
+    g = golden("engine")
+    ev = bf.FmmEvaluator(bf.kernel_by_name(name), small_plan(scheme="uniform"), cache_dir=cache_dir)
+    phi = ev.evaluate(g["cloud1500_pts"], weights=g["cloud1500_w"])
+    assert rel_l2(phi, g[f"phi_{name}_uniform"]) < PHI_TOL
+    assert rel_l2(phi, g[f"direct_{name}"]) < 1e-3
+
+
+def test_uniform_level4_multicolumn_matches_reference(cache_dir):
+    g = golden("engine")
+    plan = bf.FmmPlan(levels=4, order=5, scheme="uniform", eps=1e-6,
+                      domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+    got = ev.evaluate(g["u4_pts"], weights=g["u4_w"])
+    assert got.shape == (4000, 3)
+    assert rel_l2(got, g["u4_phi"]) < PHI_TOL
+
+
 def test_distinct_targets_match_reference(cache_dir):
     g = golden("engine")
     ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
@@ -167,7 +187,8 @@ def test_order_sweep_matches_reference(cache_dir):
         assert rel_l2(got, g[f"ord{p}_phi"]) < PHI_TOL, p
 
 
-@pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2)])
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2), ("C3", 2), ("C3", 1),
+                                        ("C5", 2), ("C4", 1)])
 def test_scaled_configs_match_reference(name, scale, cache_dir):
     g = golden(f"{name.lower()}_s{scale}")
     wl = workloads.make(name, scale)
