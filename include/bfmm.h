@@ -70,9 +70,11 @@ int bfmm_gather_weights(const double *w, int64_t n, int m,
 /* P2M leaf_moments (engine.py:159-185).  interp (host) holds the 1-D
  * basis: scheme 0 (Chebyshev) p*p coefficients S[n][j] = c_n T_n(x_j),
  * scheme 1 (uniform) p nodes followed by p*p inverse node differences.
- * geom (host) = {lo_x, lo_y, lo_z, h_leaf}.  moments must be zeroed by the
- * caller; cells without points stay zero.  ref_flag is set when a point's
- * leaf-frame coordinate exceeds 1 + 1e-9 (engine.py:339-345). */
+ * geom (host) = {lo_x, lo_y, lo_z, h_leaf, cell_lo, cell_hi}: only leaves
+ * whose Morton id lies in [cell_lo, cell_hi) are processed (a rank's shard;
+ * [0, 8^L) for all).  moments must be zeroed by the caller; cells without
+ * points stay zero.  ref_flag is set when a point's leaf-frame coordinate
+ * exceeds 1 + 1e-9 (engine.py:339-345). */
 int bfmm_p2m(const double *pts4, const double *wsorted, int m,
              const int64_t *leaves, const int64_t *starts,
              const int64_t *counts, const int64_t *n_leaves,
@@ -105,10 +107,16 @@ int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
  * cores (mma.sync m8n8k4 f64).  The 189 offsets of each cell are split into
  * nsplit contiguous ranges written to separate column blocks:
  * lt has layout (8^level, m, nsplit, rp) and the caller sums the blocks
- * (bfmm_rows_gemm with a_splits = nsplit does it while projecting). */
-int bfmm_m2l_cheb_splits(int level, int m, int rp);
+ * (bfmm_rows_gemm with a_splits = nsplit does it while projecting).
+ * Only target cells whose parent lies in [q_lo, q_lo + nq) are computed (a
+ * rank's Morton shard; q_lo = 0, nq = 8^(level-1) for all); z must hold
+ * every cell.  Warp-specialised: one producer warp gathers z rows and core
+ * tiles with cp.async into an 8-stage mbarrier ring, 8 consumer warps run
+ * the DMMAs. */
+int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq);
 int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
-                  int nsplit, const double *cores, bfmm_stream_t stream);
+                  int nsplit, int64_t q_lo, int64_t nq, const double *cores,
+                  bfmm_stream_t stream);
 
 /* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
  * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ) over the valid far
@@ -118,8 +126,9 @@ int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
  * columns per pass as its scratch holds. */
 int bfmm_m2l_fft_scratch_bytes(int level, int cols, int p, size_t *bytes);
 int bfmm_m2l_fft(const double *moments, double *locals, int level, int m,
-                 int p, const double *symbols, double scale, void *scratch,
-                 size_t scratch_bytes, bfmm_stream_t stream);
+                 int p, const double *symbols, double scale, int64_t q_lo,
+                 int64_t nq, void *scratch, size_t scratch_bytes,
+                 bfmm_stream_t stream);
 
 /* ---- downward pass ----------------------------------------------------- */
 
@@ -128,7 +137,8 @@ int bfmm_l2l(const double *parent, double *child, int64_t n_parent, int p,
              int m, const double *H, bfmm_stream_t stream);
 
 /* L2P read_potentials (engine.py:313-337): phi_sorted[i] =
- * W(x_i) . locals[leaf(i)] (assigns; targets in sorted order). */
+ * W(x_i) . locals[leaf(i)] (assigns; targets in sorted order).  geom as in
+ * bfmm_p2m (rows of leaves outside [cell_lo, cell_hi) are left untouched). */
 int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
              const int64_t *starts, const int64_t *counts,
              const int64_t *n_leaves, int64_t max_leaves, int levels, int p,
@@ -149,16 +159,17 @@ int bfmm_kernel_compile(int kind, const char *expr, int *handle);
 size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves);
 
 /* out[i] = sum over the 27 neighbour leaves of the target leaf of
- * K(x_i - y_j) w_j (assigns every target row), targets and sources both in
- * sorted order.  The source structure is the dense per-cell (start, count)
- * map of bfmm_tree_build. */
+ * K(x_i - y_j) w_j, targets and sources both in sorted order; assigns the
+ * rows of target leaves whose Morton id lies in [cell_lo, cell_hi) (a
+ * rank's shard) and leaves the other rows untouched.  The source structure
+ * is the dense per-cell (start, count) map of bfmm_tree_build. */
 int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
              const int64_t *tstarts, const int64_t *tcounts,
              const int64_t *n_tleaves, int64_t max_tleaves,
              const double *spts4, const double *swsorted, int m,
              const int32_t *scell_start, const int32_t *scell_count,
-             int levels, double *out, void *scratch, size_t scratch_bytes,
-             bfmm_stream_t stream);
+             int levels, int64_t cell_lo, int64_t cell_hi, double *out,
+             void *scratch, size_t scratch_bytes, bfmm_stream_t stream);
 
 /* Locate the first non-finite kernel value in the near field in the
  * reference's enumeration order (offset, target row, source row;

@@ -32,18 +32,19 @@ SIGNATURES = {
     "bfmm_p2m": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_m2m": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
     "bfmm_rows_gemm": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P]),
-    "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I]),
-    "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
+    "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I, _I64]),
+    "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _I64, _I64, _P, _P]),
     "bfmm_device_dmma_probe": (_I, [_DP, _P]),
     "bfmm_device_dmma_sweep": (_I, [_I, _I, _DP, _P]),
     "bfmm_launch_count": (C.c_longlong, []),
     "bfmm_m2l_fft_scratch_bytes": (_I, [_I, _I, _I, C.POINTER(_SZ)]),
-    "bfmm_m2l_fft": (_I, [_P, _P, _I, _I, _I, _P, _D, _P, _SZ, _P]),
+    "bfmm_m2l_fft": (_I, [_P, _P, _I, _I, _I, _P, _D, _I64, _I64, _P, _SZ, _P]),
     "bfmm_l2l": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
     "bfmm_l2p": (_I, [_P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P, _P]),
     "bfmm_kernel_compile": (_I, [_I, C.c_char_p, C.POINTER(_I)]),
     "bfmm_p2p_scratch_bytes": (_SZ, [_I64]),
-    "bfmm_p2p": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _P, _P, _I, _P, _P, _SZ, _P]),
+    "bfmm_p2p": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _P, _P, _I, _I64, _I64, _P, _P,
+                      _SZ, _P]),
     "bfmm_p2p_locate": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _P, _P]),
     "bfmm_scatter_output": (_I, [_P, _P, _P, _I64, _I, _P, _P, _P]),
     "bfmm_far_pairs": (_I, [_I, _I, _P, _P, _P, _P, _SZ, _P]),

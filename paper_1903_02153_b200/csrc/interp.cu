@@ -20,7 +20,14 @@ struct Interp {
 
 struct LeafGeom {
   double lo[3], h, hw;
+  int64_t cell_lo, cell_hi;  // leaf cells this call handles (Morton range)
 };
+
+inline LeafGeom make_leaf_geom(const double *geom) {
+  // host geom = {lo_x, lo_y, lo_z, h_leaf, cell_lo, cell_hi}
+  return LeafGeom{{geom[0], geom[1], geom[2]}, geom[3], 0.5 * geom[3],
+                  (int64_t)geom[4], (int64_t)geom[5]};
+}
 
 // 1-D weights of node j at x (interpolation.py:66-90).  Chebyshev:
 // sum_n T_n(x) S[n][j]; the reference evaluates T_n(x) = cos(n arccos x),
@@ -82,6 +89,7 @@ p2m_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
   const int64_t nl = *n_leaves;
   for (int64_t leaf = blockIdx.x; leaf < nl; leaf += gridDim.x) {
     const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
     const int64_t s0 = starts[leaf], cnt = counts[leaf];
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
@@ -143,6 +151,7 @@ l2p_kernel(const double *__restrict__ pts4, int m,
   const int64_t nl = *n_leaves;
   for (int64_t leaf = blockIdx.x; leaf < nl; leaf += gridDim.x) {
     const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
     const int64_t s0 = starts[leaf], cnt = counts[leaf];
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
@@ -292,6 +301,7 @@ p2m_warp_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
   for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
        leaf += int64_t(gridDim.x) * kLeafWarps) {
     const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
     const int64_t s0 = starts[leaf], cnt = counts[leaf];
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
@@ -353,6 +363,7 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
   for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
        leaf += int64_t(gridDim.x) * kLeafWarps) {
     const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
     const int64_t s0 = starts[leaf], cnt = counts[leaf];
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
@@ -419,7 +430,7 @@ extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
   }
   if (max_leaves <= 0) return 0;
   Interp ip = make_interp(p, scheme, interp);
-  LeafGeom g{{geom[0], geom[1], geom[2]}, geom[3], 0.5 * geom[3]};
+  const LeafGeom g = make_leaf_geom(geom);
   if (p <= kWarpP) {
     p2m_warp_kernel<<<grid_cap(ceil_div(max_leaves, kLeafWarps), 16), 32 * kLeafWarps, 0,
                       as_stream(stream)>>>(pts4, wsorted, m, leaves, starts, counts,
@@ -453,7 +464,7 @@ extern "C" int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
   }
   if (max_leaves <= 0) return 0;
   Interp ip = make_interp(p, scheme, interp);
-  LeafGeom g{{geom[0], geom[1], geom[2]}, geom[3], 0.5 * geom[3]};
+  const LeafGeom g = make_leaf_geom(geom);
   if (p <= kWarpP) {
     l2p_warp_kernel<<<grid_cap(ceil_div(max_leaves, kLeafWarps), 16), 32 * kLeafWarps, 0,
                       as_stream(stream)>>>(pts4, m, leaves, starts, counts, n_leaves, ip,

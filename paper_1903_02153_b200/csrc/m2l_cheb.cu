@@ -199,7 +199,6 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-#include "m2l_dmma.cuh"
 #include "m2l_ws.cuh"
 
 // ----------------------------------------------------------------------------
@@ -307,11 +306,9 @@ extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
   return check_launch("rows_gemm_kernel");
 }
 
-extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp) {
-  const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
-  const M2LConfig c = m2l_config(level, m, rp);
-  const int64_t ctas =
-      ceil_div(rows, rows <= 64 ? 64 : 128) * ceil_div(rp, 8 * c.nt8) * 8;
+extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq) {
+  const int64_t rows = nq * m;
+  const int64_t ctas = ceil_div(rows, 64 * m2l_mw(rows)) * ceil_div(rp, 8 * m2l_nt8(rp)) * 8;
   const double slots = 2.0 * kNumSMs;
   // coarse levels: too few tiles to fill the GPU, so split the 189 offsets
   // finely (down to one per CTA) and let the U projection sum the blocks
@@ -332,8 +329,8 @@ extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp) {
 }
 
 extern "C" int bfmm_m2l_cheb(const double *z, double *lt, int level, int m,
-                             int rp, int nsplit, const double *cores,
-                             bfmm_stream_t stream) {
+                             int rp, int nsplit, int64_t q_lo, int64_t nq,
+                             const double *cores, bfmm_stream_t stream) {
   if (rp % 8 != 0 || rp <= 0 || level < 2 || level > 10) {
     set_error("bfmm_m2l_cheb: rp=%d must be a positive multiple of 8, level=%d",
               rp, level);
@@ -343,12 +340,13 @@ extern "C" int bfmm_m2l_cheb(const double *z, double *lt, int level, int m,
     set_error("bfmm_m2l_cheb: nsplit=%d outside [1, 189]", nsplit);
     return 2;
   }
+  const int64_t nparent = int64_t(1) << (3 * level - 3);
+  if (q_lo < 0 || nq < 0 || q_lo + nq > nparent) {
+    set_error("bfmm_m2l_cheb: parent range [%lld, %lld) outside [0, %lld)",
+              (long long)q_lo, (long long)(q_lo + nq), (long long)nparent);
+    return 2;
+  }
   ensure_offsets();
-  const M2LConfig c = m2l_config(level, m, rp);
-  static const char *which = getenv("BFMM_M2L_KERNEL");
-  if (which && which[0] == 's')  // "sync": CTA-barrier pipeline variant
-    return dispatch_m2l(c, z, lt, level, m, rp, nsplit, cores, as_stream(stream));
-  const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
-  return dispatch_ws(rows <= 64 ? 1 : 2, c.nt8, z, lt, level, m, rp, nsplit, cores,
-                     as_stream(stream));
+  M2LCall a{z, lt, level, m, rp, nsplit, q_lo, nq, cores, as_stream(stream)};
+  return dispatch_ws(m2l_mw(nq * m), m2l_nt8(rp), a);
 }

@@ -109,16 +109,18 @@ void ensure_off() {
 // reads 32 consecutive bins of one source spectrum and of one symbol.
 __global__ void __launch_bounds__(256)
 hadamard_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y,
-                int level, int cc, int F, const double2 *__restrict__ S) {
+                int level, int cc, int F, const double2 *__restrict__ S,
+                int64_t cell_lo, int64_t ncell) {
+  // targets: cells [cell_lo, cell_lo + ncell); X holds every cell
   const int n = 1 << level;
-  const int64_t ncell = int64_t(1) << (3 * level);
   const int64_t total = ncell * cc * F;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t cw = e / F;
     const int f = (int)(e - cw * F);
-    const int64_t cell = cw / cc;
-    const int col = (int)(cw - cell * cc);
+    const int64_t rel = cw / cc;
+    const int col = (int)(cw - rel * cc);
+    const int64_t cell = cell_lo + rel;
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
     double re = 0.0, im = 0.0;
@@ -137,16 +139,18 @@ hadamard_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y,
 
 // ---- 3. inverse transform + crop + scale: one CTA per (cell, column) ---------
 __global__ void __launch_bounds__(128)
-fft_inv_kernel(const double2 *__restrict__ Y, int64_t ncell, int m, int c0,
-               int cc, FftGeom g, double scale, double *__restrict__ locals) {
+fft_inv_kernel(const double2 *__restrict__ Y, int64_t cell_lo, int64_t ncell,
+               int m, int c0, int cc, FftGeom g, double scale,
+               double *__restrict__ locals) {
   extern __shared__ double2 sm2[];
   const int p = g.p, q = g.q, h = g.h, F = q * q * h;
   double2 *C = sm2;            // [p][q][h]   x inverted, i < p
   double2 *D = C + p * q * h;  // [p][p][h]   y inverted, j < p
   const double norm = scale / ((double)q * q * q);
   for (int64_t w = blockIdx.x; w < ncell * cc; w += gridDim.x) {
-    const int64_t cell = w / cc;
-    const int col = c0 + (int)(w - cell * cc);
+    const int64_t rel = w / cc;
+    const int col = c0 + (int)(w - rel * cc);
+    const int64_t cell = cell_lo + rel;
     const double2 *src = Y + w * (int64_t)F;
     __syncthreads();
     // x: q bins -> p outputs, e^{+2 pi i i kx / q}
@@ -219,8 +223,8 @@ extern "C" int bfmm_m2l_fft_scratch_bytes(int level, int cc, int p, size_t *byte
 
 extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
                             int m, int p, const double *symbols, double scale,
-                            void *scratch, size_t scratch_bytes,
-                            bfmm_stream_t stream) {
+                            int64_t q_lo, int64_t nq, void *scratch,
+                            size_t scratch_bytes, bfmm_stream_t stream) {
   if (p < 2 || p > 12 || level < 2 || level > 10) {
     set_error("bfmm_m2l_fft: unsupported p=%d level=%d", p, level);
     return 2;
@@ -248,12 +252,15 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
     const unsigned gcell = (unsigned)std::min<int64_t>(work, kNumSMs * 16);
     fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, ncell, m, c0, ccur, g, X);
     if (check_launch("fft_fwd_kernel")) return 1;
-    const int64_t tot = work * F;
-    const unsigned gh = (unsigned)std::min<int64_t>(ceil_div(tot, 256), kNumSMs * 64);
+    const int64_t tgt = 8 * nq * ccur;
+    const unsigned gh = (unsigned)std::min<int64_t>(ceil_div(tgt * F, 256), kNumSMs * 64);
     hadamard_kernel<<<gh, 256, 0, st>>>(X, Y, level, ccur, (int)F,
-                                        reinterpret_cast<const double2 *>(symbols));
+                                        reinterpret_cast<const double2 *>(symbols),
+                                        8 * q_lo, 8 * nq);
     if (check_launch("hadamard_kernel")) return 1;
-    fft_inv_kernel<<<gcell, 128, smem_i, st>>>(Y, ncell, m, c0, ccur, g, scale, locals);
+    const unsigned gi = (unsigned)std::min<int64_t>(std::max<int64_t>(tgt, 1), kNumSMs * 16);
+    fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, 8 * q_lo, 8 * nq, m, c0, ccur, g, scale,
+                                            locals);
     if (check_launch("fft_inv_kernel")) return 1;
   }
   return 0;

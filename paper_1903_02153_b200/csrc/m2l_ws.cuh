@@ -53,7 +53,8 @@ struct WsShape {
 template <int NT8, int MW>
 __global__ void __launch_bounds__(WsShape<NT8, MW>::threads, 2)
 m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
-              int m, int rp, int nsplit, const double *__restrict__ cores) {
+              int m, int rp, int nsplit, int64_t q_lo, int64_t nq,
+              const double *__restrict__ cores) {
   using S = WsShape<NT8, MW>;
   constexpr int TM = S::TM, TNc = S::TN, LDK = S::LDK;
   extern __shared__ __align__(16) double sm[];
@@ -64,7 +65,8 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
   const int per = (189 + nsplit - 1) / nsplit;
   const int v_lo = split * per, v_hi = min(189, v_lo + per);
   const int n = 1 << level;
-  const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
+  // rows: (parent q in [q_lo, q_lo + nq), column) of target cells 8q + o
+  const int64_t rows = nq * m;
   const int64_t row0 = int64_t(blockIdx.x) * TM;
   const int n0 = blockIdx.y * TNc;
   const int groups = rp >> 3;
@@ -93,7 +95,7 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
       if (rok[i]) {
         const int64_t q = r / m;
         colm[i] = (int)(r - q * m);
-        unmorton3((uint64_t)(8 * q + o), cx[i], cy[i], cz[i]);
+        unmorton3((uint64_t)(8 * (q_lo + q) + o), cx[i], cy[i], cz[i]);
       }
     }
     int64_t srow[RPL];
@@ -177,7 +179,7 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
     if (r >= rows) continue;
     const int64_t q = r / m;
     const int c = (int)(r - q * m);
-    double *dst = lt + (((8 * q + o) * m + c) * nsplit + split) * rp;
+    double *dst = lt + (((8 * (q_lo + q) + o) * m + c) * nsplit + split) * rp;
 #pragma unroll
     for (int j = 0; j < NT8; ++j) {
       const int col = n0 + j * 8 + 2 * t4;
@@ -188,9 +190,17 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
   }
 }
 
+struct M2LCall {
+  const double *z;
+  double *lt;
+  int level, m, rp, nsplit;
+  int64_t q_lo, nq;  // target parents [q_lo, q_lo + nq) at level - 1
+  const double *cores;
+  cudaStream_t st;
+};
+
 template <int NT8, int MW>
-int launch_ws(const double *z, double *lt, int level, int m, int rp, int nsplit,
-              const double *cores, cudaStream_t st) {
+int launch_ws(const M2LCall &a) {
   using S = WsShape<NT8, MW>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -198,31 +208,38 @@ int launch_ws(const double *z, double *lt, int level, int m, int rp, int nsplit,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
     attr_set = true;
   }
-  const int64_t rows = (int64_t(1) << (3 * level - 3)) * m;
-  dim3 grid((unsigned)ceil_div(rows, S::TM), (unsigned)ceil_div(rp, S::TN), 8 * nsplit);
-  m2l_ws_kernel<NT8, MW><<<grid, S::threads, S::smem, st>>>(z, lt, level, m, rp,
-                                                           nsplit, cores);
+  const int64_t rows = a.nq * a.m;
+  if (rows <= 0) return 0;
+  dim3 grid((unsigned)ceil_div(rows, S::TM), (unsigned)ceil_div(a.rp, S::TN), 8 * a.nsplit);
+  m2l_ws_kernel<NT8, MW><<<grid, S::threads, S::smem, a.st>>>(
+      a.z, a.lt, a.level, a.m, a.rp, a.nsplit, a.q_lo, a.nq, a.cores);
   return check_launch("m2l_ws_kernel");
 }
 
 template <int MW>
-int dispatch_ws_nt8(int nt8, const double *z, double *lt, int level, int m, int rp,
-                    int nsplit, const double *cores, cudaStream_t st) {
+int dispatch_ws_nt8(int nt8, const M2LCall &a) {
   switch (nt8) {
-    case 1: return launch_ws<1, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    case 2: return launch_ws<2, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    case 3: return launch_ws<3, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    case 4: return launch_ws<4, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    case 5: return launch_ws<5, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    case 6: return launch_ws<6, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    case 7: return launch_ws<7, MW>(z, lt, level, m, rp, nsplit, cores, st);
-    default: return launch_ws<8, MW>(z, lt, level, m, rp, nsplit, cores, st);
+    case 1: return launch_ws<1, MW>(a);
+    case 2: return launch_ws<2, MW>(a);
+    case 3: return launch_ws<3, MW>(a);
+    case 4: return launch_ws<4, MW>(a);
+    case 5: return launch_ws<5, MW>(a);
+    case 6: return launch_ws<6, MW>(a);
+    case 7: return launch_ws<7, MW>(a);
+    default: return launch_ws<8, MW>(a);
   }
 }
 
-inline int dispatch_ws(int mw, int nt8, const double *z, double *lt, int level,
-                       int m, int rp, int nsplit, const double *cores,
-                       cudaStream_t st) {
-  if (mw == 1) return dispatch_ws_nt8<1>(nt8, z, lt, level, m, rp, nsplit, cores, st);
-  return dispatch_ws_nt8<2>(nt8, z, lt, level, m, rp, nsplit, cores, st);
+// Column-tile width: the whole rank when rp <= 64, else 56- or 64-wide
+// tiles, whichever pads less.  Row tiles: 128 rows, or 64 on tiny levels.
+inline int m2l_nt8(int rp) {
+  if (rp <= 64) return rp / 8;
+  const int w7 = (int)(ceil_div(rp, 56) * 56 - rp), w8 = (int)(ceil_div(rp, 64) * 64 - rp);
+  return w7 < w8 ? 7 : 8;
+}
+inline int m2l_mw(int64_t rows) { return rows <= 64 ? 1 : 2; }
+
+inline int dispatch_ws(int mw, int nt8, const M2LCall &a) {
+  if (mw == 1) return dispatch_ws_nt8<1>(nt8, a);
+  return dispatch_ws_nt8<2>(nt8, a);
 }

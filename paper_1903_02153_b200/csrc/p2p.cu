@@ -268,14 +268,18 @@ int launch_locate(int handle, const bfmm_nf::Args &a,
   return check_launch("locate_kernel");
 }
 
+// 32-target chunks per target leaf; leaves outside [cell_lo, cell_hi) (other
+// ranks' shards) get none.
 __global__ void chunk_counts_kernel(const int64_t *__restrict__ counts,
+                                    const int64_t *__restrict__ leaves,
                                     const int64_t *__restrict__ n_leaves,
-                                    int64_t max_leaves,
-                                    int64_t *__restrict__ nch) {
+                                    int64_t max_leaves, int64_t cell_lo,
+                                    int64_t cell_hi, int64_t *__restrict__ nch) {
   const int64_t nl = *n_leaves;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
        i < max_leaves; i += int64_t(gridDim.x) * blockDim.x)
-    nch[i] = i < nl ? (counts[i] + 31) / 32 : 0;
+    nch[i] = (i < nl && leaves[i] >= cell_lo && leaves[i] < cell_hi)
+                 ? (counts[i] + 31) / 32 : 0;
 }
 
 __global__ void scatter_kernel(const double *__restrict__ far,
@@ -405,8 +409,9 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
                         const int64_t *n_tleaves, int64_t max_tleaves,
                         const double *spts4, const double *swsorted, int m,
                         const int32_t *scell_start, const int32_t *scell_count,
-                        int levels, double *out, void *scratch,
-                        size_t scratch_bytes, bfmm_stream_t stream) {
+                        int levels, int64_t cell_lo, int64_t cell_hi,
+                        double *out, void *scratch, size_t scratch_bytes,
+                        bfmm_stream_t stream) {
   if (max_tleaves <= 0) return 0;
   size_t cub_off;
   size_t need = p2p_scratch(max_tleaves, &cub_off);
@@ -419,7 +424,8 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
   int64_t *incl = nch + max_tleaves;
   chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256),
                                                     kNumSMs * 16),
-                        256, 0, st>>>(tcounts, n_tleaves, max_tleaves, nch);
+                        256, 0, st>>>(tcounts, tleaves, n_tleaves, max_tleaves,
+                                      cell_lo, cell_hi, nch);
   if (check_launch("chunk_counts_kernel")) return 1;
   size_t cb = need - cub_off;
   if (cub::DeviceScan::InclusiveSum(static_cast<char *>(scratch) + cub_off, cb,

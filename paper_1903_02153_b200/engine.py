@@ -219,14 +219,19 @@ class FmmEvaluator:
                      cell_count, min(n, ncell))
 
     # -- stages -----------------------------------------------------------------
-    def _upward(self, tree, ws, m, status):
+    def _cells(self, lev, shard):
+        """[lo, hi) cells of this call's shard at a level (all cells if unsharded)."""
+        return (0, 1 << (3 * lev)) if shard is None else shard[0].cells(lev)
+
+    def _upward(self, tree, ws, m, status, shard):
         torch = _torch()
         L, p = self.plan.levels, self.plan.order
         p3 = p ** 3
         moments = {L: torch.zeros(((1 << (3 * L)) * m * p3,), dtype=torch.float64, device=self.device)}
         st = self._stream()
-        leaf_geom = np.ascontiguousarray(np.concatenate([self.plan.domain.low,
-                                                         [self.plan.domain.length / (1 << L)]]))
+        lo, hi = self._cells(L, shard)
+        leaf_geom = np.ascontiguousarray(np.concatenate(
+            [self.plan.domain.low, [self.plan.domain.length / (1 << L), float(lo), float(hi)]]))
         _native.check(self.lib.bfmm_p2m(
             tree.pts4.data_ptr(), ws.data_ptr(), m, tree.leaves.data_ptr(),
             tree.starts.data_ptr(), tree.counts.data_ptr(), tree.n_leaves.data_ptr(),
@@ -235,12 +240,15 @@ class FmmEvaluator:
             "bfmm_p2m")
         for lev in range(L, 2, -1):
             npar = 1 << (3 * (lev - 1))
-            moments[lev - 1] = torch.empty((npar * m * p3,), dtype=torch.float64, device=self.device)
-            _native.check(self.lib.bfmm_m2m(moments[lev].data_ptr(), moments[lev - 1].data_ptr(),
-                                            npar, p, m, _native.dptr(self._H), st), "bfmm_m2m")
+            qlo, qhi = self._cells(lev - 1, shard)  # parents of this shard's cells
+            row = m * p3
+            moments[lev - 1] = torch.empty((npar * row,), dtype=torch.float64, device=self.device)
+            _native.check(self.lib.bfmm_m2m(
+                moments[lev][8 * qlo * row:].data_ptr(), moments[lev - 1][qlo * row:].data_ptr(),
+                qhi - qlo, p, m, _native.dptr(self._H), st), "bfmm_m2m")
         return moments, leaf_geom
 
-    def _far_field(self, moments, m):
+    def _far_field(self, moments, m, shard):
         torch = _torch()
         L, p = self.plan.levels, self.plan.order
         p3 = p ** 3
@@ -250,23 +258,30 @@ class FmmEvaluator:
             blk = self._dev_block(lev)
             scale = float(self.table.scale_for_level(lev))
             ncell = 1 << (3 * lev)
+            lo, hi = self._cells(lev, shard)
+            nloc = hi - lo
             out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
             if blk["kind"] == "cheb":
                 rp = blk["rp"]
-                ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp))
+                ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nloc // 8))
                 z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
                 lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
-                _native.check(self.lib.bfmm_rows_gemm(moments[lev].data_ptr(), ncell * m, p3,
-                                                      blk["V"].data_ptr(), rp, z.data_ptr(),
-                                                      1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+                _native.check(self.lib.bfmm_rows_gemm(
+                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                    z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+                if shard is not None and not shard[0].full:
+                    shard[1].allgather_cells(z, m * rp, lev)  # sources from every shard
                 e0 = self._kevent()
                 _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
-                                                     blk["cores"].data_ptr(), st), "bfmm_m2l_cheb")
+                                                     lo // 8, nloc // 8, blk["cores"].data_ptr(),
+                                                     st), "bfmm_m2l_cheb")
                 self._kspan(f"m2l_l{lev}", e0)
-                _native.check(self.lib.bfmm_rows_gemm(lt.data_ptr(), ncell * m, rp,
-                                                      blk["UT"].data_ptr(), p3, out.data_ptr(),
-                                                      scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
+                _native.check(self.lib.bfmm_rows_gemm(
+                    lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
+                    out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
             else:
+                if shard is not None and not shard[0].full:
+                    shard[1].allgather_cells(moments[lev], m * p3, lev)
                 # spectra of a chunk of columns at a time (<= 16 GiB of scratch)
                 nb = _native.C.c_size_t(0)
                 _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, 1, p, _native.C.byref(nb)),
@@ -275,19 +290,24 @@ class FmmEvaluator:
                 _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, cc, p, _native.C.byref(nb)),
                               "bfmm_m2l_fft_scratch_bytes")
                 scratch = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=self.device)
+                e0 = self._kevent()
                 _native.check(self.lib.bfmm_m2l_fft(moments[lev].data_ptr(), out.data_ptr(), lev, m,
-                                                    p, blk["symbols"].data_ptr(), scale,
-                                                    scratch.data_ptr(), int(nb.value), st),
-                              "bfmm_m2l_fft")
+                                                    p, blk["symbols"].data_ptr(), scale, lo // 8,
+                                                    nloc // 8, scratch.data_ptr(), int(nb.value),
+                                                    st), "bfmm_m2l_fft")
+                self._kspan(f"m2lfft_l{lev}", e0)
             locs[lev] = out
         return locs
 
-    def _downward(self, locs, tree, m, leaf_geom, status, phi_far):
+    def _downward(self, locs, tree, m, leaf_geom, status, phi_far, shard):
         L, p = self.plan.levels, self.plan.order
         st = self._stream()
+        row = m * p ** 3
         for lev in range(2, L):
-            _native.check(self.lib.bfmm_l2l(locs[lev].data_ptr(), locs[lev + 1].data_ptr(),
-                                            1 << (3 * lev), p, m, _native.dptr(self._H), st),
+            qlo, qhi = self._cells(lev, shard)
+            _native.check(self.lib.bfmm_l2l(locs[lev][qlo * row:].data_ptr(),
+                                            locs[lev + 1][8 * qlo * row:].data_ptr(),
+                                            qhi - qlo, p, m, _native.dptr(self._H), st),
                           "bfmm_l2l")
         _native.check(self.lib.bfmm_l2p(
             tree.pts4.data_ptr(), m, tree.leaves.data_ptr(), tree.starts.data_ptr(),
@@ -295,18 +315,19 @@ class FmmEvaluator:
             self._scheme_id, _native.dptr(self._interp), _native.dptr(leaf_geom),
             locs[L].data_ptr(), phi_far.data_ptr(), status[_ST_REF:].data_ptr(), st), "bfmm_l2p")
 
-    def _near_field(self, ttree, stree, ws, m, near):
+    def _near_field(self, ttree, stree, ws, m, near, shard):
         torch = _torch()
         st = self._stream()
         sb = self.lib.bfmm_p2p_scratch_bytes(max(ttree.max_leaves, 1))
         scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        lo, hi = self._cells(self.plan.levels, shard)
         e0 = self._kevent()
         _native.check(self.lib.bfmm_p2p(
             self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(), ttree.starts.data_ptr(),
             ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(), ttree.max_leaves,
             stree.pts4.data_ptr(), ws.data_ptr(), m, stree.cell_start.data_ptr(),
-            stree.cell_count.data_ptr(), self.plan.levels, near.data_ptr(), scratch.data_ptr(),
-            sb, st), "bfmm_p2p")
+            stree.cell_count.data_ptr(), self.plan.levels, lo, hi, near.data_ptr(),
+            scratch.data_ptr(), sb, st), "bfmm_p2p")
         self._kspan("p2p", e0)
 
     # per-kernel CUDA events on the launching (current) stream, enabled by
@@ -328,9 +349,13 @@ class FmmEvaluator:
         self._kpending.append((name, e0, e1))
 
     # -- driver -----------------------------------------------------------------
-    def evaluate(self, sources, targets=None, weights=None):
-        """phi[i, c] = sum_j K(x_i, y_j) w[j, c] (reference engine.py:482-536)."""
+    def evaluate(self, sources, targets=None, weights=None, _shard=None):
+        """phi[i, c] = sum_j K(x_i, y_j) w[j, c] (reference engine.py:482-536).
+
+        ``_shard`` = (MortonShards, ShardComm) runs this call as one rank of a
+        multi-GPU matvec (paper_1903_02153_b200.parallel.ShardedEvaluator)."""
         torch = _torch()
+        sharded = _shard is not None and not _shard[0].full
         shared = targets is None or targets is sources
         as_tensor = isinstance(sources, torch.Tensor)
         out_device = sources.device if as_tensor else None
@@ -366,20 +391,23 @@ class FmmEvaluator:
                                                    ws.data_ptr(), stree.pts4.data_ptr(), st),
                       "bfmm_gather_weights")
         ev[2].record()
-        moments, leaf_geom = self._upward(stree, ws, m, status)
+        shard = _shard if sharded else None
+        moments, leaf_geom = self._upward(stree, ws, m, status, shard)
         ev[3].record()
         phi_far = None
+        # sharded: rows of other ranks' targets must read as zero
+        alloc = torch.zeros if sharded else torch.empty
         if not self._disable_far_field:
-            locs = self._far_field(moments, m)
+            locs = self._far_field(moments, m, shard)
             ev[4].record()
-            phi_far = torch.empty((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
-            self._downward(locs, ttree, m, leaf_geom, status, phi_far)
+            phi_far = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
+            self._downward(locs, ttree, m, leaf_geom, status, phi_far, shard)
         else:
             locs = None
             ev[4].record()
         ev[5].record()
-        near = torch.empty((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
-        self._near_field(ttree, stree, ws, m, near)
+        near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
+        self._near_field(ttree, stree, ws, m, near, shard)
         phi = torch.empty((n_tgt, m), dtype=torch.float64, device=self.device)
         _native.check(self.lib.bfmm_scatter_output(
             phi_far.data_ptr() if phi_far is not None else None, near.data_ptr(),
@@ -390,6 +418,8 @@ class FmmEvaluator:
             ttree.leaves.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
             ttree.max_leaves, stree.cell_count.data_ptr(), self.plan.levels,
             pairs_dev.data_ptr(), st), "bfmm_near_pair_count")
+        if sharded:
+            _shard[1].allreduce_sum(phi)  # every rank wrote only its own targets
         ev[6].record()
         if self.keep_stages:
             self.stages = {"stree": stree, "ttree": ttree, "moments": moments, "locals": locs,

@@ -34,7 +34,7 @@ def test_library_loads_and_exports_every_header_symbol():
 
 def test_library_reports_config_errors_without_a_gpu():
     lib = _native.load()
-    rc = lib.bfmm_m2l_cheb(None, None, 3, 1, 13, None, None)  # rp not a multiple of 8
+    rc = lib.bfmm_m2l_cheb(None, None, 3, 1, 13, 1, 0, 8, None, None)  # rp not a multiple of 8
     assert rc != 0
     assert b"multiple" in lib.bfmm_last_error()
 

@@ -1,0 +1,137 @@
+"""Multi-GPU path: Morton-range shards and their two exchanges.
+
+CPU: shard arithmetic, and ShardComm over a real world-size-2 gloo group
+(the same torch.distributed calls NCCL runs on the GPU box).
+GPU: the sharded matvec with 2 and 4 ranks emulated as host threads on one
+device (each rank on its own stream; the exchanges synchronise on the host,
+no kernel ever waits on another rank), against the unsharded result.
+"""
+
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2, unit_cloud
+from paper_1903_02153_b200.parallel import MortonShards, ShardComm, shard_range
+
+
+def test_shard_ranges_partition_and_nest():
+    for world in (1, 2, 4, 8):
+        for lev in (2, 3, 5):
+            cover = []
+            for r in range(world):
+                lo, hi = MortonShards(world, r).cells(lev)
+                cover.append((lo, hi))
+                plo, phi = MortonShards(world, r).cells(lev - 1) if lev > 2 else (lo // 8, hi // 8)
+                assert (lo, hi) == (8 * plo, 8 * phi)  # children of the parent range
+            assert cover[0][0] == 0 and cover[-1][1] == 8 ** lev
+            assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+    with pytest.raises(ValueError):
+        MortonShards(3, 0)
+    with pytest.raises(ValueError):
+        shard_range(64, 5, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, results):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = ShardComm(dist)
+    lev, row = 2, 3
+    full = torch.zeros(8 ** lev * row, dtype=torch.float64)
+    lo, hi = shard_range(8 ** lev, world, rank)
+    full[lo * row:hi * row] = torch.arange(lo * row, hi * row, dtype=torch.float64)
+    comm.allgather_cells(full, row, lev)
+    phi = torch.zeros(10, dtype=torch.float64)
+    phi[rank::world] = rank + 1.0
+    comm.allreduce_sum(phi)
+    results[rank] = (full.numpy().copy(), phi.numpy().copy())
+    dist.destroy_process_group()
+
+
+def test_shard_comm_over_gloo_world2():
+    import torch.multiprocessing as mp
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_gloo_worker, args=(world, port, results), nprocs=world, join=True)
+    for r in range(world):
+        full, phi = results[r]
+        assert np.array_equal(full, np.arange(64 * 3, dtype=np.float64))
+        assert np.array_equal(phi, np.array([1.0, 2.0] * 5))
+
+
+class ThreadComm:
+    """ShardComm stand-in for ranks running as threads on one GPU."""
+
+    def __init__(self, world, rank, board, barrier):
+        self.world, self.rank, self.board, self.barrier = world, rank, board, barrier
+
+    def allgather_cells(self, full, row_elems, level):
+        torch.cuda.current_stream().synchronize()
+        self.board[self.rank] = full
+        self.barrier.wait()
+        for r in range(self.world):
+            if r != self.rank:
+                lo, hi = shard_range(8 ** level, self.world, r)
+                full[lo * row_elems:hi * row_elems].copy_(
+                    self.board[r][lo * row_elems:hi * row_elems])
+        torch.cuda.current_stream().synchronize()
+        self.barrier.wait()
+        return full
+
+    def allreduce_sum(self, t):
+        torch.cuda.current_stream().synchronize()
+        self.board[self.rank] = t.clone()
+        self.barrier.wait()
+        total = sum(self.board[r] for r in range(self.world))
+        self.barrier.wait()
+        t.copy_(total)
+        return t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,scheme", [(2, "chebyshev"), (4, "chebyshev"), (2, "uniform")])
+def test_sharded_matvec_matches_unsharded(world, scheme, cache_dir):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1903_02153_b200 as bf
+    pts, w = unit_cloud(30000, seed=51, ncols=2)
+    plan = bf.FmmPlan(levels=4, order=4, scheme=scheme, eps=1e-6,
+                      domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ref = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir).evaluate(pts, weights=w)
+    board, barrier = {}, threading.Barrier(world)
+    out, errs = {}, []
+
+    def rank_main(r):
+        try:
+            ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = ev.evaluate(pts, weights=w, _shard=(MortonShards(world, r),
+                                                             ThreadComm(world, r, board, barrier)))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+            barrier.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for r in range(world):
+        assert rel_l2(out[r], ref) < 1e-13
