@@ -277,126 +277,7 @@ l2l_kernel(const double *__restrict__ parent, double *__restrict__ child,
   }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-per-leaf P2M / L2P for p <= 8 (the production path).  A warp owns one
-// leaf at a time; lanes compute the 3 x p one-dimensional weights of up to 32
-// points into the warp's shared slice, then P2M lanes each own up to
-// kMaxU = 16 of the p^3 node outputs (sum over the leaf's points in sorted
-// order), and L2P lanes own points and contract the leaf's locals.
-constexpr int kWarpP = 8, kMaxU = (kWarpP * kWarpP * kWarpP + 31) / 32;
 constexpr int kLeafWarps = 4;
-
-__global__ void __launch_bounds__(32 * kLeafWarps)
-p2m_warp_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
-                int m, const int64_t *__restrict__ leaves,
-                const int64_t *__restrict__ starts,
-                const int64_t *__restrict__ counts,
-                const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
-                double *__restrict__ moments, int32_t *flag) {
-  __shared__ double s_w[kLeafWarps][32][3 * kWarpP];
-  __shared__ double s_v[kLeafWarps][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p = ip.p, p3 = p * p * p, U = (p3 + 31) / 32;
-  const int64_t nl = *n_leaves;
-  for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
-       leaf += int64_t(gridDim.x) * kLeafWarps) {
-    const int64_t cell = leaves[leaf];
-    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
-    const int64_t s0 = starts[leaf], cnt = counts[leaf];
-    int cx, cy, cz;
-    unmorton3((uint64_t)cell, cx, cy, cz);
-    // node index of each owned output and its (i, j, k)
-    for (int c = 0; c < m; ++c) {
-      double acc[kMaxU];
-#pragma unroll
-      for (int u = 0; u < kMaxU; ++u) acc[u] = 0.0;
-      for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
-        const int nb = (int)(cnt - c0 < 32 ? cnt - c0 : 32);
-        __syncwarp();
-        if (lane < nb) {
-          const int64_t i = s0 + c0 + lane;
-          // weights are recomputed per column: cheaper than keeping m x p^3
-          // accumulators live (recurrence, no transcendentals)
-          const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
-          weights_1d(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), &s_w[wid][lane][0]);
-          weights_1d(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), &s_w[wid][lane][p]);
-          weights_1d(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), &s_w[wid][lane][2 * p]);
-          s_v[wid][lane] = ws[i * m + c];
-        }
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < kMaxU; ++u) {
-          const int a = lane + 32 * u;
-          if (u < U && a < p3) {
-            const int ii = a / (p * p), jj = (a / p) % p, kk = a % p;
-            double s = acc[u];
-            for (int t = 0; t < nb; ++t) {
-              const double *wt = s_w[wid][t];
-              s += ((wt[ii] * wt[p + jj]) * wt[2 * p + kk]) * s_v[wid][t];
-            }
-            acc[u] = s;
-          }
-        }
-      }
-      double *dst = moments + (cell * m + c) * (int64_t)p3;
-#pragma unroll
-      for (int u = 0; u < kMaxU; ++u) {
-        const int a = lane + 32 * u;
-        if (u < U && a < p3) dst[a] = acc[u];
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(32 * kLeafWarps)
-l2p_warp_kernel(const double *__restrict__ pts4, int m,
-                const int64_t *__restrict__ leaves,
-                const int64_t *__restrict__ starts,
-                const int64_t *__restrict__ counts,
-                const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
-                const double *__restrict__ locals, double *__restrict__ phi,
-                int32_t *flag) {
-  __shared__ double s_L[kLeafWarps][kWarpP * kWarpP * kWarpP];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p = ip.p, p3 = p * p * p;
-  const int64_t nl = *n_leaves;
-  for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
-       leaf += int64_t(gridDim.x) * kLeafWarps) {
-    const int64_t cell = leaves[leaf];
-    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
-    const int64_t s0 = starts[leaf], cnt = counts[leaf];
-    int cx, cy, cz;
-    unmorton3((uint64_t)cell, cx, cy, cz);
-    for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
-      const bool have = c0 + lane < cnt;
-      const int64_t i = s0 + c0 + lane;
-      double wx[kWarpP], wy[kWarpP], wz[kWarpP];
-      if (have) {
-        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
-        weights_1d(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), wx);
-        weights_1d(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), wy);
-        weights_1d(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), wz);
-      }
-      for (int c = 0; c < m; ++c) {
-        __syncwarp();
-        const double *src = locals + (cell * m + c) * (int64_t)p3;
-        for (int a = lane; a < p3; a += 32) s_L[wid][a] = src[a];
-        __syncwarp();
-        if (have) {
-          const double *L = s_L[wid];
-          double s = 0.0;
-          int a = 0;
-          for (int ii = 0; ii < p; ++ii)
-            for (int jj = 0; jj < p; ++jj) {
-              const double wxy = wx[ii] * wy[jj];
-              for (int kk = 0; kk < p; ++kk, ++a) s = fma(wxy * wz[kk], L[a], s);
-            }
-          phi[i * m + c] = s;
-        }
-      }
-    }
-  }
-}
 
 Interp make_interp(int p, int scheme, const double *host) {
   Interp ip{};
@@ -411,6 +292,8 @@ int grid_cap(int64_t work, int per_sm) {
   int64_t cap = int64_t(kNumSMs) * per_sm;
   return (int)(work < 1 ? 1 : (work < cap ? work : cap));
 }
+
+#include "leaf_kernels.cuh"
 
 }  // namespace
 }  // namespace bfmm
@@ -431,11 +314,10 @@ extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
   if (max_leaves <= 0) return 0;
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
-  if (p <= kWarpP) {
-    p2m_warp_kernel<<<grid_cap(ceil_div(max_leaves, kLeafWarps), 16), 32 * kLeafWarps, 0,
-                      as_stream(stream)>>>(pts4, wsorted, m, leaves, starts, counts,
-                                           n_leaves, ip, g, moments, ref_flag);
-    return check_launch("p2m_warp_kernel");
+  if (p >= 2 && p <= 8) {
+    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, ip, g,
+               nullptr, moments, ref_flag, as_stream(stream)};
+    return dispatch_leaf(p, true, a);
   }
   if (m * p * p * p > 27 * kLeafThreads) {
     set_error("bfmm_p2m: unsupported p=%d m=%d", p, m);
@@ -465,11 +347,10 @@ extern "C" int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
   if (max_leaves <= 0) return 0;
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
-  if (p <= kWarpP) {
-    l2p_warp_kernel<<<grid_cap(ceil_div(max_leaves, kLeafWarps), 16), 32 * kLeafWarps, 0,
-                      as_stream(stream)>>>(pts4, m, leaves, starts, counts, n_leaves, ip,
-                                           g, locals, phi_sorted, ref_flag);
-    return check_launch("l2p_warp_kernel");
+  if (p >= 2 && p <= 8) {
+    LeafCall a{pts4, nullptr, m, leaves, starts, counts, n_leaves, max_leaves, ip, g,
+               locals, phi_sorted, ref_flag, as_stream(stream)};
+    return dispatch_leaf(p, false, a);
   }
   size_t smem = sizeof(double) * m * p * p * p;
   if (smem > 200 * 1024) {

@@ -1,0 +1,198 @@
+// Warp-per-leaf P2M / L2P specialised on the interpolation order P (included
+// by interp.cu; the production path for p <= 8).
+//
+// A warp owns one leaf at a time.  P2M: lanes compute the 3 x P weights of up
+// to 32 points into the warp's shared slice; lane l then owns the node pairs
+// (i, j) = divmod(l + 32u, P) and accumulates all P nodes k of each, i.e.
+// M[i][j][k] += ((wx_i wy_j) wz_k) w over the leaf's points in sorted order
+// (the product order of interp_matrix_3d and the reduceat order of
+// engine.py:176-182).  L2P: lanes own points; the leaf's locals of one column
+// sit in shared memory and every lane contracts them with its weights.
+#pragma once
+
+template <int P>
+__device__ __forceinline__ void weights_p(const Interp &ip, double x, double *w) {
+  if (ip.scheme == 0) {
+    x = fmin(1.0, fmax(-1.0, x));
+    double T[P];
+    T[0] = 1.0;
+    if (P > 1) T[1] = x;
+#pragma unroll
+    for (int n = 2; n < P; ++n) T[n] = fma(2.0 * x, T[n - 1], -T[n - 2]);
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int n = 0; n < P; ++n) s = fma(T[n], ip.S[n * P + j], s);
+      w[j] = s;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      double v = 1.0;
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        if (k != j) v *= (x - ip.nodes[k]) / (ip.nodes[j] - ip.nodes[k]);
+      w[j] = v;
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * kLeafWarps)
+p2m_leaf_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
+                int m, const int64_t *__restrict__ leaves,
+                const int64_t *__restrict__ starts,
+                const int64_t *__restrict__ counts,
+                const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
+                double *__restrict__ moments, int32_t *flag) {
+  constexpr int NP = (P * P + 31) / 32;  // (i, j) pairs per lane
+  __shared__ double s_w[kLeafWarps][32][3 * P];
+  __shared__ double s_v[kLeafWarps][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nl = *n_leaves;
+  for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
+       leaf += int64_t(gridDim.x) * kLeafWarps) {
+    const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
+    const int64_t s0 = starts[leaf], cnt = counts[leaf];
+    int cx, cy, cz;
+    unmorton3((uint64_t)cell, cx, cy, cz);
+    for (int c = 0; c < m; ++c) {
+      double acc[NP][P];
+#pragma unroll
+      for (int u = 0; u < NP; ++u)
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[u][k] = 0.0;
+      for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
+        const int nb = (int)(cnt - c0 < 32 ? cnt - c0 : 32);
+        __syncwarp();
+        if (lane < nb) {
+          const int64_t i = s0 + c0 + lane;
+          const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+          weights_p<P>(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), &s_w[wid][lane][0]);
+          weights_p<P>(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), &s_w[wid][lane][P]);
+          weights_p<P>(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), &s_w[wid][lane][2 * P]);
+          s_v[wid][lane] = ws[i * m + c];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < NP; ++u) {
+          const int pr = lane + 32 * u;
+          if (pr < P * P) {
+            const int ii = pr / P, jj = pr - ii * P;
+            for (int t = 0; t < nb; ++t) {
+              const double *wt = s_w[wid][t];
+              const double wxy = wt[ii] * wt[P + jj], v = s_v[wid][t];
+#pragma unroll
+              for (int k = 0; k < P; ++k) acc[u][k] += (wxy * wt[2 * P + k]) * v;
+            }
+          }
+        }
+      }
+      double *dst = moments + (cell * m + c) * (int64_t)(P * P * P);
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        const int pr = lane + 32 * u;
+        if (pr < P * P) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) dst[pr * P + k] = acc[u][k];
+        }
+      }
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * kLeafWarps)
+l2p_leaf_kernel(const double *__restrict__ pts4, int m,
+                const int64_t *__restrict__ leaves,
+                const int64_t *__restrict__ starts,
+                const int64_t *__restrict__ counts,
+                const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
+                const double *__restrict__ locals, double *__restrict__ phi,
+                int32_t *flag) {
+  constexpr int P3 = P * P * P;
+  __shared__ double s_L[kLeafWarps][P3];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nl = *n_leaves;
+  for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
+       leaf += int64_t(gridDim.x) * kLeafWarps) {
+    const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
+    const int64_t s0 = starts[leaf], cnt = counts[leaf];
+    int cx, cy, cz;
+    unmorton3((uint64_t)cell, cx, cy, cz);
+    for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
+      const bool have = c0 + lane < cnt;
+      const int64_t i = s0 + c0 + lane;
+      double wx[P], wy[P], wz[P];
+      if (have) {
+        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+        weights_p<P>(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), wx);
+        weights_p<P>(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), wy);
+        weights_p<P>(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), wz);
+      }
+      for (int c = 0; c < m; ++c) {
+        __syncwarp();
+        const double *src = locals + (cell * m + c) * (int64_t)P3;
+        for (int a = lane; a < P3; a += 32) s_L[wid][a] = src[a];
+        __syncwarp();
+        if (have) {
+          const double *L = s_L[wid];
+          double s = 0.0;
+#pragma unroll
+          for (int ii = 0; ii < P; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              const double wxy = wx[ii] * wy[jj];
+#pragma unroll
+              for (int kk = 0; kk < P; ++kk)
+                s = fma(wxy * wz[kk], L[(ii * P + jj) * P + kk], s);
+            }
+          phi[i * m + c] = s;
+        }
+      }
+    }
+  }
+}
+
+struct LeafCall {
+  const double *pts4, *ws;
+  int m;
+  const int64_t *leaves, *starts, *counts, *n_leaves;
+  int64_t max_leaves;
+  Interp ip;
+  LeafGeom g;
+  const double *locals;
+  double *out;  // moments (P2M) or phi (L2P)
+  int32_t *flag;
+  cudaStream_t st;
+};
+
+template <int P>
+int launch_leaf(bool p2m, const LeafCall &a) {
+  const unsigned grid = (unsigned)grid_cap(ceil_div(a.max_leaves, kLeafWarps), 16);
+  if (p2m) {
+    p2m_leaf_kernel<P><<<grid, 32 * kLeafWarps, 0, a.st>>>(
+        a.pts4, a.ws, a.m, a.leaves, a.starts, a.counts, a.n_leaves, a.ip, a.g, a.out,
+        a.flag);
+    return check_launch("p2m_leaf_kernel");
+  }
+  l2p_leaf_kernel<P><<<grid, 32 * kLeafWarps, 0, a.st>>>(
+      a.pts4, a.m, a.leaves, a.starts, a.counts, a.n_leaves, a.ip, a.g, a.locals, a.out,
+      a.flag);
+  return check_launch("l2p_leaf_kernel");
+}
+
+inline int dispatch_leaf(int p, bool p2m, const LeafCall &a) {
+  switch (p) {
+    case 2: return launch_leaf<2>(p2m, a);
+    case 3: return launch_leaf<3>(p2m, a);
+    case 4: return launch_leaf<4>(p2m, a);
+    case 5: return launch_leaf<5>(p2m, a);
+    case 6: return launch_leaf<6>(p2m, a);
+    case 7: return launch_leaf<7>(p2m, a);
+    default: return launch_leaf<8>(p2m, a);
+  }
+}
