@@ -171,6 +171,24 @@ int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
              int levels, int64_t cell_lo, int64_t cell_hi, double *out,
              void *scratch, size_t scratch_bytes, bfmm_stream_t stream);
 
+/* Symmetric near field for shared targets = sources and a kernel with
+ * K(y, x) = sign K(x, y) (the reference's transpose replay,
+ * engine.py:361-364, 442-457): each unordered neighbour-leaf pair is
+ * evaluated once and both sides are accumulated into per-neighbour slots
+ * that are summed in neighbour order (deterministic, no atomics).  Writes
+ * out (nt rows, m = 1) for every point touched; when a leaf holds more than
+ * 64 points the library falls back to bfmm_p2p on the device (no host
+ * synchronisation).  Leaves outside [cell_lo, cell_hi) start no pairs; the
+ * pairs a shard starts may add to other shards' rows (sum across ranks). */
+size_t bfmm_p2p_symmetric_scratch_bytes(int64_t nt, int64_t max_tleaves);
+int bfmm_p2p_symmetric(int handle, const double *pts4, const int64_t *leaves,
+                       const int64_t *starts, const int64_t *counts,
+                       const int64_t *n_leaves, int64_t max_leaves,
+                       const int32_t *cell_start, const int32_t *cell_count,
+                       int levels, int64_t cell_lo, int64_t cell_hi, int64_t nt,
+                       double sign, double *out, void *scratch,
+                       size_t scratch_bytes, bfmm_stream_t stream);
+
 /* Locate the first non-finite kernel value in the near field in the
  * reference's enumeration order (offset, target row, source row;
  * engine.py:362-441).  *key (device, init UINT64_MAX) receives

@@ -87,6 +87,7 @@ Driver &driver() {
 struct JitKernel {
   CUfunction p2p[5];
   CUfunction locate;
+  CUfunction sym;
 };
 
 std::mutex g_jit_mu;
@@ -137,6 +138,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     names.push_back("bfmm_nf::p2p_kernel<bfmm_nf::KUser, " +
                     std::to_string(kMCs[i]) + ">");
   names.push_back("bfmm_nf::locate_kernel<bfmm_nf::KUser>");
+  names.push_back("bfmm_nf::p2p_sym_kernel<bfmm_nf::KUser>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17",
                         "-default-device", "-lineinfo"};
@@ -173,13 +175,13 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 6; ++i) {
+  for (int i = 0; i < 7; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
       return 3;
     }
-    if (i < 5) jk.p2p[i] = f; else jk.locate = f;
+    if (i < 5) jk.p2p[i] = f; else if (i == 5) jk.locate = f; else jk.sym = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -383,7 +385,56 @@ bfmm_nf::Args make_args(const double *tpts4, const int64_t *tleaves,
   a.levels = levels;
   a.out = out;
   a.work_incl = reinterpret_cast<const long long *>(work);
+  a.gate = nullptr;
   return a;
+}
+
+__global__ void too_big_kernel(const int64_t *__restrict__ counts,
+                               const int64_t *__restrict__ n_leaves, int limit,
+                               int *flag) {
+  const int64_t nl = *n_leaves;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nl;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (counts[i] > limit) atomicOr(flag, 1);
+}
+
+// flag = 0 -> "not too big"; the fallback P2P is gated on flag != 0
+int launch_sym(int handle, const bfmm_nf::Args &a, double *slots, int64_t nt,
+               double sgn, const int *flag, int64_t lo, int64_t hi, cudaStream_t st) {
+  const dim3 grid(kNumSMs * 16), block(32 * bfmm_nf::kWarps);
+  const long long sl = (long long)nt;
+  switch (handle) {
+    case 1: bfmm_nf::p2p_sym_kernel<KLaplace><<<grid, block, 0, st>>>(a, slots, sl, sgn, flag, lo, hi); break;
+    case 2: bfmm_nf::p2p_sym_kernel<KLaplaceForce><<<grid, block, 0, st>>>(a, slots, sl, sgn, flag, lo, hi); break;
+    case 3: bfmm_nf::p2p_sym_kernel<KGaussian><<<grid, block, 0, st>>>(a, slots, sl, sgn, flag, lo, hi); break;
+    case 4: bfmm_nf::p2p_sym_kernel<KExponential><<<grid, block, 0, st>>>(a, slots, sl, sgn, flag, lo, hi); break;
+    case 5: bfmm_nf::p2p_sym_kernel<KLogarithm><<<grid, block, 0, st>>>(a, slots, sl, sgn, flag, lo, hi); break;
+    default: {
+      JitKernel jk;
+      {
+        std::lock_guard<std::mutex> lock(g_jit_mu);
+        if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+          set_error("bfmm_p2p_symmetric: unknown kernel handle %d", handle);
+          return 2;
+        }
+        jk = g_jit[handle - kFirstJit];
+      }
+      bfmm_nf::Args args = a;
+      double *sp = slots;
+      long long n = sl, l0 = lo, h0 = hi;
+      double sg = sgn;
+      const int *fp = flag;
+      void *params[] = {&args, &sp, &n, &sg, &fp, &l0, &h0};
+      if (driver().LaunchKernel(jk.sym, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st,
+                                params, nullptr) != CUDA_SUCCESS) {
+        set_error("bfmm_p2p_symmetric: cuLaunchKernel failed");
+        return 1;
+      }
+      add_launches(1);
+      return 0;
+    }
+  }
+  return check_launch("p2p_sym_kernel");
 }
 
 }  // namespace
@@ -517,4 +568,64 @@ extern "C" int bfmm_scatter_output(const double *far_sorted,
                                                       perm, n, m, phi,
                                                       nonfinite_flag);
   return check_launch("scatter_kernel");
+}
+
+extern "C" size_t bfmm_p2p_symmetric_scratch_bytes(int64_t nt, int64_t max_tleaves) {
+  size_t off;
+  const size_t chunk = (p2p_scratch(max_tleaves < 1 ? 1 : max_tleaves, &off) + 255) & ~size_t(255);
+  return chunk + ((27 * (size_t)(nt < 1 ? 1 : nt) * sizeof(double) + 255) & ~size_t(255)) + 256;
+}
+
+extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
+                                  const int64_t *leaves, const int64_t *starts,
+                                  const int64_t *counts, const int64_t *n_leaves,
+                                  int64_t max_leaves, const int32_t *cell_start,
+                                  const int32_t *cell_count, int levels,
+                                  int64_t cell_lo, int64_t cell_hi, int64_t nt,
+                                  double sign, double *out, void *scratch,
+                                  size_t scratch_bytes, bfmm_stream_t stream) {
+  if (max_leaves <= 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  size_t cub_off;
+  const size_t chunk = (p2p_scratch(max_leaves, &cub_off) + 255) & ~size_t(255);
+  const size_t slot_bytes = (27 * (size_t)nt * sizeof(double) + 255) & ~size_t(255);
+  if (scratch_bytes < chunk + slot_bytes + 256) {
+    set_error("bfmm_p2p_symmetric: scratch too small");
+    return 2;
+  }
+  char *base = static_cast<char *>(scratch);
+  double *slots = reinterpret_cast<double *>(base + chunk);
+  int *flag = reinterpret_cast<int *>(base + chunk + slot_bytes);
+  if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess ||
+      cudaMemsetAsync(slots, 0, 27 * (size_t)nt * sizeof(double), st) != cudaSuccess) {
+    set_error("bfmm_p2p_symmetric: memset failed");
+    return 1;
+  }
+  const unsigned g1 = (unsigned)std::min<int64_t>(ceil_div(max_leaves, 256), kNumSMs * 8);
+  too_big_kernel<<<g1, 256, 0, st>>>(counts, n_leaves, bfmm_nf::kSymMax, flag);
+  if (check_launch("too_big_kernel")) return 1;
+  // fallback work list + gated plain P2P (runs only when a leaf is too big)
+  int64_t *nch = reinterpret_cast<int64_t *>(base);
+  int64_t *incl = nch + max_leaves;
+  chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_leaves, 256), kNumSMs * 16),
+                        256, 0, st>>>(counts, leaves, n_leaves, max_leaves, cell_lo, cell_hi,
+                                      nch);
+  if (check_launch("chunk_counts_kernel")) return 1;
+  size_t cb = chunk - cub_off;
+  if (cub::DeviceScan::InclusiveSum(base + cub_off, cb, nch, incl, (int)max_leaves, st) !=
+      cudaSuccess) {
+    set_error("bfmm_p2p_symmetric: scan failed");
+    return 1;
+  }
+  add_launches(2);
+  bfmm_nf::Args a = make_args(pts4, leaves, starts, counts, n_leaves, pts4, nullptr, 1,
+                              cell_start, cell_count, levels, out, incl);
+  int rc = launch_sym(handle, a, slots, nt, sign, flag, cell_lo, cell_hi, st);
+  if (rc) return rc;
+  a.gate = flag;
+  rc = launch_p2p(handle, 0, dim3(kNumSMs * 16), a, 0, st);
+  if (rc) return rc;
+  const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(nt, 256), kNumSMs * 16);
+  bfmm_nf::sym_reduce_kernel<<<g2, 256, 0, st>>>(slots, (long long)nt, out, flag);
+  return check_launch("sym_reduce_kernel");
 }

@@ -316,6 +316,50 @@ def test_device_tensors_round_trip(cache_dir):
     assert dev.is_cuda and np.array_equal(dev.cpu().numpy(), host)
 
 
+def _dipole():
+    def dipole(dx, dy, dz):
+        r2 = dx * dx + dy * dy + dz * dz
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = dx / (r2 * np.sqrt(r2))
+        return np.where(r2 == 0, 0.0, v)
+    return bf.KernelSpec(name="xdipole", diff_func=dipole, symmetry=-1, homogen=-2.0,
+                         cuda_expr="(dx * dx + dy * dy + dz * dz) == 0.0 ? 0.0 : dx / "
+                                   "((dx * dx + dy * dy + dz * dz) * sqrt(dx * dx + dy * dy + dz * dz))",
+                         cuda_arg="diff")
+
+
+@pytest.mark.parametrize("kname", ["gauss02", "laplacian", "dipole"])
+def test_symmetric_near_field_matches_full(kname, cache_dir):
+    """Transpose replay (reference engine.py:361-364) vs all 27 offsets, like
+    T/test_engine.py::test_near_field_transpose_reuse_is_faithful."""
+    kernel = _dipole() if kname == "dipole" else workload_kernel(kname)
+    pts, w = unit_cloud(40000, seed=61)
+    plan = bf.FmmPlan(levels=3, order=4, eps=1e-6, domain_center=(0.5, 0.5, 0.5),
+                      domain_length=1.0)
+    ev = bf.FmmEvaluator(kernel, plan, cache_dir=cache_dir)
+    ev._disable_far_field = True
+    ev.near_mode = "symmetric"
+    a = ev.evaluate(pts, weights=w[:, 0])
+    ev.near_mode = "full"
+    b = ev.evaluate(pts, weights=w[:, 0])
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
+
+
+def test_symmetric_near_field_falls_back_on_crowded_leaves(cache_dir):
+    gen = np.random.default_rng(71)
+    pts = np.clip(0.3 + 0.002 * gen.standard_normal((500, 3)), 0, 1)  # one crowded leaf
+    pts = np.vstack([pts, gen.random((4000, 3))])
+    w = gen.standard_normal(len(pts))
+    plan = bf.FmmPlan(levels=3, order=3, eps=1e-6, domain_center=(0.5, 0.5, 0.5),
+                      domain_length=1.0)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, plan, cache_dir=cache_dir)
+    ev.near_mode = "symmetric"
+    a = ev.evaluate(pts, weights=w)
+    ev.near_mode = "full"
+    b = ev.evaluate(pts, weights=w)
+    assert np.array_equal(a, b)  # device-side fallback runs the same kernel
+
+
 def test_empty_leaves_and_clusters(cache_dir):
     """Ragged occupancy: most leaves empty, a few crowded (C4-like)."""
     gen = np.random.default_rng(41)
