@@ -3,14 +3,20 @@
 // convolution on a q^3 grid (q = 2p - 1) and diagonal in the real-FFT basis.
 //
 // Per level and per chunk of weight columns:
-//   1. fft_fwd_kernel : X[c][f] = rfftn(pad_q(M[c]))           (pass z, y, x)
-//   2. hadamard_kernel: Y[c][f] = sum_{t valid} S_t[f] * X[c + t][f]
-//   3. fft_inv_kernel : L[c]    = scale * irfftn(Y[c], s=(q,q,q))[:p,:p,:p]
+//   1. fft_fwd_kernel : X[col][f][cell] = rfftn(pad_q(M[cell, col]))[f]
+//   2. stencil_kernel : Y[col][f][c] = sum_{t valid} S_t[f] X[col][f][c + t]
+//   3. fft_inv_kernel : L[c, col] = scale * irfftn(Y[col][:][c])[:p,:p,:p]
 // f = (kx*q + ky)*(q/2+1) + kz indexes numpy's rfftn output layout
 // (ops:156-159), so the symbols S_t are the reference's table verbatim.
+//
+// Spectra are stored frequency-major with cells in lexicographic (x, y, z)
+// order: for one frequency the Hadamard accumulation is a 3-D stencil with
+// 189 complex taps over the cell grid, which stencil_kernel
+// tiles through shared memory (an 8 x 8 x 16 target tile plus its 3-cell
+// halo) and blocks in registers along z (each thread owns 8 same-parity
+// targets, so one z-column of 21 sources serves 7 taps x 8 targets).
 // The transforms are direct DFTs along each axis with exactly tabulated
-// twiddles (q <= 23): zero padding makes them cheaper than a generic FFT
-// and their cost is a few percent of the Hadamard sum.
+// twiddles: zero padding makes them cheaper than a generic FFT.
 #include <algorithm>
 
 #include "common.cuh"
@@ -25,19 +31,27 @@ struct FftGeom {
   double c[kMaxQ], s[kMaxQ];  // cos / sin(2 pi r / q)
 };
 
+__device__ __forceinline__ int64_t lex_of(int x, int y, int z, int n) {
+  return ((int64_t)x * n + y) * n + z;
+}
+
 // ---- 1. forward transform: one CTA per (cell, column) ------------------------
 __global__ void __launch_bounds__(128)
-fft_fwd_kernel(const double *__restrict__ moments, int64_t ncell, int m, int c0,
+fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
                int cc, FftGeom g, double2 *__restrict__ X) {
   extern __shared__ double2 sm2[];
   const int p = g.p, q = g.q, h = g.h, F = q * q * h;
+  const int n = 1 << level;
+  const int64_t ncell = int64_t(1) << (3 * level);
   double2 *A = sm2;            // [p][p][h]
   double2 *B = A + p * p * h;  // [p][q][h]
   double *in = reinterpret_cast<double *>(B + p * q * h);  // [p][p][p]
   for (int64_t w = blockIdx.x; w < ncell * cc; w += gridDim.x) {
-    const int64_t cell = w / cc;
-    const int col = c0 + (int)(w - cell * cc);
-    const double *src = moments + (cell * m + col) * (int64_t)(p * p * p);
+    const int crel = (int)(w / ncell);
+    const int64_t lex = w - crel * ncell;
+    const int x = (int)(lex / ((int64_t)n * n)), y = (int)((lex / n) % n), z = (int)(lex % n);
+    const int64_t cell = (int64_t)morton3(x, y, z);
+    const double *src = moments + (cell * m + c0 + crel) * (int64_t)(p * p * p);
     __syncthreads();
     for (int e = threadIdx.x; e < p * p * p; e += blockDim.x) in[e] = src[e];
     __syncthreads();
@@ -68,8 +82,8 @@ fft_fwd_kernel(const double *__restrict__ moments, int64_t ncell, int m, int c0,
       B[e] = make_double2(re, im);
     }
     __syncthreads();
-    // x: p inputs -> q bins, straight to global
-    double2 *dst = X + w * (int64_t)F;
+    // x: p inputs -> q bins, frequency-major to global
+    double2 *dst = X + (int64_t)crel * F * ncell + lex;
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
       const int kx = f / (q * h), rem = f - kx * q * h;
       double re = 0.0, im = 0.0;
@@ -79,79 +93,112 @@ fft_fwd_kernel(const double *__restrict__ moments, int64_t ncell, int m, int c0,
         re = fma(b.x, g.c[r], fma(b.y, g.s[r], re));
         im = fma(b.y, g.c[r], fma(-b.x, g.s[r], im));
       }
-      dst[f] = make_double2(re, im);
+      dst[(int64_t)f * ncell] = make_double2(re, im);
     }
   }
 }
 
-// ---- 2. Hadamard accumulation over the far offsets ----------------------------
-__constant__ signed char c_off[316][3];
-bool g_off_ready = false;
+// ---- 2. Hadamard accumulation as a per-frequency 3-D stencil ------------------
+constexpr int kTX = 8, kTY = 8, kTZ = 16, kR = kTZ / 2;  // 128 threads x 8 targets
+constexpr int kHX = kTX + 6, kHY = kTY + 6, kHZ = kTZ + 6;
 
-void ensure_off() {
-  if (g_off_ready) return;
-  signed char h[316][3];
-  int n = 0;
-  for (int a = -3; a <= 3; ++a)
-    for (int b = -3; b <= 3; ++b)
-      for (int c = -3; c <= 3; ++c)
-        if (std::max(abs(a), std::max(abs(b), abs(c))) >= 2) {
-          h[n][0] = (signed char)a;
-          h[n][1] = (signed char)b;
-          h[n][2] = (signed char)c;
-          ++n;
-        }
-  cudaMemcpyToSymbol(c_off, h, sizeof(h));
-  g_off_ready = true;
-}
-
-// thread per (target cell, column, frequency); frequencies fastest so a warp
-// reads 32 consecutive bins of one source spectrum and of one symbol.
-__global__ void __launch_bounds__(256)
-hadamard_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y,
-                int level, int cc, int F, const double2 *__restrict__ S,
-                int64_t cell_lo, int64_t ncell) {
-  // targets: cells [cell_lo, cell_lo + ncell); X holds every cell
-  const int n = 1 << level;
-  const int64_t total = ncell * cc * F;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t cw = e / F;
-    const int f = (int)(e - cw * F);
-    const int64_t rel = cw / cc;
-    const int col = (int)(cw - rel * cc);
-    const int64_t cell = cell_lo + rel;
-    int cx, cy, cz;
-    unmorton3((uint64_t)cell, cx, cy, cz);
-    double re = 0.0, im = 0.0;
-    for (int t = 0; t < 316; ++t) {
-      const int t0 = c_off[t][0], t1 = c_off[t][1], t2 = c_off[t][2];
-      if (!far_pair(n, cx, cy, cz, t0, t1, t2)) continue;
-      const int64_t src = (int64_t)morton3(cx + t0, cy + t1, cz + t2);
-      const double2 x = X[(src * cc + col) * F + f];
-      const double2 s = S[(int64_t)t * F + f];
-      re = fma(s.x, x.x, fma(-s.y, x.y, re));
-      im = fma(s.x, x.y, fma(s.y, x.x, im));
-    }
-    Y[e] = make_double2(re, im);
-  }
-}
-
-// ---- 3. inverse transform + crop + scale: one CTA per (cell, column) ---------
+// grid: (tiles, frequencies, columns); block (8, 8, 2): thread (ix, iy, pz)
+// owns targets (x0+ix, y0+iy, z0+pz+2k), k < 8 -- one parity class, so one
+// valid-offset set (octree.py:128-145).  The symbol of every offset t sits in
+// a 7^3 table (zero for the 27 near offsets).
 __global__ void __launch_bounds__(128)
-fft_inv_kernel(const double2 *__restrict__ Y, int64_t cell_lo, int64_t ncell,
-               int m, int c0, int cc, FftGeom g, double scale,
-               double *__restrict__ locals) {
+stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level,
+               int F, const double2 *__restrict__ S, const short *__restrict__ tap_index,
+               int64_t cell_lo, int64_t cell_hi) {
   extern __shared__ double2 sm2[];
-  const int p = g.p, q = g.q, h = g.h, F = q * q * h;
+  auto halo = reinterpret_cast<double2 (*)[kHY][kHZ]>(sm2);                     // [kHX][kHY][kHZ]
+  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kHX * kHY * kHZ);      // [7][7][7]
+  const int n = 1 << level;
+  const int64_t ncell = int64_t(1) << (3 * level);
+  const int tilesx = (n + kTX - 1) / kTX, tilesy = (n + kTY - 1) / kTY;
+  const int tile = blockIdx.x;
+  const int tz = tile / (tilesx * tilesy), trem = tile - tz * tilesx * tilesy;
+  const int x0 = (trem / tilesy) * kTX, y0 = (trem % tilesy) * kTY, z0 = tz * kTZ;
+  const int f = blockIdx.y, col = blockIdx.z;
+  const int ix = threadIdx.x, iy = threadIdx.y, pz = threadIdx.z;
+  const int tid = (pz * kTY + iy) * kTX + ix;
+  const int x = x0 + ix, y = y0 + iy;
+  // shard filter: skip the tile when none of its targets is ours
+  bool mine = false;
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    const int z = z0 + pz + 2 * k;
+    if (x < n && y < n && z < n) {
+      const int64_t id = (int64_t)morton3(x, y, z);
+      mine |= id >= cell_lo && id < cell_hi;
+    }
+  }
+  if (!__syncthreads_or(mine)) return;
+  const double2 *Xf = X + ((int64_t)col * F + f) * ncell;
+  for (int e = tid; e < kHX * kHY * kHZ; e += 128) {
+    const int hx = e / (kHY * kHZ), hr = e - hx * kHY * kHZ, hy = hr / kHZ, hz = hr - hy * kHZ;
+    const int sx = x0 + hx - 3, sy = y0 + hy - 3, sz = z0 + hz - 3;
+    double2 v = make_double2(0.0, 0.0);
+    if (sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n) v = Xf[lex_of(sx, sy, sz, n)];
+    halo[hx][hy][hz] = v;
+  }
+  for (int e = tid; e < 343; e += 128) {
+    const int t = tap_index[e];
+    (&taps[0][0][0])[e] = t >= 0 ? S[(int64_t)t * F + f] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 acc[kR];
+#pragma unroll
+  for (int k = 0; k < kR; ++k) acc[k] = make_double2(0.0, 0.0);
+  // parity rule: +3 needs an even target coordinate, -3 an odd one
+  const int px = x & 1, py = y & 1, pzz = (z0 + pz) & 1;
+  for (int a = -3; a <= 3; ++a) {
+    if ((a == 3 && px) || (a == -3 && !px)) continue;
+    for (int b = -3; b <= 3; ++b) {
+      if ((b == 3 && py) || (b == -3 && !py)) continue;
+      // the z column of sources for all 8 targets and all 7 z offsets
+      double2 seg[kR * 2 + 5];
+      const double2 *col_src = &halo[ix + 3 + a][iy + 3 + b][pz];
+#pragma unroll
+      for (int u = 0; u < kR * 2 + 5; ++u) seg[u] = col_src[u];
+#pragma unroll
+      for (int c = -3; c <= 3; ++c) {
+        if ((c == 3 && pzz) || (c == -3 && !pzz)) continue;
+        const double2 s = taps[a + 3][b + 3][c + 3];  // zero for near offsets
+#pragma unroll
+        for (int k = 0; k < kR; ++k) {
+          const double2 v = seg[c + 3 + 2 * k];
+          acc[k].x = fma(s.x, v.x, fma(-s.y, v.y, acc[k].x));
+          acc[k].y = fma(s.x, v.y, fma(s.y, v.x, acc[k].y));
+        }
+      }
+    }
+  }
+  double2 *Yf = Y + ((int64_t)col * F + f) * ncell;
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    const int z = z0 + pz + 2 * k;
+    if (x < n && y < n && z < n) Yf[lex_of(x, y, z, n)] = acc[k];
+  }
+}
+
+// ---- 3. inverse transform + crop + scale: one CTA per (own cell, column) ------
+__global__ void __launch_bounds__(128)
+fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_t ncell_own,
+               int m, int c0, int cc, FftGeom g, double scale, double *__restrict__ locals) {
+  extern __shared__ double2 sm2[];
+  const int p = g.p, q = g.q, h = g.h;
+  const int n = 1 << level;
+  const int64_t ncell = int64_t(1) << (3 * level);
   double2 *C = sm2;            // [p][q][h]   x inverted, i < p
   double2 *D = C + p * q * h;  // [p][p][h]   y inverted, j < p
   const double norm = scale / ((double)q * q * q);
-  for (int64_t w = blockIdx.x; w < ncell * cc; w += gridDim.x) {
-    const int64_t rel = w / cc;
-    const int col = c0 + (int)(w - rel * cc);
-    const int64_t cell = cell_lo + rel;
-    const double2 *src = Y + w * (int64_t)F;
+  for (int64_t w = blockIdx.x; w < ncell_own * cc; w += gridDim.x) {
+    const int crel = (int)(w / ncell_own);
+    const int64_t cell = cell_lo + (w - crel * ncell_own);
+    int x, y, z;
+    unmorton3((uint64_t)cell, x, y, z);
+    const double2 *src = Y + (int64_t)crel * q * q * h * ncell + lex_of(x, y, z, n);
     __syncthreads();
     // x: q bins -> p outputs, e^{+2 pi i i kx / q}
     for (int e = threadIdx.x; e < p * q * h; e += blockDim.x) {
@@ -159,9 +206,9 @@ fft_inv_kernel(const double2 *__restrict__ Y, int64_t cell_lo, int64_t ncell,
       double re = 0.0, im = 0.0;
       for (int kx = 0; kx < q; ++kx) {
         const int r = (i * kx) % q;
-        const double2 y = src[kx * q * h + rem];
-        re = fma(y.x, g.c[r], fma(-y.y, g.s[r], re));
-        im = fma(y.y, g.c[r], fma(y.x, g.s[r], im));
+        const double2 yv = src[(int64_t)(kx * q * h + rem) * ncell];
+        re = fma(yv.x, g.c[r], fma(-yv.y, g.s[r], re));
+        im = fma(yv.y, g.c[r], fma(yv.x, g.s[r], im));
       }
       C[e] = make_double2(re, im);
     }
@@ -181,7 +228,7 @@ fft_inv_kernel(const double2 *__restrict__ Y, int64_t cell_lo, int64_t ncell,
     __syncthreads();
     // z: Hermitian half spectrum -> p real outputs (irfft: DC imaginary
     // part dropped, bins 1..q/2 counted twice; q is odd so no Nyquist bin)
-    double *dst = locals + (cell * m + col) * (int64_t)(p * p * p);
+    double *dst = locals + (cell * m + c0 + crel) * (int64_t)(p * p * p);
     for (int e = threadIdx.x; e < p * p * p; e += blockDim.x) {
       const int ij = e / p, k = e - ij * p;
       const double2 *d = D + ij * h;
@@ -208,6 +255,24 @@ FftGeom make_geom(int p) {
   return g;
 }
 
+// 7^3 table: offset (a, b, c) -> index among the 316 far offsets
+// (lexicographic, octree.py:110-119), -1 for the 27 near offsets.
+short *tap_table() {
+  static short *dev = nullptr;
+  if (dev) return dev;
+  short h[343];
+  int t = 0;
+  for (int a = -3; a <= 3; ++a)
+    for (int b = -3; b <= 3; ++b)
+      for (int c = -3; c <= 3; ++c) {
+        const int e = ((a + 3) * 7 + (b + 3)) * 7 + (c + 3);
+        h[e] = (std::max(abs(a), std::max(abs(b), abs(c))) >= 2) ? (short)t++ : (short)-1;
+      }
+  cudaMalloc(&dev, sizeof(h));
+  cudaMemcpy(dev, h, sizeof(h), cudaMemcpyHostToDevice);
+  return dev;
+}
+
 }  // namespace
 }  // namespace bfmm
 
@@ -229,37 +294,44 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
     set_error("bfmm_m2l_fft: unsupported p=%d level=%d", p, level);
     return 2;
   }
-  ensure_off();
   cudaStream_t st = as_stream(stream);
   const FftGeom g = make_geom(p);
   const int64_t F = int64_t(g.q) * g.q * g.h;
   const int64_t ncell = int64_t(1) << (3 * level);
   const size_t per_col = 2 * sizeof(double2) * ncell * F;
-  int cc = (int)std::min<size_t>((size_t)m, scratch_bytes / per_col);
+  const int cc = (int)std::min<size_t>((size_t)m, scratch_bytes / per_col);
   if (cc < 1) {
     set_error("bfmm_m2l_fft: scratch %zu B holds no column (need %zu)", scratch_bytes,
               per_col);
     return 2;
   }
+  const short *taps = tap_table();
   double2 *X = static_cast<double2 *>(scratch);
   double2 *Y = X + ncell * cc * F;
   const size_t smem_f = sizeof(double2) * (g.p * g.p * g.h + g.p * g.q * g.h) +
                         sizeof(double) * g.p * g.p * g.p;
   const size_t smem_i = sizeof(double2) * (g.p * g.q * g.h + g.p * g.p * g.h);
+  const int n = 1 << level;
+  const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
+  const size_t smem_s = sizeof(double2) * (kHX * kHY * kHZ + 343);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_s);
+    attr = true;
+  }
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
-    const int64_t work = ncell * ccur;
-    const unsigned gcell = (unsigned)std::min<int64_t>(work, kNumSMs * 16);
-    fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, ncell, m, c0, ccur, g, X);
+    const unsigned gcell = (unsigned)std::min<int64_t>(ncell * ccur, kNumSMs * 16);
+    fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, X);
     if (check_launch("fft_fwd_kernel")) return 1;
-    const int64_t tgt = 8 * nq * ccur;
-    const unsigned gh = (unsigned)std::min<int64_t>(ceil_div(tgt * F, 256), kNumSMs * 64);
-    hadamard_kernel<<<gh, 256, 0, st>>>(X, Y, level, ccur, (int)F,
-                                        reinterpret_cast<const double2 *>(symbols),
-                                        8 * q_lo, 8 * nq);
-    if (check_launch("hadamard_kernel")) return 1;
-    const unsigned gi = (unsigned)std::min<int64_t>(std::max<int64_t>(tgt, 1), kNumSMs * 16);
-    fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, 8 * q_lo, 8 * nq, m, c0, ccur, g, scale,
+    stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
+        X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
+        8 * (q_lo + nq));
+    if (check_launch("stencil_kernel")) return 1;
+    const int64_t own = 8 * nq;
+    const unsigned gi = (unsigned)std::min<int64_t>(std::max<int64_t>(own * ccur, 1), kNumSMs * 16);
+    fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, own, m, c0, ccur, g, scale,
                                             locals);
     if (check_launch("fft_inv_kernel")) return 1;
   }
