@@ -294,6 +294,7 @@ int grid_cap(int64_t work, int per_sm) {
 }
 
 #include "leaf_kernels.cuh"
+#include "transfer_kernels.cuh"
 
 }  // namespace
 }  // namespace bfmm
@@ -379,6 +380,10 @@ extern "C" int bfmm_m2m(const double *child, double *parent, int64_t n_parent,
     set_error("bfmm_m2m: unsupported p=%d", p);
     return 2;
   }
+  if (n_parent <= 0) return 0;
+  if (p >= 2 && p <= 8)
+    return dispatch_xfer(p, true, child, parent, n_parent, m, make_halves(p, H),
+                         as_stream(stream));
   size_t smem = sizeof(double) * 4 * p * p * p;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(m2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -395,6 +400,10 @@ extern "C" int bfmm_l2l(const double *parent, double *child, int64_t n_parent,
     set_error("bfmm_l2l: unsupported p=%d", p);
     return 2;
   }
+  if (n_parent <= 0) return 0;
+  if (p >= 2 && p <= 8)
+    return dispatch_xfer(p, false, parent, child, n_parent, m, make_halves(p, H),
+                         as_stream(stream));
   size_t smem = sizeof(double) * 4 * p * p * p;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(l2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
