@@ -189,6 +189,15 @@ int bfmm_p2p_symmetric(int handle, const double *pts4, const int64_t *leaves,
                        double sign, double *out, void *scratch,
                        size_t scratch_bytes, bfmm_stream_t stream);
 
+/* Direct O(nt * ns) sum, the reference's direct_evaluate (engine.py:565-624):
+ * out[i][c] = sum_j K(t_i - s_j) w[j][c] with explicit differences
+ * (coincident points give r = 0 exactly) and Neumaier-compensated
+ * accumulation in place of 80-bit long double.  tpts (nt, 3), spts (ns, 3),
+ * w (ns, m), out (nt, m). */
+int bfmm_direct(int handle, const double *tpts, int64_t nt, const double *spts,
+                const double *w, int64_t ns, int m, double *out,
+                bfmm_stream_t stream);
+
 /* Locate the first non-finite kernel value in the near field in the
  * reference's enumeration order (offset, target row, source row;
  * engine.py:362-441).  *key (device, init UINT64_MAX) receives

@@ -126,8 +126,15 @@ small_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
   const int64_t r = e / N;
   const int n = (int)(e - r * N);
   const double *a = A + r * a_splits * K;  // split block 0 holds the sum
-  double acc = 0.0;
-  for (int k = 0; k < K; ++k) acc = fma(a[k], B[(int64_t)k * N + n], acc);
+  // four independent partial sums (fixed order) keep the FMA chain short
+  double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+  int k = 0;
+  for (; k + 4 <= K; k += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc4[u] = fma(a[k + u], B[(int64_t)(k + u) * N + n], acc4[u]);
+  }
+  for (; k < K; ++k) acc4[0] = fma(a[k], B[(int64_t)k * N + n], acc4[0]);
+  const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
   double out = alpha * acc;
   if (beta != 0.0) out += beta * C[e];
   C[e] = out;
@@ -311,7 +318,8 @@ extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq) {
   const int64_t ctas = ceil_div(rows, 64 * m2l_mw(rows)) * ceil_div(rp, 8 * m2l_nt8(rp)) * 8;
   const double slots = 2.0 * kNumSMs;
   // coarse levels: too few tiles to fill the GPU, so split the 189 offsets
-  // finely (down to one per CTA) and let the U projection sum the blocks
+  // finely (down to one per CTA; measured faster than one fat wave) and let
+  // the U projection sum the blocks
   if (ctas * 4 < slots) return (int)std::min<int64_t>(189, ceil_div(4 * (int64_t)slots, ctas));
   // otherwise pick the split count whose last wave (2 CTAs per SM) is
   // fullest, with a small penalty per split for the extra lt traffic

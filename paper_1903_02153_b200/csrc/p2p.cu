@@ -88,6 +88,7 @@ struct JitKernel {
   CUfunction p2p[5];
   CUfunction locate;
   CUfunction sym;
+  CUfunction direct;
 };
 
 std::mutex g_jit_mu;
@@ -139,6 +140,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
                     std::to_string(kMCs[i]) + ">");
   names.push_back("bfmm_nf::locate_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::p2p_sym_kernel<bfmm_nf::KUser>");
+  names.push_back("bfmm_nf::direct_kernel<bfmm_nf::KUser>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17",
                         "-default-device", "-lineinfo"};
@@ -175,13 +177,16 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 7; ++i) {
+  for (int i = 0; i < 8; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
       return 3;
     }
-    if (i < 5) jk.p2p[i] = f; else if (i == 5) jk.locate = f; else jk.sym = f;
+    if (i < 5) jk.p2p[i] = f;
+    else if (i == 5) jk.locate = f;
+    else if (i == 6) jk.sym = f;
+    else jk.direct = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -628,4 +633,48 @@ extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
   const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(nt, 256), kNumSMs * 16);
   bfmm_nf::sym_reduce_kernel<<<g2, 256, 0, st>>>(slots, (long long)nt, out, flag);
   return check_launch("sym_reduce_kernel");
+}
+
+// ---- direct sum (engine.py:565-624) -------------------------------------------
+extern "C" int bfmm_direct(int handle, const double *tpts, int64_t nt,
+                           const double *spts, const double *sw, int64_t ns, int m,
+                           double *out, bfmm_stream_t stream) {
+  if (nt <= 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  const dim3 grid((unsigned)ceil_div(nt, 128)), block(128);
+  const long long lnt = nt, lns = ns;
+  for (int c0 = 0; c0 < m; c0 += 4) {
+    switch (handle) {
+      case 1: bfmm_nf::direct_kernel<KLaplace><<<grid, block, 0, st>>>(tpts, lnt, spts, sw, lns, m, c0, out); break;
+      case 2: bfmm_nf::direct_kernel<KLaplaceForce><<<grid, block, 0, st>>>(tpts, lnt, spts, sw, lns, m, c0, out); break;
+      case 3: bfmm_nf::direct_kernel<KGaussian><<<grid, block, 0, st>>>(tpts, lnt, spts, sw, lns, m, c0, out); break;
+      case 4: bfmm_nf::direct_kernel<KExponential><<<grid, block, 0, st>>>(tpts, lnt, spts, sw, lns, m, c0, out); break;
+      case 5: bfmm_nf::direct_kernel<KLogarithm><<<grid, block, 0, st>>>(tpts, lnt, spts, sw, lns, m, c0, out); break;
+      default: {
+        JitKernel jk;
+        {
+          std::lock_guard<std::mutex> lock(g_jit_mu);
+          if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+            set_error("bfmm_direct: unknown kernel handle %d", handle);
+            return 2;
+          }
+          jk = g_jit[handle - kFirstJit];
+        }
+        const double *tp = tpts, *sp = spts, *wp = sw;
+        double *op = out;
+        long long a1 = lnt, a2 = lns;
+        int mm = m, cc = c0;
+        void *params[] = {&tp, &a1, &sp, &wp, &a2, &mm, &cc, &op};
+        if (driver().LaunchKernel(jk.direct, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st,
+                                  params, nullptr) != CUDA_SUCCESS) {
+          set_error("bfmm_direct: cuLaunchKernel failed");
+          return 1;
+        }
+        add_launches(1);
+        continue;
+      }
+    }
+    if (check_launch("direct_kernel")) return 1;
+  }
+  return 0;
 }

@@ -553,6 +553,61 @@ def _check_host_points(pts, name):
         raise DomainError(f"{name} contain non-finite coordinates")
 
 
+def direct_evaluate(kernel: KernelSpec, sources, targets=None, weights=None,
+                    target_block: int = 1024, source_block: int = 8192):
+    """O(N_t N_s) direct sum on the GPU (reference engine.py:565-624).
+
+    Explicit coordinate differences throughout (a target coinciding with a
+    source gives r = 0 exactly; for shared sets this is the reference's
+    zeroed diagonal) and compensated FP64 accumulation in place of long
+    double.  ``target_block`` / ``source_block`` are accepted for signature
+    compatibility; the device tiling is fixed."""
+    torch = _torch()
+    if not isinstance(kernel, KernelSpec):
+        raise ConfigurationError("kernel must be a KernelSpec")
+    if not kernel.has_device_form:
+        raise ConfigurationError(f"kernel {kernel.name!r} has no device form")
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("no CUDA device is visible")
+    lib = _native.load()
+    as_tensor = isinstance(sources, torch.Tensor)
+    src = (sources.to("cuda", torch.float64).contiguous() if as_tensor
+           else torch.from_numpy(np.ascontiguousarray(sources, dtype=np.float64)).cuda())
+    shared = targets is None or targets is sources
+    if src.ndim != 2 or src.shape[1] != 3:
+        raise ConfigurationError(f"sources must be an (N, 3) array, got shape {tuple(src.shape)}")
+    if shared:
+        tgt = src
+    elif isinstance(targets, torch.Tensor):
+        tgt = targets.to("cuda", torch.float64).contiguous()
+    else:
+        tgt = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.float64)).cuda()
+    if weights is None:
+        raise ConfigurationError("weights are required")
+    w = (weights.to("cuda", torch.float64) if isinstance(weights, torch.Tensor)
+         else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).cuda())
+    squeeze = w.ndim == 1
+    w = (w[:, None] if squeeze else w).contiguous()
+    if w.shape[0] != src.shape[0]:
+        raise ConfigurationError(
+            f"weights shape {tuple(w.shape)} does not match {src.shape[0]} sources")
+    if kernel.builtin_id:
+        handle = int(kernel.builtin_id)
+    else:
+        h = _native.C.c_int(0)
+        _native.check(lib.bfmm_kernel_compile(_KIND[kernel.cuda_arg], kernel.cuda_expr.encode(),
+                                              _native.C.byref(h)), "NVRTC compile")
+        handle = int(h.value)
+    m = int(w.shape[1])
+    out = torch.empty((tgt.shape[0], m), dtype=torch.float64, device="cuda")
+    _native.check(lib.bfmm_direct(handle, tgt.data_ptr(), int(tgt.shape[0]), src.data_ptr(),
+                                  w.data_ptr(), int(src.shape[0]), m, out.data_ptr(),
+                                  _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                  "bfmm_direct")
+    res = out if as_tensor else out.cpu().numpy()
+    return res[:, 0] if squeeze else res
+
+
 def evaluate(kernel: KernelSpec, plan: FmmPlan, sources, targets=None, weights=None,
              cache_dir=None, threads: int = 1, table: M2LTable = None):
     """One-shot wrapper (reference engine.py:539-545)."""
@@ -560,4 +615,4 @@ def evaluate(kernel: KernelSpec, plan: FmmPlan, sources, targets=None, weights=N
     return ev.evaluate(sources, targets, weights)
 
 
-__all__ = ["FmmEvaluator", "evaluate", "neighbor_offsets"]
+__all__ = ["FmmEvaluator", "direct_evaluate", "evaluate", "neighbor_offsets"]

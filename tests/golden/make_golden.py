@@ -274,7 +274,24 @@ def case_config(name, scale, direct=True, threads=1):
     save(f"{name.lower()}_s{scale}", **out)
 
 
+def case_eig():
+    """randomized_eig on the FMM matvec, k + q = 120 columns (lin:39-104)."""
+    from boxfmm.linops import evaluator_matvec, randomized_eig
+    pts, _ = unit_cloud(4000, seed=31)
+    kernel = ref_kernel("exp03")
+    plan = FmmPlan(levels=3, order=5, scheme="chebyshev", eps=1e-7,
+                   domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ev = reng.FmmEvaluator(kernel, plan, cache_dir=CACHE)
+    t0 = time.perf_counter()
+    res = randomized_eig(evaluator_matvec(ev, pts), len(pts), 100, oversample=20, seed=7,
+                         power_iters=1)
+    print("eig", time.perf_counter() - t0, "s")
+    save("eig", pts=pts, eigenvalues=res.eigenvalues, matvec_columns=np.array(res.matvec_columns),
+         vec0=res.eigenvectors[:, 0])
+
+
 CASES = {
+    "eig": case_eig,
     "tree": case_tree,
     "lists": case_lists,
     "tables": case_tables,
