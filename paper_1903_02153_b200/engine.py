@@ -449,14 +449,19 @@ class FmmEvaluator:
         if self.keep_stages:
             self.stages = {"stree": stree, "ttree": ttree, "moments": moments, "locals": locs,
                            "near": near, "far": phi_far, "ws": ws}
+        phi_host = None
+        if not as_tensor or out_device.type != "cuda":
+            # async D2H into pinned memory, ordered before the status read
+            phi_host = torch.empty((n_tgt, m), dtype=torch.float64, pin_memory=True)
+            phi_host.copy_(phi, non_blocking=True)
         stat = status.cpu().numpy()  # the one synchronising read-back
         self.kernel_ms = {name: a.elapsed_time(b) for name, a, b in self._kpending}
         self._kpending = []
         self._raise_flags(stat, ttree, stree)
         if as_tensor:
-            result = phi if out_device.type == "cuda" else phi.to(out_device)
+            result = phi if out_device.type == "cuda" else phi_host
         else:
-            result = phi.cpu().numpy()
+            result = phi_host.numpy()
         total_host = time.perf_counter() - t_host0
         ms = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(6)]
         self.timings = {
