@@ -65,6 +65,18 @@ int bfmm_gather_weights(const double *w, int64_t n, int m,
                         const int64_t *perm, double *wsorted, double *pts4,
                         bfmm_stream_t stream);
 
+/* Active cells for sparse clouds: the sorted distinct ancestors
+ * leaves[i] >> shift (shift = 3 * (levels - level)) of the n_leaves
+ * (device) occupied leaves that lie in [lo, hi) -> list, their number ->
+ * *count (device).  Only these cells' local expansions can reach a target
+ * point (L2L / L2P descend from occupied cells only, engine.py:206-226), so
+ * the M2L restricted to them (bfmm_m2l_cheb_list) gives the same phi. */
+size_t bfmm_active_cells_scratch_bytes(int64_t max_leaves);
+int bfmm_active_cells(const int64_t *leaves, const int64_t *n_leaves,
+                      int64_t max_leaves, int shift, int64_t lo, int64_t hi,
+                      void *scratch, size_t scratch_bytes, int64_t *list,
+                      int64_t *count, bfmm_stream_t stream);
+
 /* ---- upward pass ------------------------------------------------------- */
 
 /* P2M leaf_moments (engine.py:159-185).  interp (host) holds the 1-D
@@ -98,6 +110,12 @@ int bfmm_m2m(const double *child, double *parent, int64_t n_parent, int p,
 int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
                    int N, double *C, double alpha, double beta, int a_splits,
                    bfmm_stream_t stream);
+/* Same, but A row r lands in C row groups[r / group_rows] * group_rows +
+ * r % group_rows (compact rows of listed cells scattered to their cells). */
+int bfmm_rows_gemm_scatter(const double *A, int64_t rows, int K,
+                           const double *B, int N, double *C, double alpha,
+                           double beta, int a_splits, const int64_t *groups,
+                           int64_t group_rows, bfmm_stream_t stream);
 
 /* M2L Chebyshev (engine.py:228-256): for every cell c at `level` and
  * column, lt[c][i] = sum over the valid far offsets t of
@@ -117,6 +135,12 @@ int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq);
 int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
                   int nsplit, int64_t q_lo, int64_t nq, const double *cores,
                   bfmm_stream_t stream);
+/* Same translation for the nq listed parents qlist (device, from
+ * bfmm_active_cells at level - 1) only; lt is compact: layout
+ * (nq, 8, m, nsplit, rp), row (8 q + o) for child o of qlist[q]. */
+int bfmm_m2l_cheb_list(const double *z, double *lt, int level, int m, int rp,
+                       int nsplit, const int64_t *qlist, int64_t nq,
+                       const double *cores, bfmm_stream_t stream);
 
 /* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
  * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ) over the valid far

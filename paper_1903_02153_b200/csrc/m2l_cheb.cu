@@ -24,13 +24,23 @@ namespace {
 
 constexpr int TM = 64, TN = 64, KC = 8, kThreads = 256;
 
+// Output row of A row r: r itself, or -- for the compact rows of listed
+// cells -- groups[r / group_rows] * group_rows + r % group_rows.
+__device__ __forceinline__ int64_t c_row(int64_t r, const int64_t *groups,
+                                         int64_t group_rows) {
+  if (!groups) return r;
+  const int64_t g = r / group_rows;
+  return groups[g] * group_rows + (r - g * group_rows);
+}
+
 // ----------------------------------------------------------------------------
 // Generic tiled DGEMM for row-major (rows x K) @ (K x N); the A operand may
 // be stored as a_splits blocks per row that are summed on load.
 __global__ void __launch_bounds__(kThreads)
 rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
                  int a_splits, const double *__restrict__ B, int N,
-                 double *__restrict__ C, double alpha, double beta) {
+                 double *__restrict__ C, double alpha, double beta,
+                 const int64_t *__restrict__ groups, int64_t group_rows) {
   __shared__ double As[2][KC][TM];
   __shared__ double Bs[2][KC][TN];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -89,13 +99,14 @@ rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
   for (int i = 0; i < 4; ++i) {
     const int64_t r = r0 + ty + 16 * i;
     if (r >= rows) continue;
+    const int64_t cr = c_row(r, groups, group_rows);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx + 16 * j;
       if (n >= N) continue;
       double v = alpha * acc[i][j];
-      if (beta != 0.0) v += beta * C[r * N + n];
-      C[r * N + n] = v;
+      if (beta != 0.0) v += beta * C[cr * N + n];
+      C[cr * N + n] = v;
     }
   }
 }
@@ -120,7 +131,8 @@ __global__ void reduce_splits_kernel(double *__restrict__ A, int64_t rows, int K
 __global__ void __launch_bounds__(128)
 small_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
                   int a_splits, const double *__restrict__ B, int N,
-                  double *__restrict__ C, double alpha, double beta) {
+                  double *__restrict__ C, double alpha, double beta,
+                  const int64_t *__restrict__ groups, int64_t group_rows) {
   const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (e >= rows * N) return;
   const int64_t r = e / N;
@@ -135,9 +147,10 @@ small_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
   }
   for (; k < K; ++k) acc4[0] = fma(a[k], B[(int64_t)k * N + n], acc4[0]);
   const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+  const int64_t ce = c_row(r, groups, group_rows) * N + n;
   double out = alpha * acc;
-  if (beta != 0.0) out += beta * C[e];
-  C[e] = out;
+  if (beta != 0.0) out += beta * C[ce];
+  C[ce] = out;
 }
 
 // ----------------------------------------------------------------------------
@@ -287,9 +300,10 @@ extern "C" int bfmm_far_pairs(int level, int t_index, int64_t *tg, int64_t *sr,
   return check_launch("far_emit_kernel");
 }
 
-extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
-                              const double *B, int N, double *C, double alpha,
-                              double beta, int a_splits, bfmm_stream_t stream) {
+static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int N,
+                     double *C, double alpha, double beta, int a_splits,
+                     const int64_t *groups, int64_t group_rows,
+                     bfmm_stream_t stream) {
   if (rows <= 0 || N <= 0) return 0;
   if (a_splits < 1) {
     set_error("bfmm_rows_gemm: a_splits=%d < 1", a_splits);
@@ -304,13 +318,32 @@ extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
   if (rows * N <= (int64_t(1) << 17)) {
     // small problem (coarse tree levels): one thread per output, full K
     small_gemm_kernel<<<(unsigned)ceil_div(rows * N, 128), 128, 0, st>>>(
-        A, rows, K, a_splits, B, N, C, alpha, beta);
+        A, rows, K, a_splits, B, N, C, alpha, beta, groups, group_rows);
     return check_launch("small_gemm_kernel");
   }
   dim3 grid((unsigned)ceil_div(rows, TM), (unsigned)ceil_div(N, TN));
   rows_gemm_kernel<<<grid, kThreads, 0, st>>>(A, rows, K, a_splits, B, N, C,
-                                              alpha, beta);
+                                              alpha, beta, groups, group_rows);
   return check_launch("rows_gemm_kernel");
+}
+
+extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
+                              const double *B, int N, double *C, double alpha,
+                              double beta, int a_splits, bfmm_stream_t stream) {
+  return rows_gemm(A, rows, K, B, N, C, alpha, beta, a_splits, nullptr, 1, stream);
+}
+
+extern "C" int bfmm_rows_gemm_scatter(const double *A, int64_t rows, int K,
+                                      const double *B, int N, double *C,
+                                      double alpha, double beta, int a_splits,
+                                      const int64_t *groups, int64_t group_rows,
+                                      bfmm_stream_t stream) {
+  if (!groups || group_rows < 1) {
+    set_error("bfmm_rows_gemm_scatter: groups=%p group_rows=%lld", (const void *)groups,
+              (long long)group_rows);
+    return 2;
+  }
+  return rows_gemm(A, rows, K, B, N, C, alpha, beta, a_splits, groups, group_rows, stream);
 }
 
 extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq) {
@@ -355,6 +388,29 @@ extern "C" int bfmm_m2l_cheb(const double *z, double *lt, int level, int m,
     return 2;
   }
   ensure_offsets();
-  M2LCall a{z, lt, level, m, rp, nsplit, q_lo, nq, cores, as_stream(stream)};
+  M2LCall a{z, lt, level, m, rp, nsplit, q_lo, nq, nullptr, cores, as_stream(stream)};
+  return dispatch_ws(m2l_mw(nq * m), m2l_nt8(rp), a);
+}
+
+extern "C" int bfmm_m2l_cheb_list(const double *z, double *lt, int level, int m,
+                                  int rp, int nsplit, const int64_t *qlist,
+                                  int64_t nq, const double *cores,
+                                  bfmm_stream_t stream) {
+  if (rp % 8 != 0 || rp <= 0 || level < 2 || level > 10) {
+    set_error("bfmm_m2l_cheb_list: rp=%d must be a positive multiple of 8, level=%d",
+              rp, level);
+    return 2;
+  }
+  if (nsplit < 1 || nsplit > 189) {
+    set_error("bfmm_m2l_cheb_list: nsplit=%d outside [1, 189]", nsplit);
+    return 2;
+  }
+  if (nq < 0 || nq > (int64_t(1) << (3 * level - 3)) || (nq > 0 && !qlist)) {
+    set_error("bfmm_m2l_cheb_list: %lld listed parents invalid at level %d",
+              (long long)nq, level);
+    return 2;
+  }
+  ensure_offsets();
+  M2LCall a{z, lt, level, m, rp, nsplit, 0, nq, qlist, cores, as_stream(stream)};
   return dispatch_ws(m2l_mw(nq * m), m2l_nt8(rp), a);
 }

@@ -54,6 +54,7 @@ template <int NT8, int MW>
 __global__ void __launch_bounds__(WsShape<NT8, MW>::threads, 2)
 m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
               int m, int rp, int nsplit, int64_t q_lo, int64_t nq,
+              const int64_t *__restrict__ qlist,
               const double *__restrict__ cores) {
   using S = WsShape<NT8, MW>;
   constexpr int TM = S::TM, TNc = S::TN, LDK = S::LDK;
@@ -65,7 +66,9 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
   const int per = (189 + nsplit - 1) / nsplit;
   const int v_lo = split * per, v_hi = min(189, v_lo + per);
   const int n = 1 << level;
-  // rows: (parent q in [q_lo, q_lo + nq), column) of target cells 8q + o
+  // rows: (parent index q < nq, column) of target cells 8Q + o, where the
+  // parent is Q = q_lo + q (dense range; lt rows absolute) or Q = qlist[q]
+  // (active parents only; lt rows compact, (8q + o) * m + column)
   const int64_t rows = nq * m;
   const int64_t row0 = int64_t(blockIdx.x) * TM;
   const int n0 = blockIdx.y * TNc;
@@ -95,7 +98,8 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
       if (rok[i]) {
         const int64_t q = r / m;
         colm[i] = (int)(r - q * m);
-        unmorton3((uint64_t)(8 * (q_lo + q) + o), cx[i], cy[i], cz[i]);
+        const int64_t qa = qlist ? qlist[q] : q_lo + q;
+        unmorton3((uint64_t)(8 * qa + o), cx[i], cy[i], cz[i]);
       }
     }
     int64_t srow[RPL];
@@ -179,7 +183,8 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
     if (r >= rows) continue;
     const int64_t q = r / m;
     const int c = (int)(r - q * m);
-    double *dst = lt + (((8 * (q_lo + q) + o) * m + c) * nsplit + split) * rp;
+    const int64_t qo = qlist ? q : q_lo + q;
+    double *dst = lt + (((8 * qo + o) * m + c) * nsplit + split) * rp;
 #pragma unroll
     for (int j = 0; j < NT8; ++j) {
       const int col = n0 + j * 8 + 2 * t4;
@@ -195,6 +200,7 @@ struct M2LCall {
   double *lt;
   int level, m, rp, nsplit;
   int64_t q_lo, nq;  // target parents [q_lo, q_lo + nq) at level - 1
+  const int64_t *qlist;  // or: nq listed parents (nullptr = dense range)
   const double *cores;
   cudaStream_t st;
 };
@@ -212,7 +218,7 @@ int launch_ws(const M2LCall &a) {
   if (rows <= 0) return 0;
   dim3 grid((unsigned)ceil_div(rows, S::TM), (unsigned)ceil_div(a.rp, S::TN), 8 * a.nsplit);
   m2l_ws_kernel<NT8, MW><<<grid, S::threads, S::smem, a.st>>>(
-      a.z, a.lt, a.level, a.m, a.rp, a.nsplit, a.q_lo, a.nq, a.cores);
+      a.z, a.lt, a.level, a.m, a.rp, a.nsplit, a.q_lo, a.nq, a.qlist, a.cores);
   return check_launch("m2l_ws_kernel");
 }
 

@@ -210,6 +210,38 @@ int build(const double *points, int64_t n, const TreeGeom &g, int levels,
   return check_launch("gather_points_kernel");
 }
 
+// Active cells of a coarser level: the distinct ancestors (leaf >> shift) of
+// the occupied leaves that fall in [lo, hi).  `leaves` is sorted, so an
+// ancestor is new exactly where it differs from its predecessor's.
+__global__ void active_flags_kernel(const int64_t *__restrict__ leaves,
+                                    const int64_t *__restrict__ n_leaves,
+                                    int64_t cap, int shift, int64_t lo,
+                                    int64_t hi, int32_t *__restrict__ flag) {
+  const int64_t nl = *n_leaves;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cap;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int32_t f = 0;
+    if (i < nl) {
+      const int64_t a = leaves[i] >> shift;
+      f = (a >= lo && a < hi && (i == 0 || (leaves[i - 1] >> shift) != a)) ? 1 : 0;
+    }
+    flag[i] = f;
+  }
+}
+
+__global__ void active_emit_kernel(const int64_t *__restrict__ leaves,
+                                   int64_t cap, int shift,
+                                   const int32_t *__restrict__ flag,
+                                   const int32_t *__restrict__ pos,
+                                   int64_t *__restrict__ list,
+                                   int64_t *__restrict__ count) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cap;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (flag[i]) list[pos[i]] = leaves[i] >> shift;
+    if (i == cap - 1) *count = (int64_t)pos[i] + flag[i];
+  }
+}
+
 }  // namespace
 }  // namespace bfmm
 
@@ -260,4 +292,47 @@ extern "C" int bfmm_gather_weights(const double *w, int64_t n, int m,
   gather_weights_kernel<<<grid_for(n * m, 256), 256, 0, as_stream(stream)>>>(
       w, n, m, perm, wsorted, pts4);
   return check_launch("gather_weights_kernel");
+}
+
+extern "C" size_t bfmm_active_cells_scratch_bytes(int64_t max_leaves) {
+  if (max_leaves < 1) max_leaves = 1;
+  size_t cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int32_t *)nullptr,
+                                (int32_t *)nullptr, (int)max_leaves);
+  return 2 * ((max_leaves * sizeof(int32_t) + 255) & ~size_t(255)) + cub_bytes;
+}
+
+extern "C" int bfmm_active_cells(const int64_t *leaves, const int64_t *n_leaves,
+                                 int64_t max_leaves, int shift, int64_t lo,
+                                 int64_t hi, void *scratch, size_t scratch_bytes,
+                                 int64_t *list, int64_t *count,
+                                 bfmm_stream_t stream) {
+  if (max_leaves < 1 || max_leaves > INT32_MAX || shift < 0 || shift > 60) {
+    set_error("bfmm_active_cells: max_leaves=%lld shift=%d unsupported",
+              (long long)max_leaves, shift);
+    return 2;
+  }
+  if (scratch_bytes < bfmm_active_cells_scratch_bytes(max_leaves)) {
+    set_error("bfmm_active_cells: scratch too small");
+    return 2;
+  }
+  cudaStream_t st = as_stream(stream);
+  const size_t a = (max_leaves * sizeof(int32_t) + 255) & ~size_t(255);
+  int32_t *flag = static_cast<int32_t *>(scratch);
+  int32_t *pos = reinterpret_cast<int32_t *>(static_cast<char *>(scratch) + a);
+  void *tmp = static_cast<char *>(scratch) + 2 * a;
+  size_t tb = scratch_bytes - 2 * a;
+  const int T = 256;
+  active_flags_kernel<<<grid_for(max_leaves, T), T, 0, st>>>(leaves, n_leaves, max_leaves,
+                                                            shift, lo, hi, flag);
+  if (check_launch("active_flags_kernel")) return 1;
+  if (cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, (int)max_leaves, st) !=
+      cudaSuccess) {
+    set_error("bfmm_active_cells: scan failed");
+    return 1;
+  }
+  add_launches(2);
+  active_emit_kernel<<<grid_for(max_leaves, T), T, 0, st>>>(leaves, max_leaves, shift, flag,
+                                                           pos, list, count);
+  return check_launch("active_emit_kernel");
 }

@@ -105,6 +105,11 @@ class FmmEvaluator:
         self.stages = {}
         self.profile_kernels = False
         self.near_mode = "auto"  # "auto" | "full" | "symmetric"
+        # Chebyshev M2L over every cell ("dense"), over the ancestors of
+        # occupied target leaves only ("active"), or "auto": active lists for
+        # sparse clouds (fewer than 8 points per leaf cell), per level only
+        # where they cut the target rows below 3/4
+        self.far_mode = "auto"
         self.kernel_ms = {}
         self._kpending = []
 
@@ -249,12 +254,46 @@ class FmmEvaluator:
                 qhi - qlo, p, m, _native.dptr(self._H), st), "bfmm_m2m")
         return moments, leaf_geom
 
-    def _far_field(self, moments, m, shard):
+    def _active_parents(self, ttree, shard):
+        """{level: (parents at level - 1 with an occupied target leaf below,
+        their number)} for the levels where the list pays (see far_mode)."""
+        torch = _torch()
+        L = self.plan.levels
+        if self.plan.scheme is not SchemeKind.CHEBYSHEV or self.far_mode == "dense":
+            return {}
+        if self.far_mode == "auto" and ttree.n >= 8 * (1 << (3 * L)):
+            return {}
+        cap = max(ttree.max_leaves, 1)
+        sb = self.lib.bfmm_active_cells_scratch_bytes(cap)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        levels = list(range(2, L + 1))
+        counts = torch.zeros(len(levels), dtype=torch.int64, device=self.device)
+        lists = {}
+        st = self._stream()
+        for i, lev in enumerate(levels):
+            lo, hi = self._cells(lev, shard)
+            qlo, qhi = lo // 8, hi // 8
+            lst = torch.empty(min(cap, qhi - qlo) or 1, dtype=torch.int64, device=self.device)
+            _native.check(self.lib.bfmm_active_cells(
+                ttree.leaves.data_ptr(), ttree.n_leaves.data_ptr(), cap, 3 * (L - lev + 1),
+                qlo, qhi, scratch.data_ptr(), sb, lst.data_ptr(), counts[i:].data_ptr(), st),
+                "bfmm_active_cells")
+            lists[lev] = (lst, qhi - qlo)
+        nact = counts.cpu().numpy()  # one read-back sizes every level's grid
+        out = {}
+        for i, lev in enumerate(levels):
+            lst, nq = lists[lev]
+            if self.far_mode == "active" or nact[i] * 4 < nq * 3:
+                out[lev] = (lst, int(nact[i]))
+        return out
+
+    def _far_field(self, moments, m, shard, active=None):
         torch = _torch()
         L, p = self.plan.levels, self.plan.order
         p3 = p ** 3
         st = self._stream()
         locs = {}
+        active = active or {}
         for lev in range(2, L + 1):
             blk = self._dev_block(lev)
             scale = float(self.table.scale_for_level(lev))
@@ -262,7 +301,31 @@ class FmmEvaluator:
             lo, hi = self._cells(lev, shard)
             nloc = hi - lo
             out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
-            if blk["kind"] == "cheb":
+            if blk["kind"] == "cheb" and lev in active:
+                # only the children of active parents: compact lt rows
+                qlist, nact = active[lev]
+                rp = blk["rp"]
+                ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, max(nact, 1)))
+                z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
+                lt = torch.empty((max(nact, 1) * 8 * m * ns * rp,), dtype=torch.float64,
+                                 device=self.device)
+                out.zero_()
+                _native.check(self.lib.bfmm_rows_gemm(
+                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                    z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+                if shard is not None and not shard[0].full:
+                    shard[1].allgather_cells(z, m * rp, lev)
+                e0 = self._kevent()
+                _native.check(self.lib.bfmm_m2l_cheb_list(z.data_ptr(), lt.data_ptr(), lev, m, rp,
+                                                          ns, qlist.data_ptr(), nact,
+                                                          blk["cores"].data_ptr(), st),
+                              "bfmm_m2l_cheb_list")
+                self._kspan(f"m2l_l{lev}", e0)
+                if nact:
+                    _native.check(self.lib.bfmm_rows_gemm_scatter(
+                        lt.data_ptr(), nact * 8 * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
+                        scale, 0.0, ns, qlist.data_ptr(), 8 * m, st), "bfmm_rows_gemm_scatter(U)")
+            elif blk["kind"] == "cheb":
                 rp = blk["rp"]
                 ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nloc // 8))
                 z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
@@ -423,7 +486,7 @@ class FmmEvaluator:
         # sharded: rows of other ranks' targets must read as zero
         alloc = torch.zeros if sharded else torch.empty
         if not self._disable_far_field:
-            locs = self._far_field(moments, m, shard)
+            locs = self._far_field(moments, m, shard, self._active_parents(ttree, shard))
             ev[4].record()
             phi_far = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
             self._downward(locs, ttree, m, leaf_geom, status, phi_far, shard)

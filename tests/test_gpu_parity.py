@@ -372,3 +372,28 @@ def test_empty_leaves_and_clusters(cache_dir):
     ref = O.OracleFMM(bf.LAPLACIAN, 5, 3, "chebyshev", 1e-6, (0.5, 0.5, 0.5), 1.0).matvec(
         pts, weights=w)
     assert rel_l2(got, ref) < PHI_TOL
+
+
+@pytest.mark.parametrize("ncols,distinct", [(1, False), (3, False), (1, True)])
+def test_active_far_field_matches_dense(ncols, distinct, cache_dir):
+    """M2L over the ancestors of occupied target leaves only (far_mode
+    "active") gives the dense result: empty cells' locals never reach a
+    target (engine.py:206-226)."""
+    gen = np.random.default_rng(83)
+    pts = np.vstack([np.clip(c + 0.02 * gen.standard_normal((4000, 3)), 0, 1)
+                     for c in (0.2, 0.55, 0.8)])
+    w = gen.standard_normal((len(pts), ncols))
+    tg = np.clip(0.6 + 0.05 * gen.standard_normal((3000, 3)), 0, 1) if distinct else None
+    plan = bf.FmmPlan(levels=5, order=4, eps=1e-7, domain_center=(0.5, 0.5, 0.5),
+                      domain_length=1.0)
+    ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+    res = {}
+    for mode in ("dense", "active", "auto"):
+        ev.far_mode = mode
+        res[mode] = ev.evaluate(pts, targets=tg, weights=w)
+    assert rel_l2(res["active"], res["dense"]) < 1e-14
+    assert rel_l2(res["auto"], res["dense"]) < 1e-14
+    if not distinct:
+        ref = O.OracleFMM(bf.EXPONENTIAL, 5, 4, "chebyshev", 1e-7, (0.5, 0.5, 0.5), 1.0).matvec(
+            pts, weights=w)
+        assert rel_l2(res["active"], ref.reshape(res["active"].shape)) < PHI_TOL

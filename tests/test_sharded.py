@@ -105,21 +105,30 @@ class ThreadComm:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,scheme", [(2, "chebyshev"), (4, "chebyshev"), (2, "uniform")])
-def test_sharded_matvec_matches_unsharded(world, scheme, cache_dir):
+@pytest.mark.parametrize("world,scheme,far_mode", [(2, "chebyshev", "dense"),
+                                                   (4, "chebyshev", "dense"),
+                                                   (2, "uniform", "dense"),
+                                                   (4, "chebyshev", "active")])
+def test_sharded_matvec_matches_unsharded(world, scheme, far_mode, cache_dir):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1903_02153_b200 as bf
     pts, w = unit_cloud(30000, seed=51, ncols=2)
+    if far_mode == "active":  # two clusters: most cells empty, shards uneven
+        pts[:15000] = np.clip(0.3 + 0.03 * np.random.default_rng(5).standard_normal((15000, 3)), 0, 1)
+        pts[15000:] = np.clip(0.8 + 0.02 * np.random.default_rng(6).standard_normal((15000, 3)), 0, 1)
     plan = bf.FmmPlan(levels=4, order=4, scheme=scheme, eps=1e-6,
                       domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
-    ref = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir).evaluate(pts, weights=w)
+    ref_ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+    ref_ev.far_mode = "dense"
+    ref = ref_ev.evaluate(pts, weights=w)
     board, barrier = {}, threading.Barrier(world)
     out, errs = {}, []
 
     def rank_main(r):
         try:
             ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+            ev.far_mode = far_mode
             with torch.cuda.stream(torch.cuda.Stream()):
                 out[r] = ev.evaluate(pts, weights=w, _shard=(MortonShards(world, r),
                                                              ThreadComm(world, r, board, barrier)))
