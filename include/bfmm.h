@@ -179,8 +179,11 @@ int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
  * 3 gaussian, 4 exponential, 5 logarithm. */
 int bfmm_kernel_compile(int kind, const char *expr, int *handle);
 
-/* Scratch bytes bfmm_p2p needs (per-leaf chunk prefix). */
-size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves);
+/* Scratch bytes bfmm_p2p needs for n_targets points in at most max_tleaves
+ * occupied leaves (per-leaf chunk prefix, chunk -> leaf map, work counter).
+ * n_targets = 0 gives the minimum, without the map (chunks are then located
+ * by binary search). */
+size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves, int64_t n_targets);
 
 /* out[i] = sum over the 27 neighbour leaves of the target leaf of
  * K(x_i - y_j) w_j, targets and sources both in sorted order; assigns the

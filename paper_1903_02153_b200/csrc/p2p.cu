@@ -142,9 +142,23 @@ int jit_compile(int kind, const char *expr, int *handle) {
   names.push_back("bfmm_nf::p2p_sym_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::direct_kernel<bfmm_nf::KUser>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
-  const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17",
-                        "-default-device", "-lineinfo"};
-  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--std=c++17",
+                                    "-default-device", "-lineinfo"};
+  // BFMM_JIT_OPTS: extra NVRTC options (tuning experiments, e.g. -D...)
+  if (const char *extra = getenv("BFMM_JIT_OPTS")) {
+    std::string e(extra), tok;
+    for (size_t i = 0; i <= e.size(); ++i) {
+      if (i == e.size() || e[i] == ' ') {
+        if (!tok.empty()) opt_s.push_back(tok);
+        tok.clear();
+      } else {
+        tok += e[i];
+      }
+    }
+  }
+  std::vector<const char *> opts;
+  for (auto &o : opt_s) opts.push_back(o.c_str());
+  nvrtcResult rc = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
   if (rc != NVRTC_SUCCESS) {
     size_t logn = 0;
     nvrtcGetProgramLogSize(prog, &logn);
@@ -289,6 +303,20 @@ __global__ void chunk_counts_kernel(const int64_t *__restrict__ counts,
                  ? (counts[i] + 31) / 32 : 0;
 }
 
+// chunk -> leaf map from the inclusive chunk prefix (entries past cap are
+// left to the kernel's binary search)
+__global__ void chunk_map_kernel(const int64_t *__restrict__ incl,
+                                 const int64_t *__restrict__ n_leaves,
+                                 int64_t max_leaves, int64_t cap,
+                                 int32_t *__restrict__ chunk_leaf) {
+  const int64_t nl = *n_leaves;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+       i < max_leaves && i < nl; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c1 = incl[i] < cap ? incl[i] : cap;
+    for (int64_t c = i ? incl[i - 1] : 0; c < c1; ++c) chunk_leaf[c] = (int32_t)i;
+  }
+}
+
 __global__ void scatter_kernel(const double *__restrict__ far,
                                const double *__restrict__ near,
                                const int64_t *__restrict__ perm, int64_t n,
@@ -361,13 +389,21 @@ __global__ void near_count_kernel(const int64_t *__restrict__ tleaves,
   atomicAdd(total, local);
 }
 
-size_t p2p_scratch(int64_t max_leaves, size_t *cub_off) {
+// Layout: nch[max_leaves] | incl[max_leaves] | CUB temp | chunk counter
+// (256 B) | chunk -> leaf map (int32, room for every chunk of n_targets
+// points: at most one partial chunk per leaf plus n/32 full ones; the map is
+// used only when the caller's scratch holds all of it).
+size_t p2p_fixed(int64_t max_leaves, size_t *cub_off) {
   size_t cub_bytes = 0;
   cub::DeviceScan::InclusiveSum(nullptr, cub_bytes, (int64_t *)nullptr,
                                 (int64_t *)nullptr, (int)max_leaves);
   size_t a = ((size_t)max_leaves * 2 * sizeof(int64_t) + 255) & ~size_t(255);
   *cub_off = a;
-  return a + cub_bytes + 256;
+  return a + ((cub_bytes + 255) & ~size_t(255));
+}
+size_t p2p_scratch(int64_t max_leaves, size_t *cub_off, int64_t n_targets = 0) {
+  const size_t map = n_targets > 0 ? (size_t)(max_leaves + n_targets / 32 + 1) : 0;
+  return p2p_fixed(max_leaves, cub_off) + ((map * sizeof(int32_t) + 255) & ~size_t(255)) + 256;
 }
 
 bfmm_nf::Args make_args(const double *tpts4, const int64_t *tleaves,
@@ -391,6 +427,9 @@ bfmm_nf::Args make_args(const double *tpts4, const int64_t *tleaves,
   a.out = out;
   a.work_incl = reinterpret_cast<const long long *>(work);
   a.gate = nullptr;
+  a.work_ctr = nullptr;
+  a.chunk_leaf = nullptr;
+  a.chunk_cap = 0;
   return a;
 }
 
@@ -455,9 +494,9 @@ extern "C" int bfmm_kernel_compile(int kind, const char *expr, int *handle) {
   return jit_compile(kind, expr, handle);
 }
 
-extern "C" size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves) {
+extern "C" size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves, int64_t n_targets) {
   size_t off;
-  return p2p_scratch(max_tleaves < 1 ? 1 : max_tleaves, &off);
+  return p2p_scratch(max_tleaves < 1 ? 1 : max_tleaves, &off, n_targets);
 }
 
 extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
@@ -470,11 +509,17 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
                         bfmm_stream_t stream) {
   if (max_tleaves <= 0) return 0;
   size_t cub_off;
+  const size_t fixed = p2p_fixed(max_tleaves, &cub_off);
   size_t need = p2p_scratch(max_tleaves, &cub_off);
   if (scratch_bytes < need) {
     set_error("bfmm_p2p: scratch too small (%zu < %zu)", scratch_bytes, need);
     return 2;
   }
+  // chunk map capacity: whatever the caller's scratch holds between the
+  // fixed part and the counter (bfmm_p2p_scratch_bytes sizes it for n)
+  const int64_t map_cap = (int64_t)((scratch_bytes - 256 - fixed) / sizeof(int32_t));
+  auto *ctr = reinterpret_cast<unsigned long long *>(static_cast<char *>(scratch) + fixed);
+  int32_t *chunk_leaf = reinterpret_cast<int32_t *>(static_cast<char *>(scratch) + fixed + 256);
   cudaStream_t st = as_stream(stream);
   int64_t *nch = static_cast<int64_t *>(scratch);
   int64_t *incl = nch + max_tleaves;
@@ -483,7 +528,7 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
                         256, 0, st>>>(tcounts, tleaves, n_tleaves, max_tleaves,
                                       cell_lo, cell_hi, nch);
   if (check_launch("chunk_counts_kernel")) return 1;
-  size_t cb = need - cub_off;
+  size_t cb = fixed - cub_off;
   if (cub::DeviceScan::InclusiveSum(static_cast<char *>(scratch) + cub_off, cb,
                                     nch, incl, (int)max_tleaves,
                                     st) != cudaSuccess) {
@@ -494,7 +539,16 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
   bfmm_nf::Args a = make_args(tpts4, tleaves, tstarts, tcounts, n_tleaves,
                                spts4, swsorted, m, scell_start, scell_count,
                                levels, out, incl);
-  // persistent-style grid: 16 CTAs (64 warps) per SM, grid-stride over chunks
+  a.work_ctr = ctr;
+  if (map_cap > 0) {
+    chunk_map_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256), kNumSMs * 16),
+                       256, 0, st>>>(incl, n_tleaves, max_tleaves, map_cap, chunk_leaf);
+    if (check_launch("chunk_map_kernel")) return 1;
+    a.chunk_leaf = chunk_leaf;
+    a.chunk_cap = map_cap;
+  }
+  // 16 CTAs per SM (more than fit): every resident warp claims chunks from
+  // the counter until they run out, CTAs that start later find none
   dim3 grid(kNumSMs * 16);
   int c0 = 0;
   while (c0 < m) {
@@ -506,6 +560,10 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
     else if (left >= 4) mci = 2;
     else if (left >= 2) mci = 1;
     else mci = 0;
+    if (cudaMemsetAsync(ctr, 0, sizeof(*ctr), st) != cudaSuccess) {
+      set_error("bfmm_p2p: counter reset failed");
+      return 1;
+    }
     int rc = launch_p2p(handle, mci, grid, a, c0, st);
     if (rc) return rc;
     c0 += kMCs[mci];

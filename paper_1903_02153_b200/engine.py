@@ -110,6 +110,11 @@ class FmmEvaluator:
         # sparse clouds (fewer than 8 points per leaf cell), per level only
         # where they cut the target rows below 3/4
         self.far_mode = "auto"
+        # run the near field on a second stream, concurrent with the far
+        # field.  Measured on C2 (B200): 4.95 -> 4.90 ms only -- the DMMA M2L
+        # and the DFMA P2P contend for the same SMs -- so it is opt-in.
+        self.overlap_near = False
+        self._side = None
         self.kernel_ms = {}
         self._kpending = []
 
@@ -160,6 +165,12 @@ class FmmEvaluator:
     def _stream():
         torch = _torch()
         return _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _side_stream(self):
+        torch = _torch()
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
 
     def _prepare_points(self, arr, name):
         torch = _torch()
@@ -382,7 +393,7 @@ class FmmEvaluator:
     def _near_field(self, ttree, stree, ws, m, near, shard):
         torch = _torch()
         st = self._stream()
-        sb = self.lib.bfmm_p2p_scratch_bytes(max(ttree.max_leaves, 1))
+        sb = self.lib.bfmm_p2p_scratch_bytes(max(ttree.max_leaves, 1), ttree.n)
         scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
         lo, hi = self._cells(self.plan.levels, shard)
         if self._use_symmetric(ttree, stree, m):
@@ -480,11 +491,20 @@ class FmmEvaluator:
                       "bfmm_gather_weights")
         ev[2].record()
         shard = _shard if sharded else None
+        # sharded: rows of other ranks' targets must read as zero
+        alloc = torch.zeros if sharded else torch.empty
+        near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
+        side = None
+        if self.overlap_near and not sharded:
+            # near field on a side stream, concurrent with the far field
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self._near_field(ttree, stree, ws, m, near, shard)
         moments, leaf_geom = self._upward(stree, ws, m, status, shard)
         ev[3].record()
         phi_far = None
-        # sharded: rows of other ranks' targets must read as zero
-        alloc = torch.zeros if sharded else torch.empty
         if not self._disable_far_field:
             locs = self._far_field(moments, m, shard, self._active_parents(ttree, shard))
             ev[4].record()
@@ -494,8 +514,10 @@ class FmmEvaluator:
             locs = None
             ev[4].record()
         ev[5].record()
-        near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
-        self._near_field(ttree, stree, ws, m, near, shard)
+        if side is None:
+            self._near_field(ttree, stree, ws, m, near, shard)
+        else:
+            main.wait_stream(side)
         phi = torch.empty((n_tgt, m), dtype=torch.float64, device=self.device)
         _native.check(self.lib.bfmm_scatter_output(
             phi_far.data_ptr() if phi_far is not None else None, near.data_ptr(),
