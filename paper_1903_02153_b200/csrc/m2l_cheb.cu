@@ -1,7 +1,8 @@
 // Chebyshev far field (engine.py:228-256) as FP64 GEMMs.
 //
 //  * bfmm_rows_gemm: C = alpha * A @ B + beta * C, the basis projections
-//    z = M V and locals = scale * lt U^T (engine.py:233, 252-255).
+//    z = M V and locals = scale * lt U^T (engine.py:233, 252-255), on the
+//    FP64 tensor cores with a cp.async ring (proj_gemm_kernel).
 //  * bfmm_m2l_cheb: the 316-offset translation as ONE implicit GEMM per
 //    child octant.  Every target cell c of octant o needs exactly the 189
 //    offsets t whose +/-3 components match c's coordinate parity
@@ -11,7 +12,8 @@
 //    (rows of z at the shifted cells; zero-filled when the source leaves the
 //    grid, exactly the pairs cell_pairs_for_offset omits, octree.py:202-221).
 //    The MMA is the FP64 tensor-core instruction (DMMA, mma.sync m8n8k4 f64;
-//    tcgen05 has no f64 kind), operands staged by a 3-stage cp.async ring.
+//    tcgen05 has no f64 kind); a producer warp stages the operands with
+//    cp.async into an 8-stage mbarrier ring (m2l_ws.cuh).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -22,8 +24,6 @@
 namespace bfmm {
 namespace {
 
-constexpr int TM = 64, TN = 64, KC = 8, kThreads = 256;
-
 // Output row of A row r: r itself, or -- for the compact rows of listed
 // cells -- groups[r / group_rows] * group_rows + r % group_rows.
 __device__ __forceinline__ int64_t c_row(int64_t r, const int64_t *groups,
@@ -31,84 +31,6 @@ __device__ __forceinline__ int64_t c_row(int64_t r, const int64_t *groups,
   if (!groups) return r;
   const int64_t g = r / group_rows;
   return groups[g] * group_rows + (r - g * group_rows);
-}
-
-// ----------------------------------------------------------------------------
-// Generic tiled DGEMM for row-major (rows x K) @ (K x N); the A operand may
-// be stored as a_splits blocks per row that are summed on load.
-__global__ void __launch_bounds__(kThreads)
-rows_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
-                 int a_splits, const double *__restrict__ B, int N,
-                 double *__restrict__ C, double alpha, double beta,
-                 const int64_t *__restrict__ groups, int64_t group_rows) {
-  __shared__ double As[2][KC][TM];
-  __shared__ double Bs[2][KC][TN];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t r0 = int64_t(blockIdx.x) * TM;
-  const int n0 = blockIdx.y * TN;
-  double acc[4][4] = {};
-  const int la_r = threadIdx.x >> 2, la_k = (threadIdx.x & 3) * 2;
-  const int lb_k = threadIdx.x >> 5, lb_n = (threadIdx.x & 31) * 2;
-  double ra[2], rb[2];
-  auto load = [&](int k0) {
-    const int64_t r = r0 + la_r;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int k = k0 + la_k + u;
-      // row stride a_splits * K: split block 0 holds the reduced sum
-      ra[u] = (r < rows && k < K) ? A[(r * a_splits) * K + k] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int k = k0 + lb_k, n = n0 + lb_n + u;
-      rb[u] = (k < K && n < N) ? B[(int64_t)k * N + n] : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-    As[buf][la_k][la_r] = ra[0];
-    As[buf][la_k + 1][la_r] = ra[1];
-    Bs[buf][lb_k][lb_n] = rb[0];
-    Bs[buf][lb_k][lb_n + 1] = rb[1];
-  };
-  load(0);
-  store(0);
-  __syncthreads();
-  int buf = 0;
-  for (int k0 = 0; k0 < K; k0 += KC) {
-    const bool more = k0 + KC < K;
-    if (more) load(k0 + KC);
-#pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    if (more) {
-      store(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + ty + 16 * i;
-    if (r >= rows) continue;
-    const int64_t cr = c_row(r, groups, group_rows);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tx + 16 * j;
-      if (n >= N) continue;
-      double v = alpha * acc[i][j];
-      if (beta != 0.0) v += beta * C[cr * N + n];
-      C[cr * N + n] = v;
-    }
-  }
 }
 
 // A[r][0][k] = sum_s A[r][s][k] in place, fixed order (M2L split blocks).
@@ -121,36 +43,10 @@ __global__ void reduce_splits_kernel(double *__restrict__ A, int64_t rows, int K
     const int k = (int)(e - r * K);
     double *a = A + r * a_splits * K + k;
     double v = a[0];
+#pragma unroll 4
     for (int sp = 1; sp < a_splits; ++sp) v += a[(int64_t)sp * K];
     a[0] = v;
   }
-}
-
-// One thread per output for small (coarse-level) projections: a single 64-row
-// tile would serialise the whole K loop on one SM.
-__global__ void __launch_bounds__(128)
-small_gemm_kernel(const double *__restrict__ A, int64_t rows, int K,
-                  int a_splits, const double *__restrict__ B, int N,
-                  double *__restrict__ C, double alpha, double beta,
-                  const int64_t *__restrict__ groups, int64_t group_rows) {
-  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (e >= rows * N) return;
-  const int64_t r = e / N;
-  const int n = (int)(e - r * N);
-  const double *a = A + r * a_splits * K;  // split block 0 holds the sum
-  // four independent partial sums (fixed order) keep the FMA chain short
-  double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-  int k = 0;
-  for (; k + 4 <= K; k += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc4[u] = fma(a[k + u], B[(int64_t)(k + u) * N + n], acc4[u]);
-  }
-  for (; k < K; ++k) acc4[0] = fma(a[k], B[(int64_t)k * N + n], acc4[0]);
-  const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-  const int64_t ce = c_row(r, groups, group_rows) * N + n;
-  double out = alpha * acc;
-  if (beta != 0.0) out += beta * C[ce];
-  C[ce] = out;
 }
 
 // ----------------------------------------------------------------------------
@@ -220,6 +116,148 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 #include "m2l_ws.cuh"
+
+// ----------------------------------------------------------------------------
+// Basis projections on the FP64 tensor cores: C = alpha * A @ B (+ beta C),
+// A row-major (rows, K) with row stride lda, B row-major (K, N).  CTA tile
+// 64 rows x 64*WN columns, warp (wr, wc) owns rows 16 wr.. and columns
+// 64 wc..; K is staged 16 at a time through a kPjStages-deep cp.async ring
+// (8-byte copies: rows of 125 doubles are not 16-byte aligned), each thread
+// owning fixed tile slots so a refill is a handful of pointer bumps.
+// Strides: A 20 doubles, B 64*WN + 8, so each 8 x 4 DMMA fragment load is two
+// conflict-free wavefronts.
+constexpr int kPjTM = 64, kPjKC = 16, kPjLDA = 20, kPjStages = 4;
+
+template <int WN>
+constexpr int pj_ldb() { return 64 * WN + 8; }
+template <int WN>
+constexpr size_t pj_smem() {
+  return sizeof(double) * kPjStages * (kPjTM * kPjLDA + kPjKC * pj_ldb<WN>());
+}
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+
+template <int WN>
+__global__ void __launch_bounds__(128 * WN)
+proj_gemm_kernel(const double *__restrict__ A, int64_t rows, int64_t lda, int K,
+                 const double *__restrict__ B, int N, double *__restrict__ C, double alpha,
+                 double beta, const int64_t *__restrict__ groups, int64_t group_rows) {
+  constexpr int TN = 64 * WN, NT = 8, LDB = pj_ldb<WN>(), NTH = 128 * WN;
+  constexpr int A_ELEMS = kPjTM * kPjLDA, STAGE = A_ELEMS + kPjKC * LDB;
+  constexpr int AEPT = kPjTM * kPjKC / NTH;  // A slots per thread
+  constexpr int BEPT = kPjKC * TN / NTH;      // B slots per thread (8)
+  constexpr int AR_STEP = NTH / kPjKC;        // rows between a thread's A slots
+  constexpr int BK_STEP = NTH / TN;           // k rows between its B slots
+  extern __shared__ __align__(16) double pj[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 3, wc = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t row0 = int64_t(blockIdx.x) * kPjTM;
+  const int n0 = blockIdx.y * TN;
+  const int nk = (K + kPjKC - 1) / kPjKC;
+  // slot u of a thread: A (row ar + u AR_STEP, k ak), B (k bk + u BK_STEP,
+  // column bn): consecutive lanes walk consecutive k of a row (A) and
+  // consecutive columns (B), so each copy instruction touches 2-4 lines
+  const int ar = tid / kPjKC, ak = tid % kPjKC;
+  const int bk = tid / TN, bn = tid % TN;
+  const bool bn_ok = n0 + bn < N;
+  auto issue = [&](int chunk) {
+    double *As = pj + (chunk % kPjStages) * STAGE, *Bs = As + A_ELEMS;
+    const int k0 = chunk * kPjKC;
+    const bool akv = k0 + ak < K;
+#pragma unroll
+    for (int u = 0; u < AEPT; ++u) {
+      const int64_t r = row0 + ar + u * AR_STEP;
+      const bool v = akv && r < rows;
+      cp_async8(As + (ar + u * AR_STEP) * kPjLDA + ak, v ? A + r * lda + k0 + ak : A, v);
+    }
+#pragma unroll
+    for (int u = 0; u < BEPT; ++u) {
+      const int k = k0 + bk + u * BK_STEP;
+      const bool v = bn_ok && k < K;
+      cp_async8(Bs + (bk + u * BK_STEP) * LDB + bn, v ? B + (int64_t)k * N + n0 + bn : B, v);
+    }
+  };
+  double acc[2][NT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < kPjStages - 1; ++st) {
+    if (st < nk) issue(st);
+    cp_async_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<kPjStages - 2>();
+    __syncthreads();
+    // refill the stage consumed last iteration (everyone is past it now)
+    if (kc + kPjStages - 1 < nk) issue(kc + kPjStages - 1);
+    cp_async_commit();
+    const double *As = pj + (kc % kPjStages) * STAGE, *Bs = As + A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < kPjKC; ks += 4) {
+      double a[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = As[(wr * 16 + i * 8 + g) * kPjLDA + ks + t4];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const double b = Bs[(ks + t4) * LDB + wc * 64 + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b);
+      }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int64_t r = row0 + wr * 16 + i * 8 + g;
+    if (r >= rows) continue;
+    double *crow = C + c_row(r, groups, group_rows) * N;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wc * 64 + j * 8 + 2 * t4 + h;
+        if (n >= N) continue;
+        double v = alpha * acc[i][j][h];
+        if (beta != 0.0) v += beta * crow[n];
+        crow[n] = v;
+      }
+    }
+  }
+}
+
+// A[r][0][k] = sum_s A[r][s][k] in place for many splits: CTA per row, the
+// splits dealt round-robin to G = 256 / K thread groups that sum theirs in
+// order, then the G partials are added in group order (fixed tree, so the
+// result is the same on every run).
+__global__ void __launch_bounds__(256)
+reduce_splits_wide_kernel(double *__restrict__ A, int64_t rows, int K, int a_splits) {
+  __shared__ double part[256];
+  const int G = 256 / K;
+  const int t = threadIdx.x, k = t % K, grp = t / K;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    double *a = A + r * a_splits * (int64_t)K;
+    double v = 0.0;
+    if (grp < G) {
+#pragma unroll 4
+      for (int sp = grp; sp < a_splits; sp += G) v += a[(int64_t)sp * K + k];
+      part[grp * K + k] = v;
+    }
+    __syncthreads();
+    if (t < K) {
+      double s = part[t];
+      for (int gi = 1; gi < G; ++gi) s += part[gi * K + t];
+      a[t] = s;
+    }
+    __syncthreads();
+  }
+}
 
 // ----------------------------------------------------------------------------
 // Explicit far list for one offset, in the reference's meshgrid(ij) order
@@ -305,26 +343,40 @@ static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int 
                      const int64_t *groups, int64_t group_rows,
                      bfmm_stream_t stream) {
   if (rows <= 0 || N <= 0) return 0;
-  if (a_splits < 1) {
-    set_error("bfmm_rows_gemm: a_splits=%d < 1", a_splits);
+  if (a_splits < 1 || K < 1) {
+    set_error("bfmm_rows_gemm: a_splits=%d K=%d", a_splits, K);
     return 2;
   }
   cudaStream_t st = as_stream(stream);
-  if (a_splits > 1) {
-    reduce_splits_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * K, 256), 4096), 256,
-                           0, st>>>(const_cast<double *>(A), rows, K, a_splits);
+  // split blocks are first summed in place into block 0, in a fixed order
+  if (a_splits > 16 && K <= 256) {
+    reduce_splits_wide_kernel<<<(unsigned)std::min<int64_t>(rows, 65535), 256, 0, st>>>(
+        const_cast<double *>(A), rows, K, a_splits);
+    if (check_launch("reduce_splits_wide_kernel")) return 1;
+  } else if (a_splits > 1) {
+    reduce_splits_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * K, 256), 8192), 256, 0,
+                           st>>>(const_cast<double *>(A), rows, K, a_splits);
     if (check_launch("reduce_splits_kernel")) return 1;
   }
-  if (rows * N <= (int64_t(1) << 17)) {
-    // small problem (coarse tree levels): one thread per output, full K
-    small_gemm_kernel<<<(unsigned)ceil_div(rows * N, 128), 128, 0, st>>>(
-        A, rows, K, a_splits, B, N, C, alpha, beta, groups, group_rows);
-    return check_launch("small_gemm_kernel");
+  const int64_t lda = (int64_t)a_splits * K;
+  // one CTA spans all N <= 128 columns, so A is read once
+  const int wn = N > 64 ? 2 : 1;
+  dim3 grid((unsigned)ceil_div(rows, kPjTM), (unsigned)ceil_div(N, 64 * wn));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(proj_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pj_smem<1>());
+    cudaFuncSetAttribute(proj_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pj_smem<2>());
+    attr = true;
   }
-  dim3 grid((unsigned)ceil_div(rows, TM), (unsigned)ceil_div(N, TN));
-  rows_gemm_kernel<<<grid, kThreads, 0, st>>>(A, rows, K, a_splits, B, N, C,
-                                              alpha, beta, groups, group_rows);
-  return check_launch("rows_gemm_kernel");
+  if (wn == 2)
+    proj_gemm_kernel<2><<<grid, 256, pj_smem<2>(), st>>>(A, rows, lda, K, B, N, C, alpha,
+                                                        beta, groups, group_rows);
+  else
+    proj_gemm_kernel<1><<<grid, 128, pj_smem<1>(), st>>>(A, rows, lda, K, B, N, C, alpha,
+                                                        beta, groups, group_rows);
+  return check_launch("proj_gemm_kernel");
 }
 
 extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,

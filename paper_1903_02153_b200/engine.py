@@ -114,6 +114,8 @@ class FmmEvaluator:
         # field.  Measured on C2 (B200): 4.95 -> 4.90 ms only -- the DMMA M2L
         # and the DFMA P2P contend for the same SMs -- so it is opt-in.
         self.overlap_near = False
+        # coarse far-field levels on a side stream (see _far_field)
+        self.stream_levels = True
         self._side = None
         self.kernel_ms = {}
         self._kpending = []
@@ -299,80 +301,101 @@ class FmmEvaluator:
         return out
 
     def _far_field(self, moments, m, shard, active=None):
+        """Locals of every level 2..L (engine.py:228-292).  The levels are
+        independent; with stream_levels the coarse ones (2..L-2, small and
+        latency-bound) run on a side stream under the two finest."""
         torch = _torch()
-        L, p = self.plan.levels, self.plan.order
+        L = self.plan.levels
+        active = active or {}
+        locs = {}
+        coarse = list(range(2, L - 1)) if (self.stream_levels and shard is None) else []
+        if coarse:
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                for lev in coarse:
+                    locs[lev] = self._far_level(lev, moments, m, shard, active)
+        for lev in range(2, L + 1):
+            if lev not in locs:
+                locs[lev] = self._far_level(lev, moments, m, shard, active)
+        if coarse:
+            main.wait_stream(side)
+            for lev in coarse:
+                locs[lev].record_stream(main)
+        return locs
+
+    def _far_level(self, lev, moments, m, shard, active):
+        torch = _torch()
+        p = self.plan.order
         p3 = p ** 3
         st = self._stream()
-        locs = {}
-        active = active or {}
-        for lev in range(2, L + 1):
-            blk = self._dev_block(lev)
-            scale = float(self.table.scale_for_level(lev))
-            ncell = 1 << (3 * lev)
-            lo, hi = self._cells(lev, shard)
-            nloc = hi - lo
-            out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
-            if blk["kind"] == "cheb" and lev in active:
-                # only the children of active parents: compact lt rows
-                qlist, nact = active[lev]
-                rp = blk["rp"]
-                ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, max(nact, 1)))
-                z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
-                lt = torch.empty((max(nact, 1) * 8 * m * ns * rp,), dtype=torch.float64,
-                                 device=self.device)
-                out.zero_()
-                _native.check(self.lib.bfmm_rows_gemm(
-                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
-                    z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
-                if shard is not None and not shard[0].full:
-                    shard[1].allgather_cells(z, m * rp, lev)
-                e0 = self._kevent()
-                _native.check(self.lib.bfmm_m2l_cheb_list(z.data_ptr(), lt.data_ptr(), lev, m, rp,
-                                                          ns, qlist.data_ptr(), nact,
-                                                          blk["cores"].data_ptr(), st),
-                              "bfmm_m2l_cheb_list")
-                self._kspan(f"m2l_l{lev}", e0)
-                if nact:
-                    _native.check(self.lib.bfmm_rows_gemm_scatter(
-                        lt.data_ptr(), nact * 8 * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
-                        scale, 0.0, ns, qlist.data_ptr(), 8 * m, st), "bfmm_rows_gemm_scatter(U)")
-            elif blk["kind"] == "cheb":
-                rp = blk["rp"]
-                ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nloc // 8))
-                z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
-                lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
-                _native.check(self.lib.bfmm_rows_gemm(
-                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
-                    z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
-                if shard is not None and not shard[0].full:
-                    shard[1].allgather_cells(z, m * rp, lev)  # sources from every shard
-                e0 = self._kevent()
-                _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
-                                                     lo // 8, nloc // 8, blk["cores"].data_ptr(),
-                                                     st), "bfmm_m2l_cheb")
-                self._kspan(f"m2l_l{lev}", e0)
-                _native.check(self.lib.bfmm_rows_gemm(
-                    lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
-                    out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
-            else:
-                if shard is not None and not shard[0].full:
-                    shard[1].allgather_cells(moments[lev], m * p3, lev)
-                # spectra of a chunk of columns at a time (<= 16 GiB of scratch)
-                nb = _native.C.c_size_t(0)
-                _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, 1, p, _native.C.byref(nb)),
-                              "bfmm_m2l_fft_scratch_bytes")
-                cc = max(1, min(m, (16 << 30) // max(int(nb.value), 1)))
-                _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, cc, p, _native.C.byref(nb)),
-                              "bfmm_m2l_fft_scratch_bytes")
-                scratch = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=self.device)
-                e0 = self._kevent()
-                _native.check(self.lib.bfmm_m2l_fft(moments[lev].data_ptr(), out.data_ptr(), lev, m,
-                                                    p, blk["symbols"].data_ptr(), scale, lo // 8,
-                                                    nloc // 8, scratch.data_ptr(), int(nb.value),
-                                                    st), "bfmm_m2l_fft")
-                self._kspan(f"m2lfft_l{lev}", e0)
-            locs[lev] = out
-        return locs
+        blk = self._dev_block(lev)
+        scale = float(self.table.scale_for_level(lev))
+        ncell = 1 << (3 * lev)
+        lo, hi = self._cells(lev, shard)
+        nloc = hi - lo
+        out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
+        if blk["kind"] == "cheb" and lev in active:
+            # only the children of active parents: compact lt rows
+            qlist, nact = active[lev]
+            rp = blk["rp"]
+            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, max(nact, 1)))
+            z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
+            lt = torch.empty((max(nact, 1) * 8 * m * ns * rp,), dtype=torch.float64,
+                             device=self.device)
+            out.zero_()
+            _native.check(self.lib.bfmm_rows_gemm(
+                moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+            if shard is not None and not shard[0].full:
+                shard[1].allgather_cells(z, m * rp, lev)
+            e0 = self._kevent()
+            _native.check(self.lib.bfmm_m2l_cheb_list(z.data_ptr(), lt.data_ptr(), lev, m, rp,
+                                                      ns, qlist.data_ptr(), nact,
+                                                      blk["cores"].data_ptr(), st),
+                          "bfmm_m2l_cheb_list")
+            self._kspan(f"m2l_l{lev}", e0)
+            if nact:
+                _native.check(self.lib.bfmm_rows_gemm_scatter(
+                    lt.data_ptr(), nact * 8 * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
+                    scale, 0.0, ns, qlist.data_ptr(), 8 * m, st), "bfmm_rows_gemm_scatter(U)")
+        elif blk["kind"] == "cheb":
+            rp = blk["rp"]
+            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nloc // 8))
+            z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
+            lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
+            _native.check(self.lib.bfmm_rows_gemm(
+                moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+            if shard is not None and not shard[0].full:
+                shard[1].allgather_cells(z, m * rp, lev)  # sources from every shard
+            e0 = self._kevent()
+            _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
+                                                 lo // 8, nloc // 8, blk["cores"].data_ptr(),
+                                                 st), "bfmm_m2l_cheb")
+            self._kspan(f"m2l_l{lev}", e0)
+            _native.check(self.lib.bfmm_rows_gemm(
+                lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
+                out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
+        else:
+            if shard is not None and not shard[0].full:
+                shard[1].allgather_cells(moments[lev], m * p3, lev)
+            # spectra of a chunk of columns at a time (<= 16 GiB of scratch)
+            nb = _native.C.c_size_t(0)
+            _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, 1, p, _native.C.byref(nb)),
+                          "bfmm_m2l_fft_scratch_bytes")
+            cc = max(1, min(m, (16 << 30) // max(int(nb.value), 1)))
+            _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, cc, p, _native.C.byref(nb)),
+                          "bfmm_m2l_fft_scratch_bytes")
+            scratch = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=self.device)
+            e0 = self._kevent()
+            _native.check(self.lib.bfmm_m2l_fft(moments[lev].data_ptr(), out.data_ptr(), lev, m,
+                                                p, blk["symbols"].data_ptr(), scale, lo // 8,
+                                                nloc // 8, scratch.data_ptr(), int(nb.value),
+                                                st), "bfmm_m2l_fft")
+            self._kspan(f"m2lfft_l{lev}", e0)
+        return out
 
     def _downward(self, locs, tree, m, leaf_geom, status, phi_far, shard):
         L, p = self.plan.levels, self.plan.order
