@@ -316,7 +316,7 @@ extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
   if (p >= 2 && p <= 8) {
-    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, ip, g,
+    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, ip, g,
                nullptr, moments, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, true, a);
   }
@@ -349,7 +349,7 @@ extern "C" int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
   if (p >= 2 && p <= 8) {
-    LeafCall a{pts4, nullptr, m, leaves, starts, counts, n_leaves, max_leaves, ip, g,
+    LeafCall a{pts4, nullptr, m, leaves, starts, counts, n_leaves, max_leaves, levels, ip, g,
                locals, phi_sorted, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, false, a);
   }

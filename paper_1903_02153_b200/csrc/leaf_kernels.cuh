@@ -10,9 +10,13 @@
 // sit in shared memory and every lane contracts them with its weights.
 #pragma once
 
+// 1-D weights from the basis staged in shared memory (sS = S[n][j] for
+// Chebyshev, sN = nodes for uniform): keeping the P^2 coefficients out of
+// registers is what lets these kernels run at full occupancy.
 template <int P>
-__device__ __forceinline__ void weights_p(const Interp &ip, double x, double *w) {
-  if (ip.scheme == 0) {
+__device__ __forceinline__ void weights_s(const double *sS, const double *sN, int scheme,
+                                          double x, double *w) {
+  if (scheme == 0) {
     x = fmin(1.0, fmax(-1.0, x));
     double T[P];
     T[0] = 1.0;
@@ -23,19 +27,57 @@ __device__ __forceinline__ void weights_p(const Interp &ip, double x, double *w)
     for (int j = 0; j < P; ++j) {
       double s = 0.0;
 #pragma unroll
-      for (int n = 0; n < P; ++n) s = fma(T[n], ip.S[n * P + j], s);
+      for (int n = 0; n < P; ++n) s = fma(T[n], sS[n * P + j], s);
       w[j] = s;
     }
   } else {
+    // Lagrange products in the reference's factor order, with the inverse
+    // node differences staged in sS (one rounding per factor off the
+    // reference's division, far inside the 1e-10 parity bar)
 #pragma unroll
     for (int j = 0; j < P; ++j) {
       double v = 1.0;
 #pragma unroll
       for (int k = 0; k < P; ++k)
-        if (k != j) v *= (x - ip.nodes[k]) / (ip.nodes[j] - ip.nodes[k]);
+        if (k != j) v *= (x - sN[k]) * sS[j * P + k];
       w[j] = v;
     }
   }
+}
+
+template <int P>
+__device__ __forceinline__ void stage_basis(const Interp &ip, double *sS, double *sN) {
+  // static indices into the parameter block (a dynamic index would make the
+  // compiler materialise the whole Interp struct)
+  if (threadIdx.x < P) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      if (threadIdx.x == k) sN[k] = ip.nodes[k];
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+        if (threadIdx.x == j)
+          sS[j * P + k] = ip.scheme == 0 ? ip.S[j * P + k]
+                                         : (j != k ? 1.0 / (ip.nodes[j] - ip.nodes[k]) : 0.0);
+    }
+  }
+  __syncthreads();
+}
+
+// Leaf-frame coordinate like ref_coord, scaled by the precomputed 1 / hw.
+__device__ __forceinline__ double ref_coord_m(double x, double lo, double h, double inv_hw,
+                                             int cell, int32_t *flag) {
+  const double center = lo + ((double)cell + 0.5) * h;
+  const double r = (x - center) * inv_hw;
+  if (fabs(r) > 1.0 + 1e-9) atomicOr(flag, 1);
+  return fmin(1.0, fmax(-1.0, r));
+}
+
+// The leaf cell of a coordinate, computed exactly like the tree build
+// (tree.cu leaf_keys_kernel): IEEE subtraction and division, floor, clip.
+__device__ __forceinline__ int leaf_coord(double x, double lo, double h, int nmax) {
+  const double f = floor(__ddiv_rn(__dsub_rn(x, lo), h));
+  const int64_t v = (int64_t)f;
+  return (int)(v < 0 ? 0 : (v > nmax ? nmax : v));
 }
 
 template <int P>
@@ -49,6 +91,8 @@ p2m_leaf_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
   constexpr int NP = (P * P + 31) / 32;  // (i, j) pairs per lane
   __shared__ double s_w[kLeafWarps][32][3 * P];
   __shared__ double s_v[kLeafWarps][32];
+  __shared__ double sS[P * P], sN[P];
+  stage_basis<P>(ip, sS, sN);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t nl = *n_leaves;
   for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
@@ -70,9 +114,12 @@ p2m_leaf_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
         if (lane < nb) {
           const int64_t i = s0 + c0 + lane;
           const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
-          weights_p<P>(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), &s_w[wid][lane][0]);
-          weights_p<P>(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), &s_w[wid][lane][P]);
-          weights_p<P>(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), &s_w[wid][lane][2 * P]);
+          weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, 1.0 / g.hw, cx, flag),
+                       &s_w[wid][lane][0]);
+          weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.y, g.lo[1], g.h, 1.0 / g.hw, cy, flag),
+                       &s_w[wid][lane][P]);
+          weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, 1.0 / g.hw, cz, flag),
+                       &s_w[wid][lane][2 * P]);
           s_v[wid][lane] = ws[i * m + c];
         }
         __syncwarp();
@@ -103,21 +150,32 @@ p2m_leaf_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
   }
 }
 
+// L2P (engine.py:313-347), one warp per leaf: the leaf's locals (one column
+// at a time) are brought into the warp's shared slice with coalesced loads;
+// each lane evaluates its point's weights, parks the P^2 products wx wy in
+// its own shared column, and contracts the locals pair by pair (broadcast
+// reads of L, z weights in registers), which keeps the kernel at ~40
+// registers and full occupancy.
 template <int P>
-__global__ void __launch_bounds__(32 * kLeafWarps)
-l2p_leaf_kernel(const double *__restrict__ pts4, int m,
-                const int64_t *__restrict__ leaves,
-                const int64_t *__restrict__ starts,
-                const int64_t *__restrict__ counts,
-                const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
-                const double *__restrict__ locals, double *__restrict__ phi,
-                int32_t *flag) {
-  constexpr int P3 = P * P * P;
-  __shared__ double s_L[kLeafWarps][P3];
+constexpr int l2p_warps() { return P <= 6 ? kLeafWarps : 1; }  // static smem < 48 KB
+
+template <int P>
+__global__ void __launch_bounds__(32 * l2p_warps<P>())
+l2p_warp_kernel(const double *__restrict__ pts4, int m,
+                const int64_t *__restrict__ leaves, const int64_t *__restrict__ starts,
+                const int64_t *__restrict__ counts, const int64_t *__restrict__ n_leaves,
+                Interp ip, LeafGeom g, const double *__restrict__ locals,
+                double *__restrict__ phi, int32_t *flag) {
+  constexpr int P2 = P * P, P3 = P2 * P, W = l2p_warps<P>();
+  __shared__ double sL[W][P3];
+  __shared__ double sWxy[W][P2][32];
+  __shared__ double sS[P * P], sN[P];
+  stage_basis<P>(ip, sS, sN);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double inv_hw = 1.0 / g.hw;
   const int64_t nl = *n_leaves;
-  for (int64_t leaf = int64_t(blockIdx.x) * kLeafWarps + wid; leaf < nl;
-       leaf += int64_t(gridDim.x) * kLeafWarps) {
+  for (int64_t leaf = int64_t(blockIdx.x) * W + wid; leaf < nl;
+       leaf += int64_t(gridDim.x) * W) {
     const int64_t cell = leaves[leaf];
     if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
     const int64_t s0 = starts[leaf], cnt = counts[leaf];
@@ -125,33 +183,35 @@ l2p_leaf_kernel(const double *__restrict__ pts4, int m,
     unmorton3((uint64_t)cell, cx, cy, cz);
     for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
       const bool have = c0 + lane < cnt;
-      const int64_t i = s0 + c0 + lane;
-      double wx[P], wy[P], wz[P];
-      if (have) {
-        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
-        weights_p<P>(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), wx);
-        weights_p<P>(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), wy);
-        weights_p<P>(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), wz);
+      const int64_t i = s0 + c0 + (have ? lane : 0);
+      double wz[P];
+      const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+      {
+        double wx[P], wy[P];
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, inv_hw, cx, flag), wx);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.y, g.lo[1], g.h, inv_hw, cy, flag), wy);
+        __syncwarp();
+#pragma unroll
+        for (int a = 0; a < P; ++a)
+#pragma unroll
+          for (int b = 0; b < P; ++b) sWxy[wid][a * P + b][lane] = wx[a] * wy[b];
       }
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
       for (int c = 0; c < m; ++c) {
         __syncwarp();
         const double *src = locals + (cell * m + c) * (int64_t)P3;
-        for (int a = lane; a < P3; a += 32) s_L[wid][a] = src[a];
+        for (int e = lane; e < P3; e += 32) sL[wid][e] = src[e];
         __syncwarp();
-        if (have) {
-          const double *L = s_L[wid];
-          double s = 0.0;
+        const double *L = sL[wid];
+        double s = 0.0;
+#pragma unroll 1
+        for (int ab = 0; ab < P2; ++ab) {
+          double sb = 0.0;
 #pragma unroll
-          for (int ii = 0; ii < P; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-              const double wxy = wx[ii] * wy[jj];
-#pragma unroll
-              for (int kk = 0; kk < P; ++kk)
-                s = fma(wxy * wz[kk], L[(ii * P + jj) * P + kk], s);
-            }
-          phi[i * m + c] = s;
+          for (int k = 0; k < P; ++k) sb = fma(wz[k], L[ab * P + k], sb);
+          s = fma(sWxy[wid][ab][lane], sb, s);
         }
+        if (have) phi[i * m + c] = s;
       }
     }
   }
@@ -162,6 +222,7 @@ struct LeafCall {
   int m;
   const int64_t *leaves, *starts, *counts, *n_leaves;
   int64_t max_leaves;
+  int levels;
   Interp ip;
   LeafGeom g;
   const double *locals;
@@ -179,10 +240,11 @@ int launch_leaf(bool p2m, const LeafCall &a) {
         a.flag);
     return check_launch("p2m_leaf_kernel");
   }
-  l2p_leaf_kernel<P><<<grid, 32 * kLeafWarps, 0, a.st>>>(
+  l2p_warp_kernel<P><<<(unsigned)grid_cap(ceil_div(a.max_leaves, l2p_warps<P>()), 16),
+                       32 * l2p_warps<P>(), 0, a.st>>>(
       a.pts4, a.m, a.leaves, a.starts, a.counts, a.n_leaves, a.ip, a.g, a.locals, a.out,
       a.flag);
-  return check_launch("l2p_leaf_kernel");
+  return check_launch("l2p_warp_kernel");
 }
 
 inline int dispatch_leaf(int p, bool p2m, const LeafCall &a) {
