@@ -201,8 +201,10 @@ int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
 /* Symmetric near field for shared targets = sources and a kernel with
  * K(y, x) = sign K(x, y) (the reference's transpose replay,
  * engine.py:361-364, 442-457): each unordered neighbour-leaf pair is
- * evaluated once and both sides are accumulated into per-neighbour slots
- * that are summed in neighbour order (deterministic, no atomics).  Writes
+ * evaluated once; a leaf's own points accumulate their row sums over its 14
+ * half-neighbours in registers (slot 0), the partner leaf's points receive
+ * the column sums in slot h of the half-neighbour offset, and the 14 slots
+ * are added in a fixed order (deterministic, no atomics).  Writes
  * out (nt rows, m = 1) for every point touched; when a leaf holds more than
  * 64 points the library falls back to bfmm_p2p on the device (no host
  * synchronisation).  Leaves outside [cell_lo, cell_hi) start no pairs; the

@@ -101,6 +101,10 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
 // ---- 2. Hadamard accumulation as a per-frequency 3-D stencil ------------------
 constexpr int kTX = 8, kTY = 8, kTZ = 16, kR = kTZ / 2;  // 128 threads x 8 targets
 constexpr int kHX = kTX + 6, kHY = kTY + 6, kHZ = kTZ + 6;
+// z stride padded to 23 (= 7 mod 8 16-byte slots, x stride 14*23 = 2 mod 8):
+// the 8 x 4 (ix, iy) lanes of a warp reading one double2 each then cover all
+// eight 16-byte bank slots evenly, 4 wavefronts per LDS.128 (unpadded: 8)
+constexpr int kHZP = kHZ + 1;
 
 // grid: (tiles, frequencies, columns); block (8, 8, 2): thread (ix, iy, pz)
 // owns targets (x0+ix, y0+iy, z0+pz+2k), k < 8 -- one parity class, so one
@@ -111,8 +115,8 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
                int F, const double2 *__restrict__ S, const short *__restrict__ tap_index,
                int64_t cell_lo, int64_t cell_hi) {
   extern __shared__ double2 sm2[];
-  auto halo = reinterpret_cast<double2 (*)[kHY][kHZ]>(sm2);                     // [kHX][kHY][kHZ]
-  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kHX * kHY * kHZ);      // [7][7][7]
+  auto halo = reinterpret_cast<double2 (*)[kHY][kHZP]>(sm2);                    // [kHX][kHY][kHZP]
+  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kHX * kHY * kHZP);     // [7][7][7]
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
   const int tilesx = (n + kTX - 1) / kTX, tilesy = (n + kTY - 1) / kTY;
@@ -313,7 +317,7 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const size_t smem_i = sizeof(double2) * (g.p * g.q * g.h + g.p * g.p * g.h);
   const int n = 1 << level;
   const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
-  const size_t smem_s = sizeof(double2) * (kHX * kHY * kHZ + 343);
+  const size_t smem_s = sizeof(double2) * (kHX * kHY * kHZP + 343);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

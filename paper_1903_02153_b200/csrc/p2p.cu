@@ -636,7 +636,7 @@ extern "C" int bfmm_scatter_output(const double *far_sorted,
 extern "C" size_t bfmm_p2p_symmetric_scratch_bytes(int64_t nt, int64_t max_tleaves) {
   size_t off;
   const size_t chunk = (p2p_scratch(max_tleaves < 1 ? 1 : max_tleaves, &off) + 255) & ~size_t(255);
-  return chunk + ((27 * (size_t)(nt < 1 ? 1 : nt) * sizeof(double) + 255) & ~size_t(255)) + 256;
+  return chunk + ((14 * (size_t)(nt < 1 ? 1 : nt) * sizeof(double) + 255) & ~size_t(255)) + 512;
 }
 
 extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
@@ -651,16 +651,18 @@ extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
   cudaStream_t st = as_stream(stream);
   size_t cub_off;
   const size_t chunk = (p2p_scratch(max_leaves, &cub_off) + 255) & ~size_t(255);
-  const size_t slot_bytes = (27 * (size_t)nt * sizeof(double) + 255) & ~size_t(255);
-  if (scratch_bytes < chunk + slot_bytes + 256) {
+  const size_t slot_bytes = (14 * (size_t)nt * sizeof(double) + 255) & ~size_t(255);
+  if (scratch_bytes < chunk + slot_bytes + 512) {
     set_error("bfmm_p2p_symmetric: scratch too small");
     return 2;
   }
   char *base = static_cast<char *>(scratch);
   double *slots = reinterpret_cast<double *>(base + chunk);
   int *flag = reinterpret_cast<int *>(base + chunk + slot_bytes);
+  auto *ctr = reinterpret_cast<unsigned long long *>(base + chunk + slot_bytes + 256);
   if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess ||
-      cudaMemsetAsync(slots, 0, 27 * (size_t)nt * sizeof(double), st) != cudaSuccess) {
+      cudaMemsetAsync(ctr, 0, sizeof(*ctr), st) != cudaSuccess ||
+      cudaMemsetAsync(slots, 0, 14 * (size_t)nt * sizeof(double), st) != cudaSuccess) {
     set_error("bfmm_p2p_symmetric: memset failed");
     return 1;
   }
@@ -683,8 +685,10 @@ extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
   add_launches(2);
   bfmm_nf::Args a = make_args(pts4, leaves, starts, counts, n_leaves, pts4, nullptr, 1,
                               cell_start, cell_count, levels, out, incl);
+  a.work_ctr = ctr;
   int rc = launch_sym(handle, a, slots, nt, sign, flag, cell_lo, cell_hi, st);
   if (rc) return rc;
+  a.work_ctr = nullptr;
   a.gate = flag;
   rc = launch_p2p(handle, 0, dim3(kNumSMs * 16), a, 0, st);
   if (rc) return rc;
