@@ -180,6 +180,18 @@ def fp64_peaks(lib, stream):
     return g1.value / 1e3, g2.value / 1e3  # TFLOP/s
 
 
+def committed_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/r01_traffic.json), or None when that kernel was not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(config, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+    return None if rec is None else rec["bytes"]
+
+
 def m2l_flops(ev, wl):
     """Algorithmic M2L flops per level: pairs P_l * 2 r_l^2 * m."""
     from paper_1903_02153_b200.tables import OFFSETS
@@ -329,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
             roof = {"kernel": f"m2l level {lev} (DMMA implicit GEMM)", "bound": "fp64-tensor"}
         achieved = flops / (ms * 1e-3) / 1e12
         roof.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": committed_traffic(args.config, dom),
                      "peak_source": "measured live: DFMA / DMMA microbenchmarks (libbfmm.so); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                      "kernel_ms": ms, "share_of_step": ms / (total_ms / args.steps)})
