@@ -18,10 +18,15 @@ namespace {
 
 // ---- built-in kernels (kernel.py:149-180): profile f(r) with r = |x - y| ----
 // 1/r, r = 0 -> 0
+// eval_fast: the hot-loop body; bodies with exp use the flagged fast exp
+// (bfmm_exp_fast), the others are eval itself.
 struct KLaplace {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : rsqrt(r2);
+  }
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &) {
+    return eval(dx, dy, dz);
   }
 };
 // 1/r^4, r = 0 -> 0
@@ -30,11 +35,17 @@ struct KLaplaceForce {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : 1.0 / (r2 * r2);
   }
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &) {
+    return eval(dx, dy, dz);
+  }
 };
 // exp(-r^2)
 struct KGaussian {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     return bfmm_nf::bfmm_exp(-(dx * dx + dy * dy + dz * dz));
+  }
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+    return bfmm_nf::bfmm_exp_fast(-(dx * dx + dy * dy + dz * dz), bad);
   }
 };
 // exp(-r)
@@ -42,12 +53,18 @@ struct KExponential {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     return bfmm_nf::bfmm_exp(-sqrt(dx * dx + dy * dy + dz * dz));
   }
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+    return bfmm_nf::bfmm_exp_fast(-sqrt(dx * dx + dy * dy + dz * dz), bad);
+  }
 };
 // log r, r = 0 -> 0
 struct KLogarithm {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : 0.5 * log(r2);
+  }
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &) {
+    return eval(dx, dy, dz);
   }
 };
 
@@ -107,10 +124,13 @@ std::string functor_source(int kind, const char *expr) {
            std::string(expr) + ");";
   else
     body = "return (" + std::string(expr) + ");";
-  // exp() in user expressions maps to the branch-free bfmm_exp (p2p.cuh)
+  // exp() in user expressions maps to the branch-free bfmm_exp (p2p.cuh);
+  // eval_fast uses the flagged fast path (bfmm_exp_fast)
   return "#define exp(x) bfmm_exp(x)\nstruct KUser {\n __device__ __forceinline__ "
          "static double eval(double dx, double dy, double dz) {\n " +
-         body + "\n }\n};\n#undef exp\n";
+         body + "\n }\n#undef exp\n#define exp(x) bfmm_exp_fast(x, bfmm_bad_)\n"
+         " __device__ __forceinline__ static double eval_fast(double dx, double dy, "
+         "double dz, bool &bfmm_bad_) {\n " + body + "\n }\n#undef exp\n};\n";
 }
 
 int jit_compile(int kind, const char *expr, int *handle) {

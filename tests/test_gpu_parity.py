@@ -289,6 +289,40 @@ def test_nonfinite_kernel_value_reports_indices(cache_dir):
     assert err.value.indices == (0, 37)
 
 
+@pytest.mark.parametrize("expr,edge", [("exp(-(r2 * 4.0e4))", "underflow"),
+                                       ("exp(1.0 / r2)", "inf")])
+def test_exp_out_of_range_arguments(expr, edge, cache_dir):
+    """exp() arguments beyond the fast path (|x| >= 708, inf, NaN) take the
+    exact path for their tile: tiny terms flush to 0 like NumPy's exp; an
+    infinite exponent still reports the offending pair."""
+    import numpy as _np
+    if edge == "underflow":
+        k = bf.KernelSpec(name="sharp", profile=lambda r: _np.exp(-(r * r) * 4.0e4),
+                          homogen=0.0, symmetry=1, cuda_expr=expr, cuda_arg="r2")
+        pts, w = unit_cloud(6000, seed=23)
+        w = w[:, 0]
+        plan = small_plan(levels=3, order=4)
+        ev = bf.FmmEvaluator(k, plan, cache_dir=cache_dir)
+        ev._disable_far_field = True
+        got = ev.evaluate(pts, weights=w)
+        # brute-force near field: sources in the 27 neighbour leaves (L = 3)
+        cell = _np.clip(_np.floor(pts * 8.0).astype(_np.int64), 0, 7)
+        ref = _np.zeros(len(pts))
+        for i0 in range(0, len(pts), 500):
+            d2 = ((pts[i0:i0 + 500, None, :] - pts[None, :, :]) ** 2).sum(-1)
+            near = (_np.abs(cell[i0:i0 + 500, None, :] - cell[None, :, :]) <= 1).all(-1)
+            ref[i0:i0 + 500] = (_np.where(near, _np.exp(-d2 * 4.0e4), 0.0) * w[None, :]).sum(1)
+        assert rel_l2(got, ref) < 1e-12
+    else:
+        # finite on the far-field node grids, +inf at the self pairs (r = 0)
+        k = bf.KernelSpec(name="blowup", profile=lambda r: _np.exp(1.0 / (r * r)),
+                          homogen=0.0, symmetry=1, cuda_expr=expr, cuda_arg="r2")
+        pts, w = unit_cloud(200, seed=24)
+        ev = bf.FmmEvaluator(k, small_plan(levels=2, order=2), cache_dir=cache_dir)
+        with pytest.raises(bf.KernelEvaluationError):
+            ev.evaluate(pts, weights=w)
+
+
 def test_rejects_bad_inputs(cache_dir):
     pts, w = unit_cloud(100, seed=0)
     ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
