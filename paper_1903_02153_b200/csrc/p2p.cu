@@ -21,12 +21,18 @@ namespace {
 // eval_fast: the hot-loop body; bodies with exp use the flagged fast exp
 // (bfmm_exp_fast), the others are eval itself.
 struct KLaplace {
+  // cheap body: keep 6 CTAs/SM (<= 80 registers) for latency-bound sparse leaves
+  static constexpr int kMinBlocks = 6;
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : rsqrt(r2);
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &) {
-    return eval(dx, dy, dz);
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    bool b = false;
+    const double v = bfmm_nf::bfmm_rsqrt_fast(r2, b);
+    bad |= b && r2 != 0.0;
+    return r2 == 0.0 ? 0.0 : v;
   }
 };
 // 1/r^4, r = 0 -> 0
@@ -35,8 +41,12 @@ struct KLaplaceForce {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : 1.0 / (r2 * r2);
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &) {
-    return eval(dx, dy, dz);
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    bool b = false;
+    const double v = bfmm_nf::bfmm_rcp_fast(r2 * r2, b);
+    bad |= b && r2 != 0.0;
+    return r2 == 0.0 ? 0.0 : v;
   }
 };
 // exp(-r^2)
