@@ -290,7 +290,62 @@ def case_eig():
          vec0=res.eigenvectors[:, 0])
 
 
+def case_cli():
+    """The reference CLI (cli.py) and file formats (io.py) on small inputs."""
+    import contextlib
+    import io as pyio
+    import tempfile
+    from boxfmm import io as rio
+    from boxfmm.cli import main as rmain
+    out = {}
+    gen = np.random.default_rng(44)
+    pts = gen.random((3000, 3))
+    w = gen.standard_normal((3000, 2))
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "src.csv")
+        rio.write_points_file(src, pts, w)
+        out["src_csv_sha"] = np.array(hashlib.sha256(open(src, "rb").read()).hexdigest())
+        rio.write_matrix_binary(os.path.join(d, "w.bin"), w)
+        out["w_bin_sha"] = np.array(
+            hashlib.sha256(open(os.path.join(d, "w.bin"), "rb").read()).hexdigest())
+        phi = os.path.join(d, "phi.bin")
+        buf = pyio.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = rmain(["evaluate", "--kernel", "exponential", "--sources", src, "--levels", "3",
+                        "--order", "4", "--eps", "1e-6", "--cache-dir", CACHE, "--out", phi])
+        assert rc == 0
+        out["eval_phi"] = rio.read_matrix(phi)
+        out["eval_stdout"] = np.array(buf.getvalue())
+        syn = os.path.join(d, "syn.bin")
+        with contextlib.redirect_stdout(pyio.StringIO()):
+            rc = rmain(["evaluate", "--kernel", "gaussian", "--synthetic", "2000", "--seed", "9",
+                        "--order", "3", "--levels", "2", "--cache-dir", CACHE, "--out", syn])
+        assert rc == 0
+        out["syn_phi"] = rio.read_matrix(syn)
+        rows = os.path.join(d, "conv.csv")
+        with contextlib.redirect_stdout(pyio.StringIO()):
+            rc = rmain(["bench", "--mode", "convergence", "--kernel", "laplacian", "--n", "400",
+                        "--orders", "2,4", "--eps", "1e-8", "--cache-dir", CACHE, "--out", rows])
+        assert rc == 0
+        import csv
+        with open(rows) as fh:
+            recs = list(csv.DictReader(fh))
+        out["conv_scheme"] = np.array([r["scheme"] for r in recs])
+        out["conv_order"] = np.array([int(r["order"]) for r in recs])
+        out["conv_error"] = np.array([float(r["error"]) for r in recs])
+        eigs = os.path.join(d, "eigs.bin")
+        with contextlib.redirect_stdout(pyio.StringIO()):
+            rc = rmain(["bench", "--mode", "randsvd", "--kernel", "gaussian", "--n", "300",
+                        "--rank", "10", "--oversample", "5", "--power-iters", "2", "--levels",
+                        "2", "--cache-dir", CACHE, "--eigs-out", eigs,
+                        "--out", os.path.join(d, "r.csv")])
+        assert rc == 0
+        out["randsvd_eigs"] = rio.read_matrix(eigs)
+    save("cli", **out)  # inputs: default_rng(44): random((3000, 3)), standard_normal((3000, 2))
+
+
 CASES = {
+    "cli": case_cli,
     "eig": case_eig,
     "tree": case_tree,
     "lists": case_lists,
