@@ -12,14 +12,15 @@
 // Spectra are stored frequency-major with cells in lexicographic (x, y, z)
 // order: for one frequency the Hadamard accumulation is a 3-D stencil with
 // 189 complex taps over the cell grid, which stencil_kernel
-// tiles through shared memory (an 8 x 8 x 16 target tile plus its 3-cell
-// halo) and blocks in registers along z (each thread owns 8 same-parity
-// targets, so one z-column of 21 sources serves 7 taps x 8 targets).
+// tiles through shared memory (an 8 x 8 x 8 target tile plus its 3-cell
+// halo) and blocks in registers along z (each thread owns 4 same-parity
+// targets, so one z-column of 13 sources serves 7 taps x 4 targets).
 // The transforms are direct DFTs along each axis with exactly tabulated
 // twiddles: zero padding makes them cheaper than a generic FFT.
 #include <algorithm>
 
 #include "common.cuh"
+
 
 namespace bfmm {
 namespace {
@@ -99,15 +100,18 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
 }
 
 // ---- 2. Hadamard accumulation as a per-frequency 3-D stencil ------------------
-constexpr int kTX = 8, kTY = 8, kTZ = 16, kR = kTZ / 2;  // 128 threads x 8 targets
+// 8 x 8 x 8 targets, 128 threads x 4: a 47 KB halo keeps 4 CTAs per SM
+// (measured: 16-deep z tiles reuse each source more but fit only 3 CTAs and
+// run 3 % slower, the kernel being shared-memory-latency bound)
+constexpr int kTX = 8, kTY = 8, kTZ = 8, kR = kTZ / 2;
 constexpr int kHX = kTX + 6, kHY = kTY + 6, kHZ = kTZ + 6;
-// z stride padded to 23 (= 7 mod 8 16-byte slots, x stride 14*23 = 2 mod 8):
-// the 8 x 4 (ix, iy) lanes of a warp reading one double2 each then cover all
-// eight 16-byte bank slots evenly, 4 wavefronts per LDS.128 (unpadded: 8)
+// z stride padded to 15 (= 7 mod 8 16-byte slots; with the lane layout
+// below the x step 2*14*15 = 4 and y step 2*15 = 6 mod 8): a warp's LDS.128
+// covers the eight 16-byte bank slots evenly, 4 wavefronts (unpadded: 8)
 constexpr int kHZP = kHZ + 1;
 
 // grid: (tiles, frequencies, columns); block (8, 8, 2): thread (ix, iy, pz)
-// owns targets (x0+ix, y0+iy, z0+pz+2k), k < 8 -- one parity class, so one
+// owns targets (x0+ix, y0+iy, z0+pz+2k), k < kR -- one parity class, so one
 // valid-offset set (octree.py:128-145).  The symbol of every offset t sits in
 // a 7^3 table (zero for the 27 near offsets).
 __global__ void __launch_bounds__(128)
@@ -124,8 +128,14 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
   const int tz = tile / (tilesx * tilesy), trem = tile - tz * tilesx * tilesy;
   const int x0 = (trem / tilesy) * kTX, y0 = (trem % tilesy) * kTY, z0 = tz * kTZ;
   const int f = blockIdx.y, col = blockIdx.z;
-  const int ix = threadIdx.x, iy = threadIdx.y, pz = threadIdx.z;
-  const int tid = (pz * kTY + iy) * kTX + ix;
+  // warp w handles the (x, y) parity class (w >> 1, w & 1): its 32 lanes are
+  // 4 x 4 same-parity (x, y) positions x 2 z-parities, so the +-3 offset skips
+  // below are warp-uniform (no divergence), and the lanes' LDS.128 still
+  // cover the 8 bank slots evenly
+  const int tid = (threadIdx.z * kTY + threadIdx.y) * kTX + threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5;
+  const int ix = ((w >> 1) & 1) + 2 * (lane & 3), iy = (w & 1) + 2 * ((lane >> 2) & 3);
+  const int pz = lane >> 4;
   const int x = x0 + ix, y = y0 + iy;
   // shard filter: skip the tile when none of its targets is ours
   bool mine = false;
