@@ -416,7 +416,10 @@ __global__ void near_count_kernel(const int64_t *__restrict__ tleaves,
     }
     local += (unsigned long long)(s * tcounts[i]);
   }
-  atomicAdd(total, local);
+  // one atomic per warp (a same-address atomic per thread serialises)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(total, local);
 }
 
 // Layout: nch[max_leaves] | incl[max_leaves] | CUB temp | chunk counter

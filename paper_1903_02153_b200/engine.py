@@ -500,7 +500,21 @@ class FmmEvaluator:
         ev[0].record()
         src = self._prepare_points(sources, "sources")
         tgt = src if shared else self._prepare_points(targets, "targets")
-        w, squeeze = self._prepare_weights(weights, src.shape[0])
+        w_event = None
+        if (isinstance(weights, torch.Tensor) and weights.device.type == "cpu"
+                and weights.is_pinned() and not sharded):
+            # pinned host weights: copy them on the side stream while the
+            # trees are built (they are first needed by gather_weights)
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                w, squeeze = self._prepare_weights(weights, src.shape[0])
+                w_event = torch.cuda.Event()
+                w_event.record()
+            w.record_stream(main)
+        else:
+            w, squeeze = self._prepare_weights(weights, src.shape[0])
         m = int(w.shape[1])
         n_src, n_tgt = int(src.shape[0]), int(tgt.shape[0])
         status = torch.zeros(16, dtype=torch.int32, device=self.device)
@@ -508,6 +522,8 @@ class FmmEvaluator:
         ev[1].record()
         stree = self._build_tree(src, status, _ST_DOMAIN_SRC)
         ttree = stree if shared else self._build_tree(tgt, status, _ST_DOMAIN_TGT)
+        if w_event is not None:
+            torch.cuda.current_stream().wait_event(w_event)
         ws = torch.empty((max(n_src, 1), m), dtype=torch.float64, device=self.device)
         _native.check(self.lib.bfmm_gather_weights(w.data_ptr(), n_src, m, stree.perm.data_ptr(),
                                                    ws.data_ptr(), stree.pts4.data_ptr(), st),
