@@ -169,6 +169,16 @@ int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
              int scheme, const double *interp, const double *geom,
              const double *locals, double *phi_sorted, int32_t *ref_flag,
              bfmm_stream_t stream);
+/* Same contraction with one thread per sorted point (the point's leaf is
+ * recomputed from its coordinates exactly as bfmm_tree_build bins it): for
+ * sparse leaves of a few points, where a warp per leaf leaves lanes idle.
+ * Bitwise-identical results to bfmm_l2p. */
+int bfmm_l2p_points(const double *pts4, int m, const int64_t *leaves,
+                    const int64_t *starts, const int64_t *counts,
+                    const int64_t *n_leaves, int64_t max_leaves, int levels, int p,
+                    int scheme, const double *interp, const double *geom,
+                    const double *locals, double *phi_sorted, int32_t *ref_flag,
+                    bfmm_stream_t stream);
 
 /* ---- near field (engine.py:349-478) ------------------------------------ */
 

@@ -45,6 +45,7 @@ SIGNATURES = {
     "bfmm_m2l_fft": (_I, [_P, _P, _I, _I, _I, _P, _D, _I64, _I64, _P, _SZ, _P]),
     "bfmm_l2l": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
     "bfmm_l2p": (_I, [_P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P, _P]),
+    "bfmm_l2p_points": (_I, [_P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P, _P]),
     "bfmm_kernel_compile": (_I, [_I, C.c_char_p, C.POINTER(_I)]),
     "bfmm_p2p_scratch_bytes": (_SZ, [_I64, _I64]),
     "bfmm_p2p": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _P, _P, _I, _I64, _I64, _P, _P,

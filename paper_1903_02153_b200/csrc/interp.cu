@@ -316,7 +316,7 @@ extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
   if (p >= 2 && p <= 8) {
-    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, ip, g,
+    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, false, ip, g,
                nullptr, moments, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, true, a);
   }
@@ -334,13 +334,13 @@ extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
   return check_launch("p2m_kernel");
 }
 
-extern "C" int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
-                        const int64_t *starts, const int64_t *counts,
-                        const int64_t *n_leaves, int64_t max_leaves, int levels,
-                        int p, int scheme, const double *interp,
-                        const double *geom, const double *locals,
-                        double *phi_sorted, int32_t *ref_flag,
-                        bfmm_stream_t stream) {
+static int l2p_impl(const double *pts4, int m, const int64_t *leaves,
+                    const int64_t *starts, const int64_t *counts,
+                    const int64_t *n_leaves, int64_t max_leaves, int levels,
+                    int p, int scheme, const double *interp,
+                    const double *geom, const double *locals,
+                    double *phi_sorted, int32_t *ref_flag, bool per_point,
+                    bfmm_stream_t stream) {
   if (p < 1 || p > kMaxP || m < 1) {
     set_error("bfmm_l2p: unsupported p=%d m=%d", p, m);
     return 2;
@@ -349,8 +349,8 @@ extern "C" int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
   if (p >= 2 && p <= 8) {
-    LeafCall a{pts4, nullptr, m, leaves, starts, counts, n_leaves, max_leaves, levels, ip, g,
-               locals, phi_sorted, ref_flag, as_stream(stream)};
+    LeafCall a{pts4, nullptr, m, leaves, starts, counts, n_leaves, max_leaves, levels,
+               per_point, ip, g, locals, phi_sorted, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, false, a);
   }
   size_t smem = sizeof(double) * m * p * p * p;
@@ -412,4 +412,26 @@ extern "C" int bfmm_l2l(const double *parent, double *child, int64_t n_parent,
                as_stream(stream)>>>(parent, child, n_parent, p, m,
                                     make_halves(p, H));
   return check_launch("l2l_kernel");
+}
+
+extern "C" int bfmm_l2p(const double *pts4, int m, const int64_t *leaves,
+                        const int64_t *starts, const int64_t *counts,
+                        const int64_t *n_leaves, int64_t max_leaves, int levels,
+                        int p, int scheme, const double *interp,
+                        const double *geom, const double *locals,
+                        double *phi_sorted, int32_t *ref_flag,
+                        bfmm_stream_t stream) {
+  return l2p_impl(pts4, m, leaves, starts, counts, n_leaves, max_leaves, levels, p, scheme,
+                  interp, geom, locals, phi_sorted, ref_flag, false, stream);
+}
+
+extern "C" int bfmm_l2p_points(const double *pts4, int m, const int64_t *leaves,
+                               const int64_t *starts, const int64_t *counts,
+                               const int64_t *n_leaves, int64_t max_leaves, int levels,
+                               int p, int scheme, const double *interp,
+                               const double *geom, const double *locals,
+                               double *phi_sorted, int32_t *ref_flag,
+                               bfmm_stream_t stream) {
+  return l2p_impl(pts4, m, leaves, starts, counts, n_leaves, max_leaves, levels, p, scheme,
+                  interp, geom, locals, phi_sorted, ref_flag, true, stream);
 }

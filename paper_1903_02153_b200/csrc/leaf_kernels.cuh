@@ -217,12 +217,64 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
   }
 }
 
+// L2P for sparse leaves (a few points each, e.g. C5's 3.8): one thread per
+// sorted point instead of one warp per leaf, so no lanes idle.  The point's
+// leaf is recomputed from its coordinates (bit-identical to the tree build),
+// its weights evaluated once, and the leaf's locals contracted z, y, x
+// straight from global memory (neighbouring threads share a leaf: L1
+// broadcasts).  Same arithmetic as l2p_warp_kernel.
+template <int P>
+__global__ void __launch_bounds__(128)
+l2p_point_kernel(const double *__restrict__ pts4, int m,
+                 const int64_t *__restrict__ starts, const int64_t *__restrict__ counts,
+                 const int64_t *__restrict__ n_leaves, int levels, Interp ip, LeafGeom g,
+                 const double *__restrict__ locals, double *__restrict__ phi,
+                 int32_t *flag) {
+  constexpr int P2 = P * P, P3 = P2 * P;
+  __shared__ double sS[P * P], sN[P];
+  stage_basis<P>(ip, sS, sN);
+  const int64_t nl = *n_leaves;
+  if (nl == 0) return;
+  const int64_t n = starts[nl - 1] + counts[nl - 1];
+  const int nmax = (1 << levels) - 1;
+  const double inv_hw = 1.0 / g.hw;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+    const int cx = leaf_coord(q.x, g.lo[0], g.h, nmax), cy = leaf_coord(q.y, g.lo[1], g.h, nmax),
+              cz = leaf_coord(q.z, g.lo[2], g.h, nmax);
+    const int64_t cell = (int64_t)morton3(cx, cy, cz);
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
+    double wx[P], wy[P], wz[P];
+    weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, inv_hw, cx, flag), wx);
+    weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.y, g.lo[1], g.h, inv_hw, cy, flag), wy);
+    weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
+    for (int c = 0; c < m; ++c) {
+      const double *L = locals + (cell * m + c) * (int64_t)P3;
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < P; ++a) {
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          const double *Lab = L + (a * P + b) * P;
+          double sb = 0.0;
+#pragma unroll
+          for (int k = 0; k < P; ++k) sb = fma(wz[k], Lab[k], sb);
+          s = fma(wx[a] * wy[b], sb, s);  // same products as the warp kernel
+        }
+      }
+      phi[i * m + c] = s;
+    }
+  }
+}
+
 struct LeafCall {
   const double *pts4, *ws;
   int m;
   const int64_t *leaves, *starts, *counts, *n_leaves;
   int64_t max_leaves;
   int levels;
+  bool per_point;  // L2P: thread per point (sparse leaves)
   Interp ip;
   LeafGeom g;
   const double *locals;
@@ -239,6 +291,12 @@ int launch_leaf(bool p2m, const LeafCall &a) {
         a.pts4, a.ws, a.m, a.leaves, a.starts, a.counts, a.n_leaves, a.ip, a.g, a.out,
         a.flag);
     return check_launch("p2m_leaf_kernel");
+  }
+  if (a.per_point) {
+    l2p_point_kernel<P><<<(unsigned)(kNumSMs * 16), 128, 0, a.st>>>(
+        a.pts4, a.m, a.starts, a.counts, a.n_leaves, a.levels, a.ip, a.g, a.locals, a.out,
+        a.flag);
+    return check_launch("l2p_point_kernel");
   }
   l2p_warp_kernel<P><<<(unsigned)grid_cap(ceil_div(a.max_leaves, l2p_warps<P>()), 16),
                        32 * l2p_warps<P>(), 0, a.st>>>(

@@ -114,6 +114,9 @@ class FmmEvaluator:
         # field.  Measured on C2 (B200): 4.95 -> 4.90 ms only -- the DMMA M2L
         # and the DFMA P2P contend for the same SMs -- so it is opt-in.
         self.overlap_near = False
+        # L2P: warp per leaf ("warp"), thread per point ("point"), or "auto"
+        # (point for sparse clouds); bitwise-identical results
+        self.l2p_mode = "auto"
         # coarse far-field levels on a side stream (see _far_field)
         self.stream_levels = True
         self._side = None
@@ -407,7 +410,11 @@ class FmmEvaluator:
                                             locs[lev + 1][8 * qlo * row:].data_ptr(),
                                             qhi - qlo, p, m, _native.dptr(self._H), st),
                           "bfmm_l2l")
-        _native.check(self.lib.bfmm_l2p(
+        # fewer than 8 points per leaf cell on average: one thread per point
+        sparse = (self.l2p_mode == "point" or
+                  (self.l2p_mode == "auto" and tree.n < 8 * (1 << (3 * L))))
+        l2p = self.lib.bfmm_l2p_points if sparse else self.lib.bfmm_l2p
+        _native.check(l2p(
             tree.pts4.data_ptr(), m, tree.leaves.data_ptr(), tree.starts.data_ptr(),
             tree.counts.data_ptr(), tree.n_leaves.data_ptr(), tree.max_leaves, L, p,
             self._scheme_id, _native.dptr(self._interp), _native.dptr(leaf_geom),

@@ -431,3 +431,22 @@ def test_active_far_field_matches_dense(ncols, distinct, cache_dir):
         ref = O.OracleFMM(bf.EXPONENTIAL, 5, 4, "chebyshev", 1e-7, (0.5, 0.5, 0.5), 1.0).matvec(
             pts, weights=w)
         assert rel_l2(res["active"], ref.reshape(res["active"].shape)) < PHI_TOL
+
+
+@pytest.mark.parametrize("scheme", ["chebyshev", "uniform"])
+def test_l2p_point_and_warp_kernels_agree_bitwise(scheme, cache_dir):
+    """The thread-per-point L2P (sparse clouds) and the warp-per-leaf one do
+    the same arithmetic: identical phi, including 3 columns and crowded
+    leaves (> 32 points)."""
+    gen = np.random.default_rng(97)
+    pts = np.vstack([gen.random((3000, 3)),
+                     np.clip(0.4 + 0.01 * gen.standard_normal((400, 3)), 0, 1)])
+    w = gen.standard_normal((len(pts), 3))
+    plan = bf.FmmPlan(levels=4, order=4, scheme=scheme, eps=1e-6,
+                      domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+    ev.l2p_mode = "warp"
+    a = ev.evaluate(pts, weights=w)
+    ev.l2p_mode = "point"
+    b = ev.evaluate(pts, weights=w)
+    assert np.array_equal(a, b)
