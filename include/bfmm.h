@@ -76,6 +76,14 @@ int bfmm_active_cells(const int64_t *leaves, const int64_t *n_leaves,
                       int64_t max_leaves, int shift, int64_t lo, int64_t hi,
                       void *scratch, size_t scratch_bytes, int64_t *list,
                       int64_t *count, bfmm_stream_t stream);
+/* hist[o] (device, 8 entries) = number of the first *n_dev cells with
+ * (cell & 7) == o. */
+int bfmm_octant_histogram(const int64_t *cells, const int64_t *n_dev, int64_t max_n,
+                          int64_t *hist, bfmm_stream_t stream);
+/* out = cells stably grouped by octant (cell & 7), ascending within a group. */
+size_t bfmm_group_by_octant_scratch_bytes(int64_t n);
+int bfmm_group_by_octant(const int64_t *cells, int64_t n, int64_t *out, void *scratch,
+                         size_t scratch_bytes, bfmm_stream_t stream);
 
 /* ---- upward pass ------------------------------------------------------- */
 
@@ -135,12 +143,15 @@ int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq);
 int bfmm_m2l_cheb(const double *z, double *lt, int level, int m, int rp,
                   int nsplit, int64_t q_lo, int64_t nq, const double *cores,
                   bfmm_stream_t stream);
-/* Same translation for the nq listed parents qlist (device, from
- * bfmm_active_cells at level - 1) only; lt is compact: layout
- * (nq, 8, m, nsplit, rp), row (8 q + o) for child o of qlist[q]. */
-int bfmm_m2l_cheb_list(const double *z, double *lt, int level, int m, int rp,
-                       int nsplit, const int64_t *qlist, int64_t nq,
-                       const double *cores, bfmm_stream_t stream);
+/* Same translation for listed target cells only (sparse clouds): cells
+ * (device) holds the active cells grouped by octant -- cells[oct_off[o] ..
+ * oct_off[o + 1]) have (cell & 7) == o -- and oct_off (host, 9 entries) the
+ * group offsets (bfmm_active_cells at this level, bfmm_octant_histogram,
+ * bfmm_group_by_octant).  lt is compact: row oct_off[o] + q for listed cell
+ * q of octant o, layout (n_listed, m, nsplit, rp). */
+int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m, int rp,
+                        int nsplit, const int64_t *cells, const int64_t *oct_off,
+                        const double *cores, bfmm_stream_t stream);
 
 /* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
  * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ) over the valid far

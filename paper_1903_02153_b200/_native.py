@@ -33,7 +33,10 @@ SIGNATURES = {
     "bfmm_m2m": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
     "bfmm_rows_gemm": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P]),
     "bfmm_rows_gemm_scatter": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P, _I64, _P]),
-    "bfmm_m2l_cheb_list": (_I, [_P, _P, _I, _I, _I, _I, _P, _I64, _P, _P]),
+    "bfmm_m2l_cheb_cells": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "bfmm_octant_histogram": (_I, [_P, _P, _I64, _P, _P]),
+    "bfmm_group_by_octant_scratch_bytes": (_SZ, [_I64]),
+    "bfmm_group_by_octant": (_I, [_P, _I64, _P, _P, _SZ, _P]),
     "bfmm_active_cells_scratch_bytes": (_SZ, [_I64]),
     "bfmm_active_cells": (_I, [_P, _P, _I64, _I, _I64, _I64, _P, _SZ, _P, _P, _P]),
     "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I, _I64]),

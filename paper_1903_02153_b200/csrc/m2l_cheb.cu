@@ -440,29 +440,41 @@ extern "C" int bfmm_m2l_cheb(const double *z, double *lt, int level, int m,
     return 2;
   }
   ensure_offsets();
-  M2LCall a{z, lt, level, m, rp, nsplit, q_lo, nq, nullptr, cores, as_stream(stream)};
+  M2LCall a{z, lt, level, m, rp, nsplit, q_lo, nq, OctList{nullptr, {}}, cores,
+            as_stream(stream)};
   return dispatch_ws(m2l_mw(nq * m), m2l_nt8(rp), a);
 }
 
-extern "C" int bfmm_m2l_cheb_list(const double *z, double *lt, int level, int m,
-                                  int rp, int nsplit, const int64_t *qlist,
-                                  int64_t nq, const double *cores,
-                                  bfmm_stream_t stream) {
+extern "C" int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m,
+                                   int rp, int nsplit, const int64_t *cells,
+                                   const int64_t *oct_off, const double *cores,
+                                   bfmm_stream_t stream) {
   if (rp % 8 != 0 || rp <= 0 || level < 2 || level > 10) {
-    set_error("bfmm_m2l_cheb_list: rp=%d must be a positive multiple of 8, level=%d",
+    set_error("bfmm_m2l_cheb_cells: rp=%d must be a positive multiple of 8, level=%d",
               rp, level);
     return 2;
   }
   if (nsplit < 1 || nsplit > 189) {
-    set_error("bfmm_m2l_cheb_list: nsplit=%d outside [1, 189]", nsplit);
+    set_error("bfmm_m2l_cheb_cells: nsplit=%d outside [1, 189]", nsplit);
     return 2;
   }
-  if (nq < 0 || nq > (int64_t(1) << (3 * level - 3)) || (nq > 0 && !qlist)) {
-    set_error("bfmm_m2l_cheb_list: %lld listed parents invalid at level %d",
-              (long long)nq, level);
+  OctList act{cells, {}};
+  int64_t longest = 0;
+  for (int o = 0; o <= 8; ++o) {
+    act.off[o] = oct_off[o];
+    if (o > 0 && (oct_off[o] < oct_off[o - 1])) {
+      set_error("bfmm_m2l_cheb_cells: octant offsets not ascending");
+      return 2;
+    }
+    if (o > 0) longest = std::max(longest, oct_off[o] - oct_off[o - 1]);
+  }
+  if (oct_off[8] > (int64_t(1) << (3 * level)) || (oct_off[8] > 0 && !cells)) {
+    set_error("bfmm_m2l_cheb_cells: %lld listed cells invalid at level %d",
+              (long long)oct_off[8], level);
     return 2;
   }
+  if (oct_off[8] == 0) return 0;
   ensure_offsets();
-  M2LCall a{z, lt, level, m, rp, nsplit, 0, nq, qlist, cores, as_stream(stream)};
-  return dispatch_ws(m2l_mw(nq * m), m2l_nt8(rp), a);
+  M2LCall a{z, lt, level, m, rp, nsplit, 0, 0, act, cores, as_stream(stream)};
+  return dispatch_ws(m2l_mw(longest * m), m2l_nt8(rp), a);
 }

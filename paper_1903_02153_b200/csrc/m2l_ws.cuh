@@ -50,11 +50,17 @@ struct WsShape {
   static constexpr int threads = 32 * (kWsConsumers + 1);
 };
 
+// Octant-grouped active target cells: cells[off[o] .. off[o + 1]) are the
+// listed cells with (cell & 7) == o.
+struct OctList {
+  const int64_t *cells;
+  int64_t off[9];
+};
+
 template <int NT8, int MW>
 __global__ void __launch_bounds__(WsShape<NT8, MW>::threads, 2)
 m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
-              int m, int rp, int nsplit, int64_t q_lo, int64_t nq,
-              const int64_t *__restrict__ qlist,
+              int m, int rp, int nsplit, int64_t q_lo, int64_t nq, OctList act,
               const double *__restrict__ cores) {
   using S = WsShape<NT8, MW>;
   constexpr int TM = S::TM, TNc = S::TN, LDK = S::LDK;
@@ -66,11 +72,13 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
   const int per = (189 + nsplit - 1) / nsplit;
   const int v_lo = split * per, v_hi = min(189, v_lo + per);
   const int n = 1 << level;
-  // rows: (parent index q < nq, column) of target cells 8Q + o, where the
-  // parent is Q = q_lo + q (dense range; lt rows absolute) or Q = qlist[q]
-  // (active parents only; lt rows compact, (8q + o) * m + column)
-  const int64_t rows = nq * m;
+  // rows: (index q, column) of the octant-o target cells, either the children
+  // 8 (q_lo + q) + o of a dense parent range (lt rows absolute), or the listed
+  // active cells act.cells[act.off[o] + q] (lt rows compact, in list order)
+  const int64_t *ocells = act.cells ? act.cells + act.off[o] : nullptr;
+  const int64_t rows = (act.cells ? act.off[o + 1] - act.off[o] : nq) * m;
   const int64_t row0 = int64_t(blockIdx.x) * TM;
+  if (row0 >= rows) return;  // octant lists differ in length (whole CTA)
   const int n0 = blockIdx.y * TNc;
   const int groups = rp >> 3;
   const int nsteps = (v_hi - v_lo) * groups;
@@ -98,8 +106,8 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
       if (rok[i]) {
         const int64_t q = r / m;
         colm[i] = (int)(r - q * m);
-        const int64_t qa = qlist ? qlist[q] : q_lo + q;
-        unmorton3((uint64_t)(8 * qa + o), cx[i], cy[i], cz[i]);
+        const int64_t cell = ocells ? ocells[q] : 8 * (q_lo + q) + o;
+        unmorton3((uint64_t)cell, cx[i], cy[i], cz[i]);
       }
     }
     int64_t srow[RPL];
@@ -183,8 +191,8 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
     if (r >= rows) continue;
     const int64_t q = r / m;
     const int c = (int)(r - q * m);
-    const int64_t qo = qlist ? q : q_lo + q;
-    double *dst = lt + (((8 * qo + o) * m + c) * nsplit + split) * rp;
+    const int64_t orow = ocells ? act.off[o] + q : 8 * (q_lo + q) + o;
+    double *dst = lt + ((orow * m + c) * nsplit + split) * rp;
 #pragma unroll
     for (int j = 0; j < NT8; ++j) {
       const int col = n0 + j * 8 + 2 * t4;
@@ -200,7 +208,7 @@ struct M2LCall {
   double *lt;
   int level, m, rp, nsplit;
   int64_t q_lo, nq;  // target parents [q_lo, q_lo + nq) at level - 1
-  const int64_t *qlist;  // or: nq listed parents (nullptr = dense range)
+  OctList act;       // or: listed active cells (act.cells != nullptr)
   const double *cores;
   cudaStream_t st;
 };
@@ -214,11 +222,15 @@ int launch_ws(const M2LCall &a) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
     attr_set = true;
   }
-  const int64_t rows = a.nq * a.m;
+  int64_t rows = a.nq * a.m;
+  if (a.act.cells) {  // the longest octant list sizes the grid
+    rows = 0;
+    for (int o = 0; o < 8; ++o) rows = std::max(rows, (a.act.off[o + 1] - a.act.off[o]) * a.m);
+  }
   if (rows <= 0) return 0;
   dim3 grid((unsigned)ceil_div(rows, S::TM), (unsigned)ceil_div(a.rp, S::TN), 8 * a.nsplit);
   m2l_ws_kernel<NT8, MW><<<grid, S::threads, S::smem, a.st>>>(
-      a.z, a.lt, a.level, a.m, a.rp, a.nsplit, a.q_lo, a.nq, a.qlist, a.cores);
+      a.z, a.lt, a.level, a.m, a.rp, a.nsplit, a.q_lo, a.nq, a.act, a.cores);
   return check_launch("m2l_ws_kernel");
 }
 

@@ -242,6 +242,22 @@ __global__ void active_emit_kernel(const int64_t *__restrict__ leaves,
   }
 }
 
+// Histogram of the octant (cell & 7) of the first *n cells.
+__global__ void octant_hist_kernel(const int64_t *__restrict__ cells,
+                                   const int64_t *__restrict__ n_dev,
+                                   int64_t *__restrict__ hist) {
+  __shared__ unsigned long long h[8];
+  if (threadIdx.x < 8) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t n = *n_dev;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&h[cells[i] & 7], 1ull);
+  __syncthreads();
+  if (threadIdx.x < 8 && h[threadIdx.x])
+    atomicAdd(reinterpret_cast<unsigned long long *>(hist) + threadIdx.x, h[threadIdx.x]);
+}
+
 }  // namespace
 }  // namespace bfmm
 
@@ -335,4 +351,43 @@ extern "C" int bfmm_active_cells(const int64_t *leaves, const int64_t *n_leaves,
   active_emit_kernel<<<grid_for(max_leaves, T), T, 0, st>>>(leaves, max_leaves, shift, flag,
                                                            pos, list, count);
   return check_launch("active_emit_kernel");
+}
+
+extern "C" int bfmm_octant_histogram(const int64_t *cells, const int64_t *n_dev,
+                                     int64_t max_n, int64_t *hist, bfmm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(hist, 0, 8 * sizeof(int64_t), st) != cudaSuccess) {
+    set_error("bfmm_octant_histogram: memset failed");
+    return 1;
+  }
+  if (max_n <= 0) return 0;
+  octant_hist_kernel<<<grid_for(max_n, 256), 256, 0, st>>>(cells, n_dev, hist);
+  return check_launch("octant_hist_kernel");
+}
+
+extern "C" size_t bfmm_group_by_octant_scratch_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (unsigned long long *)nullptr,
+                                 (unsigned long long *)nullptr, (int)(n < 1 ? 1 : n), 0, 3);
+  return bytes;
+}
+
+extern "C" int bfmm_group_by_octant(const int64_t *cells, int64_t n, int64_t *out,
+                                    void *scratch, size_t scratch_bytes,
+                                    bfmm_stream_t stream) {
+  if (n <= 0) return 0;
+  if (n > INT32_MAX || scratch_bytes < bfmm_group_by_octant_scratch_bytes(n)) {
+    set_error("bfmm_group_by_octant: n=%lld or scratch too small", (long long)n);
+    return 2;
+  }
+  // stable LSD sort on the 3 octant bits: grouped by octant, ascending within
+  if (cub::DeviceRadixSort::SortKeys(scratch, scratch_bytes,
+                                     reinterpret_cast<const unsigned long long *>(cells),
+                                     reinterpret_cast<unsigned long long *>(out), (int)n, 0,
+                                     3, as_stream(stream)) != cudaSuccess) {
+    set_error("bfmm_group_by_octant: sort failed");
+    return 1;
+  }
+  add_launches(2);
+  return 0;
 }

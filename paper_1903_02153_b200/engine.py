@@ -270,9 +270,10 @@ class FmmEvaluator:
                 qhi - qlo, p, m, _native.dptr(self._H), st), "bfmm_m2m")
         return moments, leaf_geom
 
-    def _active_parents(self, ttree, shard):
-        """{level: (parents at level - 1 with an occupied target leaf below,
-        their number)} for the levels where the list pays (see far_mode)."""
+    def _active_cells(self, ttree, shard):
+        """{level: (active target cells grouped by octant, host octant offsets
+        (9), their number)} for the levels where the list pays (see far_mode):
+        the cells at that level with an occupied target leaf below them."""
         torch = _torch()
         L = self.plan.levels
         if self.plan.scheme is not SchemeKind.CHEBYSHEV or self.far_mode == "dense":
@@ -283,24 +284,37 @@ class FmmEvaluator:
         sb = self.lib.bfmm_active_cells_scratch_bytes(cap)
         scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
         levels = list(range(2, L + 1))
-        counts = torch.zeros(len(levels), dtype=torch.int64, device=self.device)
+        counts = torch.zeros(len(levels) * 9, dtype=torch.int64, device=self.device)
         lists = {}
         st = self._stream()
         for i, lev in enumerate(levels):
             lo, hi = self._cells(lev, shard)
-            qlo, qhi = lo // 8, hi // 8
-            lst = torch.empty(min(cap, qhi - qlo) or 1, dtype=torch.int64, device=self.device)
+            lst = torch.empty(min(cap, hi - lo) or 1, dtype=torch.int64, device=self.device)
             _native.check(self.lib.bfmm_active_cells(
-                ttree.leaves.data_ptr(), ttree.n_leaves.data_ptr(), cap, 3 * (L - lev + 1),
-                qlo, qhi, scratch.data_ptr(), sb, lst.data_ptr(), counts[i:].data_ptr(), st),
+                ttree.leaves.data_ptr(), ttree.n_leaves.data_ptr(), cap, 3 * (L - lev), lo, hi,
+                scratch.data_ptr(), sb, lst.data_ptr(), counts[9 * i:].data_ptr(), st),
                 "bfmm_active_cells")
-            lists[lev] = (lst, qhi - qlo)
-        nact = counts.cpu().numpy()  # one read-back sizes every level's grid
+            _native.check(self.lib.bfmm_octant_histogram(
+                lst.data_ptr(), counts[9 * i:].data_ptr(), lst.numel(),
+                counts[9 * i + 1:].data_ptr(), st), "bfmm_octant_histogram")
+            lists[lev] = (lst, hi - lo)
+        cnt = counts.cpu().numpy().reshape(len(levels), 9)  # one read-back sizes every grid
         out = {}
         for i, lev in enumerate(levels):
-            lst, nq = lists[lev]
-            if self.far_mode == "active" or nact[i] * 4 < nq * 3:
-                out[lev] = (lst, int(nact[i]))
+            lst, ncell = lists[lev]
+            nact = int(cnt[i, 0])
+            if not (self.far_mode == "active" or nact * 4 < ncell * 3):
+                continue
+            grouped = torch.empty(max(nact, 1), dtype=torch.int64, device=self.device)
+            if nact:
+                gb = self.lib.bfmm_group_by_octant_scratch_bytes(nact)
+                gs = torch.empty(max(gb, 1), dtype=torch.uint8, device=self.device)
+                _native.check(self.lib.bfmm_group_by_octant(
+                    lst.data_ptr(), nact, grouped.data_ptr(), gs.data_ptr(), gb, st),
+                    "bfmm_group_by_octant")
+            off = np.zeros(9, dtype=np.int64)
+            off[1:] = np.cumsum(cnt[i, 1:])
+            out[lev] = (grouped, off, nact)
         return out
 
     def _far_field(self, moments, m, shard, active=None):
@@ -340,12 +354,13 @@ class FmmEvaluator:
         nloc = hi - lo
         out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
         if blk["kind"] == "cheb" and lev in active:
-            # only the children of active parents: compact lt rows
-            qlist, nact = active[lev]
+            # only the listed active target cells: compact lt rows
+            cells, off, nact = active[lev]
             rp = blk["rp"]
-            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, max(nact, 1)))
+            longest = int(np.max(off[1:] - off[:-1]))
+            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, max(longest, 1)))
             z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
-            lt = torch.empty((max(nact, 1) * 8 * m * ns * rp,), dtype=torch.float64,
+            lt = torch.empty((max(nact, 1) * m * ns * rp,), dtype=torch.float64,
                              device=self.device)
             out.zero_()
             _native.check(self.lib.bfmm_rows_gemm(
@@ -354,15 +369,14 @@ class FmmEvaluator:
             if shard is not None and not shard[0].full:
                 shard[1].allgather_cells(z, m * rp, lev)
             e0 = self._kevent()
-            _native.check(self.lib.bfmm_m2l_cheb_list(z.data_ptr(), lt.data_ptr(), lev, m, rp,
-                                                      ns, qlist.data_ptr(), nact,
-                                                      blk["cores"].data_ptr(), st),
-                          "bfmm_m2l_cheb_list")
+            _native.check(self.lib.bfmm_m2l_cheb_cells(
+                z.data_ptr(), lt.data_ptr(), lev, m, rp, ns, cells.data_ptr(),
+                off.ctypes.data, blk["cores"].data_ptr(), st), "bfmm_m2l_cheb_cells")
             self._kspan(f"m2l_l{lev}", e0)
             if nact:
                 _native.check(self.lib.bfmm_rows_gemm_scatter(
-                    lt.data_ptr(), nact * 8 * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
-                    scale, 0.0, ns, qlist.data_ptr(), 8 * m, st), "bfmm_rows_gemm_scatter(U)")
+                    lt.data_ptr(), nact * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
+                    scale, 0.0, ns, cells.data_ptr(), m, st), "bfmm_rows_gemm_scatter(U)")
         elif blk["kind"] == "cheb":
             rp = blk["rp"]
             ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nloc // 8))
@@ -552,7 +566,7 @@ class FmmEvaluator:
         ev[3].record()
         phi_far = None
         if not self._disable_far_field:
-            locs = self._far_field(moments, m, shard, self._active_parents(ttree, shard))
+            locs = self._far_field(moments, m, shard, self._active_cells(ttree, shard))
             ev[4].record()
             phi_far = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
             self._downward(locs, ttree, m, leaf_geom, status, phi_far, shard)
