@@ -36,65 +36,99 @@ __device__ __forceinline__ int64_t lex_of(int x, int y, int z, int n) {
   return ((int64_t)x * n + y) * n + z;
 }
 
-// ---- 1. forward transform: one CTA per (cell, column) ------------------------
+// The transforms work on G lexicographically consecutive cells (a z-run)
+// per CTA pass, so the frequency-major spectra are written / read as
+// G * 16-byte runs (64 B for G = 4) instead of isolated 16-byte values, and every
+// spectrum value is touched once.  Twiddles come from a q x q shared table
+// tw[a][b] = e^{2 pi i (a b mod q) / q} (no integer modulo in the loops).
+// G = 4 cells per run when the tiles fit in shared memory, else 2 or 1
+// (large p); fft_group() picks it.
+
+__device__ __forceinline__ void stage_twiddles(const FftGeom &g, double2 *tw) {
+  for (int e = threadIdx.x; e < g.q * g.q; e += blockDim.x) {
+    const int r = ((e / g.q) * (e % g.q)) % g.q;
+    tw[e] = make_double2(g.c[r], g.s[r]);
+  }
+}
+
+inline size_t fft_fwd_smem(const FftGeom &g, int G) {
+  const size_t F = size_t(g.q) * g.q * g.h;
+  return sizeof(double2) * (g.q * g.q + G * (g.p * g.p * g.h + g.p * g.q * g.h) + F * G) +
+         sizeof(double) * G * g.p * g.p * g.p;
+}
+
+// ---- 1. forward transform: X[col][f][lex] = rfftn(pad_q(M[cell, col]))[f] ---
 __global__ void __launch_bounds__(128)
 fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
-               int cc, FftGeom g, double2 *__restrict__ X) {
+               int cc, FftGeom g, int G, double2 *__restrict__ X) {
   extern __shared__ double2 sm2[];
   const int p = g.p, q = g.q, h = g.h, F = q * q * h;
+  const int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
-  double2 *A = sm2;            // [p][p][h]
-  double2 *B = A + p * p * h;  // [p][q][h]
-  double *in = reinterpret_cast<double *>(B + p * q * h);  // [p][p][p]
-  for (int64_t w = blockIdx.x; w < ncell * cc; w += gridDim.x) {
-    const int crel = (int)(w / ncell);
-    const int64_t lex = w - crel * ncell;
-    const int x = (int)(lex / ((int64_t)n * n)), y = (int)((lex / n) % n), z = (int)(lex % n);
-    const int64_t cell = (int64_t)morton3(x, y, z);
-    const double *src = moments + (cell * m + c0 + crel) * (int64_t)(p * p * p);
+  const int64_t ngroups = ncell / G;
+  double2 *tw = sm2;                   // [q][q]
+  double2 *A = tw + q * q;             // [G][p][p][h]  z transformed
+  double2 *B = A + G * PPH;        // [G][p][q][h]  y transformed
+  double2 *stage = B + G * PQH;    // [F][G]        x transformed
+  double *in = reinterpret_cast<double *>(stage + F * G);  // [G][p^3]
+  stage_twiddles(g, tw);
+  for (int64_t w = blockIdx.x; w < ngroups * cc; w += gridDim.x) {
+    const int crel = (int)(w / ngroups);
+    const int64_t lex0 = (w - crel * ngroups) * G;
     __syncthreads();
-    for (int e = threadIdx.x; e < p * p * p; e += blockDim.x) in[e] = src[e];
+    for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
+      const int gi = e / P3, r = e - gi * P3;
+      const int64_t lex = lex0 + gi;
+      const int x = (int)(lex / ((int64_t)n * n)), y = (int)((lex / n) % n), z = (int)(lex % n);
+      in[e] = moments[((int64_t)morton3(x, y, z) * m + c0 + crel) * P3 + r];
+    }
     __syncthreads();
     // z: real -> h complex bins, e^{-2 pi i k kz / q}
-    for (int e = threadIdx.x; e < p * p * h; e += blockDim.x) {
-      const int ij = e / h, kz = e - ij * h;
+    for (int e = threadIdx.x; e < G * PPH; e += blockDim.x) {
+      const int gi = e / PPH, r = e - gi * PPH, ij = r / h, kz = r - ij * h;
+      const double *v = in + gi * P3 + ij * p;
       double re = 0.0, im = 0.0;
       for (int k = 0; k < p; ++k) {
-        const int r = (k * kz) % q;
-        const double v = in[ij * p + k];
-        re = fma(v, g.c[r], re);
-        im = fma(-v, g.s[r], im);
+        const double2 t = tw[k * q + kz];
+        re = fma(v[k], t.x, re);
+        im = fma(-v[k], t.y, im);
       }
       A[e] = make_double2(re, im);
     }
     __syncthreads();
     // y: p inputs -> q bins
-    for (int e = threadIdx.x; e < p * q * h; e += blockDim.x) {
-      const int i = e / (q * h), rem = e - i * q * h, ky = rem / h, kz = rem - ky * h;
+    for (int e = threadIdx.x; e < G * PQH; e += blockDim.x) {
+      const int gi = e / PQH, r = e - gi * PQH;
+      const int i = r / (q * h), rem = r - i * q * h, ky = rem / h, kz = rem - ky * h;
+      const double2 *a = A + gi * PPH + i * p * h + kz;
       double re = 0.0, im = 0.0;
       for (int j = 0; j < p; ++j) {
-        const int r = (j * ky) % q;
-        const double2 a = A[(i * p + j) * h + kz];
-        // (a.x + i a.y)(c - i s)
-        re = fma(a.x, g.c[r], fma(a.y, g.s[r], re));
-        im = fma(a.y, g.c[r], fma(-a.x, g.s[r], im));
+        const double2 t = tw[j * q + ky], v = a[j * h];
+        re = fma(v.x, t.x, fma(v.y, t.y, re));  // (v.x + i v.y)(c - i s)
+        im = fma(v.y, t.x, fma(-v.x, t.y, im));
       }
       B[e] = make_double2(re, im);
     }
     __syncthreads();
-    // x: p inputs -> q bins, frequency-major to global
-    double2 *dst = X + (int64_t)crel * F * ncell + lex;
-    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    // x: p inputs -> q bins, into the [f][cell] staging tile
+    for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
+      const int f = e / G, gi = e - f * G;
       const int kx = f / (q * h), rem = f - kx * q * h;
+      const double2 *b = B + gi * PQH + rem;
       double re = 0.0, im = 0.0;
       for (int i = 0; i < p; ++i) {
-        const int r = (i * kx) % q;
-        const double2 b = B[i * q * h + rem];
-        re = fma(b.x, g.c[r], fma(b.y, g.s[r], re));
-        im = fma(b.y, g.c[r], fma(-b.x, g.s[r], im));
+        const double2 t = tw[i * q + kx], v = b[i * q * h];
+        re = fma(v.x, t.x, fma(v.y, t.y, re));
+        im = fma(v.y, t.x, fma(-v.x, t.y, im));
       }
-      dst[(int64_t)f * ncell] = make_double2(re, im);
+      stage[e] = make_double2(re, im);
+    }
+    __syncthreads();
+    double2 *dst = X + (int64_t)crel * F * ncell + lex0;
+    for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
+      const int f = e / G, gi = e - f * G;
+      dst[(int64_t)f * ncell + gi] = stage[e];
     }
   }
 }
@@ -196,62 +230,91 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
   }
 }
 
-// ---- 3. inverse transform + crop + scale: one CTA per (own cell, column) ------
+// ---- 3. inverse transform + crop + scale ------------------------------------
+inline size_t fft_inv_smem(const FftGeom &g, int G) {
+  const size_t F = size_t(g.q) * g.q * g.h;
+  return sizeof(double2) * (g.q * g.q + F * G + G * (g.p * g.q * g.h + g.p * g.p * g.h));
+}
+
+inline int fft_group(const FftGeom &g) {
+  for (int G = 4; G > 1; G /= 2)
+    if (std::max(fft_fwd_smem(g, G), fft_inv_smem(g, G)) <= 200 * 1024) return G;
+  return 1;
+}
+
 __global__ void __launch_bounds__(128)
-fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_t ncell_own,
-               int m, int c0, int cc, FftGeom g, double scale, double *__restrict__ locals) {
+fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_t cell_hi,
+               int m, int c0, int cc, FftGeom g, int G, double scale,
+               double *__restrict__ locals) {
   extern __shared__ double2 sm2[];
-  const int p = g.p, q = g.q, h = g.h;
+  const int p = g.p, q = g.q, h = g.h, F = q * q * h;
+  const int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
-  double2 *C = sm2;            // [p][q][h]   x inverted, i < p
-  double2 *D = C + p * q * h;  // [p][p][h]   y inverted, j < p
+  const int64_t ngroups = ncell / G;
+  double2 *tw = sm2;                 // [q][q]
+  double2 *stage = tw + q * q;       // [F][G]
+  double2 *C = stage + F * G;    // [G][p][q][h]  x inverted, i < p
+  double2 *D = C + G * PQH;      // [G][p][p][h]  y inverted, j < p
   const double norm = scale / ((double)q * q * q);
-  for (int64_t w = blockIdx.x; w < ncell_own * cc; w += gridDim.x) {
-    const int crel = (int)(w / ncell_own);
-    const int64_t cell = cell_lo + (w - crel * ncell_own);
-    int x, y, z;
-    unmorton3((uint64_t)cell, x, y, z);
-    const double2 *src = Y + (int64_t)crel * q * q * h * ncell + lex_of(x, y, z, n);
+  stage_twiddles(g, tw);
+  for (int64_t w = blockIdx.x; w < ngroups * cc; w += gridDim.x) {
+    const int crel = (int)(w / ngroups);
+    const int64_t lex0 = (w - crel * ngroups) * G;
+    const int x = (int)(lex0 / ((int64_t)n * n)), y = (int)((lex0 / n) % n), z0 = (int)(lex0 % n);
+    // the run's cells in this call's Morton range (a shard's own targets)
+    bool any = false;
+    for (int gi = 0; gi < G; ++gi) {
+      const int64_t id = (int64_t)morton3(x, y, z0 + gi);
+      any |= id >= cell_lo && id < cell_hi;
+    }
+    if (!any) continue;  // uniform across the CTA
+    __syncthreads();
+    const double2 *src = Y + (int64_t)crel * F * ncell + lex0;
+    for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
+      const int f = e / G, gi = e - f * G;
+      stage[e] = src[(int64_t)f * ncell + gi];
+    }
     __syncthreads();
     // x: q bins -> p outputs, e^{+2 pi i i kx / q}
-    for (int e = threadIdx.x; e < p * q * h; e += blockDim.x) {
-      const int i = e / (q * h), rem = e - i * q * h;
+    for (int e = threadIdx.x; e < G * PQH; e += blockDim.x) {
+      const int gi = e / PQH, r = e - gi * PQH, i = r / (q * h), rem = r - i * q * h;
       double re = 0.0, im = 0.0;
       for (int kx = 0; kx < q; ++kx) {
-        const int r = (i * kx) % q;
-        const double2 yv = src[(int64_t)(kx * q * h + rem) * ncell];
-        re = fma(yv.x, g.c[r], fma(-yv.y, g.s[r], re));
-        im = fma(yv.y, g.c[r], fma(yv.x, g.s[r], im));
+        const double2 t = tw[i * q + kx], v = stage[(kx * q * h + rem) * G + gi];
+        re = fma(v.x, t.x, fma(-v.y, t.y, re));
+        im = fma(v.y, t.x, fma(v.x, t.y, im));
       }
       C[e] = make_double2(re, im);
     }
     __syncthreads();
     // y: q bins -> p outputs
-    for (int e = threadIdx.x; e < p * p * h; e += blockDim.x) {
-      const int i = e / (p * h), rem = e - i * p * h, j = rem / h, kz = rem - j * h;
+    for (int e = threadIdx.x; e < G * PPH; e += blockDim.x) {
+      const int gi = e / PPH, r = e - gi * PPH, i = r / (p * h), rem = r - i * p * h;
+      const int j = rem / h, kz = rem - j * h;
+      const double2 *c = C + gi * PQH + i * q * h + kz;
       double re = 0.0, im = 0.0;
       for (int ky = 0; ky < q; ++ky) {
-        const int r = (j * ky) % q;
-        const double2 c = C[(i * q + ky) * h + kz];
-        re = fma(c.x, g.c[r], fma(-c.y, g.s[r], re));
-        im = fma(c.y, g.c[r], fma(c.x, g.s[r], im));
+        const double2 t = tw[j * q + ky], v = c[ky * h];
+        re = fma(v.x, t.x, fma(-v.y, t.y, re));
+        im = fma(v.y, t.x, fma(v.x, t.y, im));
       }
       D[e] = make_double2(re, im);
     }
     __syncthreads();
     // z: Hermitian half spectrum -> p real outputs (irfft: DC imaginary
     // part dropped, bins 1..q/2 counted twice; q is odd so no Nyquist bin)
-    double *dst = locals + (cell * m + c0 + crel) * (int64_t)(p * p * p);
-    for (int e = threadIdx.x; e < p * p * p; e += blockDim.x) {
-      const int ij = e / p, k = e - ij * p;
-      const double2 *d = D + ij * h;
+    for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
+      const int gi = e / P3, r = e - gi * P3, ij = r / p, k = r - ij * p;
+      const int64_t cell = (int64_t)morton3(x, y, z0 + gi);
+      if (cell < cell_lo || cell >= cell_hi) continue;
+      const double2 *d = D + gi * PPH + ij * h;
       double v = d[0].x;
       for (int kz = 1; kz < h; ++kz) {
-        const int r = (k * kz) % q;
-        v = fma(2.0 * d[kz].x, g.c[r], fma(-2.0 * d[kz].y, g.s[r], v));
+        const double2 t = tw[k * q + kz];
+        v = fma(2.0 * d[kz].x, t.x, fma(-2.0 * d[kz].y, t.y, v));
       }
-      dst[e] = norm * v;
+      locals[(cell * m + c0 + crel) * (int64_t)P3 + r] = norm * v;
     }
   }
 }
@@ -322,9 +385,8 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const short *taps = tap_table();
   double2 *X = static_cast<double2 *>(scratch);
   double2 *Y = X + ncell * cc * F;
-  const size_t smem_f = sizeof(double2) * (g.p * g.p * g.h + g.p * g.q * g.h) +
-                        sizeof(double) * g.p * g.p * g.p;
-  const size_t smem_i = sizeof(double2) * (g.p * g.q * g.h + g.p * g.p * g.h);
+  const int G = fft_group(g);
+  const size_t smem_f = fft_fwd_smem(g, G), smem_i = fft_inv_smem(g, G);
   const int n = 1 << level;
   const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
   const size_t smem_s = sizeof(double2) * (kHX * kHY * kHZP + 343);
@@ -334,19 +396,21 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
                          (int)smem_s);
     attr = true;
   }
+  cudaFuncSetAttribute(fft_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+  cudaFuncSetAttribute(fft_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_i);
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
-    const unsigned gcell = (unsigned)std::min<int64_t>(ncell * ccur, kNumSMs * 16);
-    fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, X);
+    const int64_t groups = ncell / G * ccur;
+    const unsigned gcell = (unsigned)std::min<int64_t>(groups, kNumSMs * 8);
+    fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, G, X);
     if (check_launch("fft_fwd_kernel")) return 1;
     stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
         X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
         8 * (q_lo + nq));
     if (check_launch("stencil_kernel")) return 1;
-    const int64_t own = 8 * nq;
-    const unsigned gi = (unsigned)std::min<int64_t>(std::max<int64_t>(own * ccur, 1), kNumSMs * 16);
-    fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, own, m, c0, ccur, g, scale,
-                                            locals);
+    const unsigned gi = (unsigned)std::min<int64_t>(groups, kNumSMs * 8);
+    fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, 8 * (q_lo + nq), m, c0, ccur, g,
+                                            G, scale, locals);
     if (check_launch("fft_inv_kernel")) return 1;
   }
   return 0;
