@@ -38,11 +38,11 @@ __device__ __forceinline__ int64_t lex_of(int x, int y, int z, int n) {
 
 // The transforms work on G lexicographically consecutive cells (a z-run)
 // per CTA pass, so the frequency-major spectra are written / read as
-// G * 16-byte runs (64 B for G = 4) instead of isolated 16-byte values, and every
+// G * 16-byte runs instead of isolated 16-byte values, and every
 // spectrum value is touched once.  Twiddles come from a q x q shared table
 // tw[a][b] = e^{2 pi i (a b mod q) / q} (no integer modulo in the loops).
-// G = 4 cells per run when the tiles fit in shared memory, else 2 or 1
-// (large p); fft_group() picks it.
+// G = 2 cells per run when the tiles fit in shared memory, else 1 (large
+// p); fft_group() picks it.
 
 __device__ __forceinline__ void stage_twiddles(const FftGeom &g, double2 *tw) {
   for (int e = threadIdx.x; e < g.q * g.q; e += blockDim.x) {
@@ -237,7 +237,8 @@ inline size_t fft_inv_smem(const FftGeom &g, int G) {
 }
 
 inline int fft_group(const FftGeom &g) {
-  for (int G = 4; G > 1; G /= 2)
+  // measured on C3 (p = 6): G = 2 (4 CTAs/SM) 661 ms, G = 4 763 ms, G = 1 712 ms
+  for (int G = 2; G > 1; G /= 2)
     if (std::max(fft_fwd_smem(g, G), fft_inv_smem(g, G)) <= 200 * 1024) return G;
   return 1;
 }
@@ -401,14 +402,14 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
     const int64_t groups = ncell / G * ccur;
-    const unsigned gcell = (unsigned)std::min<int64_t>(groups, kNumSMs * 8);
+    const unsigned gcell = (unsigned)std::min<int64_t>(groups, kNumSMs * 16);
     fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, G, X);
     if (check_launch("fft_fwd_kernel")) return 1;
     stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
         X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
         8 * (q_lo + nq));
     if (check_launch("stencil_kernel")) return 1;
-    const unsigned gi = (unsigned)std::min<int64_t>(groups, kNumSMs * 8);
+    const unsigned gi = (unsigned)std::min<int64_t>(groups, kNumSMs * 16);
     fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, 8 * (q_lo + nq), m, c0, ccur, g,
                                             G, scale, locals);
     if (check_launch("fft_inv_kernel")) return 1;
