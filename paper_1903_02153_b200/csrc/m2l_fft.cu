@@ -139,10 +139,13 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
 // run 3 % slower, the kernel being shared-memory-latency bound)
 constexpr int kTX = 8, kTY = 8, kTZ = 8, kR = kTZ / 2;
 constexpr int kHX = kTX + 6, kHY = kTY + 6, kHZ = kTZ + 6;
-// z stride padded to 15 (= 7 mod 8 16-byte slots; with the lane layout
-// below the x step 2*14*15 = 4 and y step 2*15 = 6 mod 8): a warp's LDS.128
-// covers the eight 16-byte bank slots evenly, 4 wavefronts (unpadded: 8)
-constexpr int kHZP = kHZ + 1;
+// Bank layout: an LDS.128 is served 8 lanes (one quarter-warp phase) at a
+// time, and those 8 lanes must hit 8 distinct 16-byte slots (mod 8).  A
+// phase's lanes vary z parity (stride 1) and 4 same-parity x positions
+// (stride 2 * HYP * HZP), so the halo is padded to HYP = 15, HZP = 15:
+// 2 * 15 * 15 = 450 = 2 (mod 8) -> slots {0,2,4,6} + {0,1}, conflict-free
+// (the unpadded 14 x 14 layout is 2-way conflicted).
+constexpr int kHYP = kHY + 1, kHZP = kHZ + 1;
 
 // grid: (tiles, frequencies, columns); block (8, 8, 2): thread (ix, iy, pz)
 // owns targets (x0+ix, y0+iy, z0+pz+2k), k < kR -- one parity class, so one
@@ -153,8 +156,8 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
                int F, const double2 *__restrict__ S, const short *__restrict__ tap_index,
                int64_t cell_lo, int64_t cell_hi) {
   extern __shared__ double2 sm2[];
-  auto halo = reinterpret_cast<double2 (*)[kHY][kHZP]>(sm2);                    // [kHX][kHY][kHZP]
-  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kHX * kHY * kHZP);     // [7][7][7]
+  auto halo = reinterpret_cast<double2 (*)[kHYP][kHZP]>(sm2);                   // [kHX][kHYP][kHZP]
+  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kHX * kHYP * kHZP);    // [7][7][7]
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
   const int tilesx = (n + kTX - 1) / kTX, tilesy = (n + kTY - 1) / kTY;
@@ -163,13 +166,13 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
   const int x0 = (trem / tilesy) * kTX, y0 = (trem % tilesy) * kTY, z0 = tz * kTZ;
   const int f = blockIdx.y, col = blockIdx.z;
   // warp w handles the (x, y) parity class (w >> 1, w & 1): its 32 lanes are
-  // 4 x 4 same-parity (x, y) positions x 2 z-parities, so the +-3 offset skips
-  // below are warp-uniform (no divergence), and the lanes' LDS.128 still
-  // cover the 8 bank slots evenly
+  // 2 z-parities (lane bit 0) x 4 same-parity x (bits 1-2) x 4 same-parity y
+  // (bits 3-4), so the +-3 offset skips below are warp-uniform (no
+  // divergence) and each 8-lane phase of an LDS.128 is conflict-free
   const int tid = (threadIdx.z * kTY + threadIdx.y) * kTX + threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
-  const int ix = ((w >> 1) & 1) + 2 * (lane & 3), iy = (w & 1) + 2 * ((lane >> 2) & 3);
-  const int pz = lane >> 4;
+  const int ix = ((w >> 1) & 1) + 2 * ((lane >> 1) & 3), iy = (w & 1) + 2 * ((lane >> 3) & 3);
+  const int pz = lane & 1;
   const int x = x0 + ix, y = y0 + iy;
   // shard filter: skip the tile when none of its targets is ours
   bool mine = false;
@@ -390,7 +393,7 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const size_t smem_f = fft_fwd_smem(g, G), smem_i = fft_inv_smem(g, G);
   const int n = 1 << level;
   const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
-  const size_t smem_s = sizeof(double2) * (kHX * kHY * kHZP + 343);
+  const size_t smem_s = sizeof(double2) * (kHX * kHYP * kHZP + 343);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
