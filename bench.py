@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--balance", default="auto", choices=["auto", "cells", "work"],
+                    help="N>1 shard ranges: equal cell ranges, work-weighted, or auto "
+                         "(work-weighted for the clustered C4)")
     return ap.parse_args()
 
 
@@ -245,7 +248,9 @@ def run_ours(args, rank, world, local_rank):
     W = torch.from_numpy(np.ascontiguousarray(wl["weights"])).cuda()
     if world > 1:
         from paper_1903_02153_b200.parallel import ShardedEvaluator
-        runner = ShardedEvaluator(ev, dist)
+        balance = args.balance if args.balance != "auto" else (
+            "work" if args.config == "C4" else "cells")
+        runner = ShardedEvaluator(ev, dist, balance=balance)
         step = lambda x, w: runner.evaluate(x, weights=w)  # noqa: E731
     else:
         runner = ev

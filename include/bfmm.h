@@ -291,6 +291,14 @@ int bfmm_near_pair_count(const int64_t *tleaves, const int64_t *tcounts,
                          const int32_t *scell_count, int levels,
                          int64_t *total, bfmm_stream_t stream);
 
+/* bins[c] (device, 64) = work of the target leaves under level-2 cell c:
+ * sum over its leaves of count * (1 + sources in the 27 neighbour leaves).
+ * Feeds work-balanced Morton shard boundaries (parallel.py). */
+int bfmm_level2_work(const int64_t *tleaves, const int64_t *tcounts,
+                     const int64_t *n_tleaves, int64_t max_tleaves,
+                     const int32_t *scell_count, int levels, int64_t *bins,
+                     bfmm_stream_t stream);
+
 /* ---- diagnostics ------------------------------------------------------- */
 
 /* Measure the FP64 FMA peak of this device (GFLOP/s) with a DFMA chain

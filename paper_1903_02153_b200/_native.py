@@ -63,6 +63,7 @@ SIGNATURES = {
     "bfmm_far_pairs_scratch_bytes": (_SZ, [_I]),
     "bfmm_near_pairs": (_I, [_I, _I, _P, _P, _I64, _P, _P, _P, _P]),
     "bfmm_near_pair_count": (_I, [_P, _P, _P, _I64, _P, _I, _P, _P]),
+    "bfmm_level2_work": (_I, [_P, _P, _P, _I64, _P, _I, _P, _P]),
     "bfmm_device_fp64_probe": (_I, [_DP, _P]),
 }
 

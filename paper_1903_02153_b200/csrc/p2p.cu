@@ -422,6 +422,36 @@ __global__ void near_count_kernel(const int64_t *__restrict__ tleaves,
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(total, local);
 }
 
+// Work of each level-2 subtree for balanced Morton shards: near pairs of its
+// target leaves (27-neighbourhood source count x target count) plus one
+// unit per target point, summed into 64 bins (leaf >> 3 (levels - 2)).
+__global__ void level2_work_kernel(const int64_t *__restrict__ tleaves,
+                                   const int64_t *__restrict__ tcounts,
+                                   const int64_t *__restrict__ n_tleaves,
+                                   const int32_t *__restrict__ scell_count, int levels,
+                                   unsigned long long *__restrict__ bins) {
+  __shared__ unsigned long long b[64];
+  if (threadIdx.x < 64) b[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t nt = *n_tleaves;
+  const int n = 1 << levels;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nt;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int cx, cy, cz;
+    unmorton3((uint64_t)tleaves[i], cx, cy, cz);
+    int64_t s = 0;
+    for (int nb = 0; nb < 27; ++nb) {
+      const int sx = cx + nb / 9 - 1, sy = cy + (nb / 3) % 3 - 1, sz = cz + nb % 3 - 1;
+      if (sx < 0 || sx >= n || sy < 0 || sy >= n || sz < 0 || sz >= n) continue;
+      s += scell_count[morton3(sx, sy, sz)];
+    }
+    atomicAdd(&b[tleaves[i] >> (3 * (levels - 2))],
+              (unsigned long long)((s + 1) * tcounts[i]));
+  }
+  __syncthreads();
+  if (threadIdx.x < 64 && b[threadIdx.x]) atomicAdd(&bins[threadIdx.x], b[threadIdx.x]);
+}
+
 // Layout: nch[max_leaves] | incl[max_leaves] | CUB temp | chunk counter
 // (256 B) | chunk -> leaf map (int32, room for every chunk of n_targets
 // points: at most one partial chunk per leaf plus n/32 full ones; the map is
@@ -772,4 +802,24 @@ extern "C" int bfmm_direct(int handle, const double *tpts, int64_t nt,
     if (check_launch("direct_kernel")) return 1;
   }
   return 0;
+}
+
+extern "C" int bfmm_level2_work(const int64_t *tleaves, const int64_t *tcounts,
+                                const int64_t *n_tleaves, int64_t max_tleaves,
+                                const int32_t *scell_count, int levels, int64_t *bins,
+                                bfmm_stream_t stream) {
+  if (levels < 2) {
+    set_error("bfmm_level2_work: levels %d < 2", levels);
+    return 2;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(bins, 0, 64 * sizeof(int64_t), st) != cudaSuccess) {
+    set_error("bfmm_level2_work: memset failed");
+    return 1;
+  }
+  if (max_tleaves <= 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256), kNumSMs * 4);
+  level2_work_kernel<<<grid, 256, 0, st>>>(tleaves, tcounts, n_tleaves, scell_count, levels,
+                                           reinterpret_cast<unsigned long long *>(bins));
+  return check_launch("level2_work_kernel");
 }

@@ -352,6 +352,9 @@ class FmmEvaluator:
         ncell = 1 << (3 * lev)
         lo, hi = self._cells(lev, shard)
         nloc = hi - lo
+        # parents covering [lo, hi) (work-balanced shards need not be
+        # 8-aligned at level 2: the few extra children computed are unused)
+        q_lo, nq = lo // 8, -(-hi // 8) - lo // 8
         out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
         if blk["kind"] == "cheb" and lev in active:
             # only the listed active target cells: compact lt rows
@@ -367,7 +370,7 @@ class FmmEvaluator:
                 moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
-                shard[1].allgather_cells(z, m * rp, lev)
+                shard[1].allgather_cells(z, m * rp, lev, shard[0])
             e0 = self._kevent()
             _native.check(self.lib.bfmm_m2l_cheb_cells(
                 z.data_ptr(), lt.data_ptr(), lev, m, rp, ns, cells.data_ptr(),
@@ -379,17 +382,17 @@ class FmmEvaluator:
                     scale, 0.0, ns, cells.data_ptr(), m, st), "bfmm_rows_gemm_scatter(U)")
         elif blk["kind"] == "cheb":
             rp = blk["rp"]
-            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nloc // 8))
+            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nq))
             z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
             _native.check(self.lib.bfmm_rows_gemm(
                 moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
-                shard[1].allgather_cells(z, m * rp, lev)  # sources from every shard
+                shard[1].allgather_cells(z, m * rp, lev, shard[0])  # sources from every shard
             e0 = self._kevent()
             _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
-                                                 lo // 8, nloc // 8, blk["cores"].data_ptr(),
+                                                 q_lo, nq, blk["cores"].data_ptr(),
                                                  st), "bfmm_m2l_cheb")
             self._kspan(f"m2l_l{lev}", e0)
             _native.check(self.lib.bfmm_rows_gemm(
@@ -397,7 +400,7 @@ class FmmEvaluator:
                 out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
         else:
             if shard is not None and not shard[0].full:
-                shard[1].allgather_cells(moments[lev], m * p3, lev)
+                shard[1].allgather_cells(moments[lev], m * p3, lev, shard[0])
             # spectra of a chunk of columns at a time (<= 16 GiB of scratch)
             nb = _native.C.c_size_t(0)
             _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, 1, p, _native.C.byref(nb)),
@@ -408,8 +411,8 @@ class FmmEvaluator:
             scratch = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=self.device)
             e0 = self._kevent()
             _native.check(self.lib.bfmm_m2l_fft(moments[lev].data_ptr(), out.data_ptr(), lev, m,
-                                                p, blk["symbols"].data_ptr(), scale, lo // 8,
-                                                nloc // 8, scratch.data_ptr(), int(nb.value),
+                                                p, blk["symbols"].data_ptr(), scale, q_lo,
+                                                nq, scratch.data_ptr(), int(nb.value),
                                                 st), "bfmm_m2l_fft")
             self._kspan(f"m2lfft_l{lev}", e0)
         return out
@@ -551,6 +554,14 @@ class FmmEvaluator:
                       "bfmm_gather_weights")
         ev[2].record()
         shard = _shard if sharded else None
+        if sharded and _shard[0].balance == "work":
+            # work-balanced Morton ranges from this target tree (same on every rank)
+            bins = torch.empty(64, dtype=torch.int64, device=self.device)
+            _native.check(self.lib.bfmm_level2_work(
+                ttree.leaves.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
+                ttree.max_leaves, stree.cell_count.data_ptr(), self.plan.levels,
+                bins.data_ptr(), st), "bfmm_level2_work")
+            _shard[0].set_work(bins.cpu().numpy())
         # sharded: rows of other ranks' targets must read as zero
         alloc = torch.zeros if sharded else torch.empty
         near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)

@@ -18,7 +18,9 @@ torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
+
+import numpy as np
 
 
 def shard_range(n_cells: int, world: int, rank: int):
@@ -29,19 +31,71 @@ def shard_range(n_cells: int, world: int, rank: int):
     return rank * per, (rank + 1) * per
 
 
+def balanced_bounds(work, world: int):
+    """Split the 64 level-2 cells into `world` contiguous non-empty groups
+    minimising the largest group's work (exact linear partition, O(64^2 G)).
+    Returns the world + 1 group boundaries; ties go to the lexicographically
+    smallest boundaries, so every rank computes the same split."""
+    w = np.asarray(work, dtype=np.float64)
+    n = len(w)
+    if not 1 <= world <= n:
+        raise ValueError(f"cannot split {n} level-2 cells over {world} ranks")
+    pre = np.concatenate([[0.0], np.cumsum(w)])
+    inf = float("inf")
+    best = np.full((world + 1, n + 1), inf)
+    cut = np.zeros((world + 1, n + 1), dtype=np.int64)
+    best[0, 0] = 0.0
+    for g in range(1, world + 1):
+        for i in range(g, n - (world - g) + 1):
+            for j in range(g - 1, i):
+                v = max(best[g - 1, j], pre[i] - pre[j])
+                if v < best[g, i]:
+                    best[g, i], cut[g, i] = v, j
+    bounds = [n]
+    for g in range(world, 0, -1):
+        bounds.append(int(cut[g, bounds[-1]]))
+    return tuple(reversed(bounds))
+
+
 @dataclass
 class MortonShards:
+    """Morton-range ownership of cells.  Ranges are unions of the 64 level-2
+    cells, bounds[r] .. bounds[r + 1], scaled by 8^(l - 2) at level l, so they
+    nest across levels.  balance="cells": equal ranges (world divides 64);
+    balance="work": boundaries from the per-level-2-cell work of the target
+    tree (set_work: equal leaf counts are wrong for C4)."""
     world: int
     rank: int
+    balance: str = "cells"
+    bounds: tuple = field(default=None)
 
     def __post_init__(self):
-        if self.world < 1 or 64 % self.world:
-            raise ValueError("the world size must divide 64 (8^2 cells at level 2)")
         if not 0 <= self.rank < self.world:
             raise ValueError(f"rank {self.rank} outside [0, {self.world})")
+        if self.balance not in ("cells", "work"):
+            raise ValueError(f"balance must be 'cells' or 'work', got {self.balance!r}")
+        if self.balance == "cells":
+            if self.world < 1 or 64 % self.world:
+                raise ValueError("the world size must divide 64 (8^2 cells at level 2)")
+            self.bounds = tuple(range(0, 65, 64 // self.world))
+        elif not 1 <= self.world <= 64:
+            raise ValueError("work-balanced shards need 1 <= world <= 64")
+
+    def set_work(self, work64):
+        self.bounds = balanced_bounds(work64, self.world)
+
+    def cells_of(self, rank: int, level: int):
+        if self.bounds is None:
+            raise ValueError("work-balanced shards need set_work() before use")
+        scale = 8 ** (level - 2)
+        return self.bounds[rank] * scale, self.bounds[rank + 1] * scale
 
     def cells(self, level: int):
-        return shard_range(8 ** level, self.world, self.rank)
+        return self.cells_of(self.rank, level)
+
+    @property
+    def equal(self) -> bool:
+        return self.bounds is not None and len(set(np.diff(self.bounds))) == 1
 
     @property
     def full(self) -> bool:
@@ -57,13 +111,26 @@ class ShardComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
-    def allgather_cells(self, full, row_elems: int, level: int):
+    def allgather_cells(self, full, row_elems: int, level: int, shards=None):
         """full: flat tensor over every cell of a level, row_elems values per
-        cell; each rank filled its own shard; afterwards all shards are
-        everywhere (all_gather_into_tensor of equal contiguous slices)."""
-        lo, hi = shard_range(8 ** level, self.world, self.rank)
-        mine = full[lo * row_elems:hi * row_elems].clone()
-        self.dist.all_gather_into_tensor(full, mine, group=self.group)
+        cell; each rank filled its own range; afterwards all ranges are
+        everywhere.  Equal ranges: one all_gather_into_tensor of the slices;
+        work-balanced ranges: slices padded to the longest, gathered, placed."""
+        if shards is None or shards.equal:
+            lo, hi = shard_range(8 ** level, self.world, self.rank)
+            mine = full[lo * row_elems:hi * row_elems].clone()
+            self.dist.all_gather_into_tensor(full, mine, group=self.group)
+            return full
+        spans = [shards.cells_of(r, level) for r in range(self.world)]
+        longest = max(hi - lo for lo, hi in spans) * row_elems
+        lo, hi = spans[self.rank]
+        mine = full.new_zeros(longest)
+        mine[:(hi - lo) * row_elems] = full[lo * row_elems:hi * row_elems]
+        buf = full.new_empty(self.world * longest)
+        self.dist.all_gather_into_tensor(buf, mine, group=self.group)
+        for r, (a, b) in enumerate(spans):
+            if r != self.rank:
+                full[a * row_elems:b * row_elems] = buf[r * longest:r * longest + (b - a) * row_elems]
         return full
 
     def allreduce_sum(self, t):
@@ -72,12 +139,16 @@ class ShardComm:
 
 
 class ShardedEvaluator:
-    """FmmEvaluator driven as one shard of a multi-GPU matvec."""
+    """FmmEvaluator driven as one shard of a multi-GPU matvec.
 
-    def __init__(self, evaluator, dist, group=None):
+    balance="work" re-balances the Morton ranges on every call from the
+    target tree's per-level-2-cell near-field work (deterministic, identical
+    on every rank, no exchange needed)."""
+
+    def __init__(self, evaluator, dist, group=None, balance="cells"):
         self.ev = evaluator
         self.comm = ShardComm(dist, group)
-        self.shards = MortonShards(self.comm.world, self.comm.rank)
+        self.shards = MortonShards(self.comm.world, self.comm.rank, balance=balance)
 
     def evaluate(self, sources, targets=None, weights=None):
         return self.ev.evaluate(sources, targets, weights, _shard=(self.shards, self.comm))

@@ -62,6 +62,52 @@ def _gloo_worker(rank, world, port, results):
     dist.destroy_process_group()
 
 
+def test_balanced_bounds_minimise_the_largest_share():
+    from paper_1903_02153_b200.parallel import balanced_bounds
+    w = np.ones(64)
+    assert balanced_bounds(w, 4) == (0, 16, 32, 48, 64)
+    w = np.zeros(64)
+    w[5] = 100.0          # one heavy cell, a light remainder
+    w[40:] = 1.0
+    b = balanced_bounds(w, 3)
+    loads = [w[b[i]:b[i + 1]].sum() for i in range(3)]
+    assert max(loads) == 100.0 and b[0] == 0 and b[-1] == 64
+    assert all(b[i] < b[i + 1] for i in range(3))
+    s = MortonShards(3, 1, balance="work")
+    s.set_work(w)
+    assert s.cells(2) == (b[1], b[2]) and s.cells(4) == (b[1] * 64, b[2] * 64)
+    assert not s.equal
+
+
+def _gloo_balanced_worker(rank, world, port, results):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = ShardComm(dist)
+    shards = MortonShards(world, rank, balance="work")
+    w = np.ones(64)
+    w[:10] = 20.0
+    shards.set_work(w)
+    lev, row = 3, 2
+    full = torch.zeros(8 ** lev * row, dtype=torch.float64)
+    lo, hi = shards.cells(lev)
+    full[lo * row:hi * row] = torch.arange(lo * row, hi * row, dtype=torch.float64)
+    comm.allgather_cells(full, row, lev, shards)
+    results[rank] = (full.numpy().copy(), shards.bounds)
+    dist.destroy_process_group()
+
+
+def test_unequal_shards_allgather_over_gloo_world2():
+    import torch.multiprocessing as mp
+    port = _free_port()
+    results = mp.Manager().dict()
+    mp.spawn(_gloo_balanced_worker, args=(2, port, results), nprocs=2, join=True)
+    assert results[0][1] == results[1][1] and results[0][1][1] != 32
+    for r in range(2):
+        assert np.array_equal(results[r][0], np.arange(8 ** 3 * 2, dtype=np.float64))
+
+
 def test_shard_comm_over_gloo_world2():
     import torch.multiprocessing as mp
     world = 2
@@ -81,13 +127,14 @@ class ThreadComm:
     def __init__(self, world, rank, board, barrier):
         self.world, self.rank, self.board, self.barrier = world, rank, board, barrier
 
-    def allgather_cells(self, full, row_elems, level):
+    def allgather_cells(self, full, row_elems, level, shards=None):
         torch.cuda.current_stream().synchronize()
         self.board[self.rank] = full
         self.barrier.wait()
         for r in range(self.world):
             if r != self.rank:
-                lo, hi = shard_range(8 ** level, self.world, r)
+                lo, hi = (shards.cells_of(r, level) if shards is not None
+                          else shard_range(8 ** level, self.world, r))
                 full[lo * row_elems:hi * row_elems].copy_(
                     self.board[r][lo * row_elems:hi * row_elems])
         torch.cuda.current_stream().synchronize()
@@ -105,16 +152,18 @@ class ThreadComm:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,scheme,far_mode", [(2, "chebyshev", "dense"),
-                                                   (4, "chebyshev", "dense"),
-                                                   (2, "uniform", "dense"),
-                                                   (4, "chebyshev", "active")])
-def test_sharded_matvec_matches_unsharded(world, scheme, far_mode, cache_dir):
+@pytest.mark.parametrize("world,scheme,far_mode,balance", [(2, "chebyshev", "dense", "cells"),
+                                                           (4, "chebyshev", "dense", "cells"),
+                                                           (2, "uniform", "dense", "cells"),
+                                                           (4, "chebyshev", "active", "cells"),
+                                                           (3, "chebyshev", "active", "work"),
+                                                           (2, "uniform", "dense", "work")])
+def test_sharded_matvec_matches_unsharded(world, scheme, far_mode, balance, cache_dir):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1903_02153_b200 as bf
     pts, w = unit_cloud(30000, seed=51, ncols=2)
-    if far_mode == "active":  # two clusters: most cells empty, shards uneven
+    if far_mode == "active" or balance == "work":  # two clusters: most cells empty
         pts[:15000] = np.clip(0.3 + 0.03 * np.random.default_rng(5).standard_normal((15000, 3)), 0, 1)
         pts[15000:] = np.clip(0.8 + 0.02 * np.random.default_rng(6).standard_normal((15000, 3)), 0, 1)
     plan = bf.FmmPlan(levels=4, order=4, scheme=scheme, eps=1e-6,
@@ -130,8 +179,9 @@ def test_sharded_matvec_matches_unsharded(world, scheme, far_mode, cache_dir):
             ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
             ev.far_mode = far_mode
             with torch.cuda.stream(torch.cuda.Stream()):
-                out[r] = ev.evaluate(pts, weights=w, _shard=(MortonShards(world, r),
-                                                             ThreadComm(world, r, board, barrier)))
+                out[r] = ev.evaluate(pts, weights=w,
+                                     _shard=(MortonShards(world, r, balance=balance),
+                                             ThreadComm(world, r, board, barrier)))
         except Exception as e:  # pragma: no cover
             errs.append(e)
             barrier.abort()
