@@ -114,6 +114,9 @@ class FmmEvaluator:
         # field.  Measured on C2 (B200): 4.95 -> 4.90 ms only -- the DMMA M2L
         # and the DFMA P2P contend for the same SMs -- so it is opt-in.
         self.overlap_near = False
+        # ... which is the default for sharded runs, where it hides the
+        # far field's all-gathers (SURVEY §8(e) "overlap")
+        self.overlap_near_sharded = True
         # L2P: warp per leaf ("warp"), thread per point ("point"), or "auto"
         # (point for sparse clouds); bitwise-identical results
         self.l2p_mode = "auto"
@@ -566,8 +569,9 @@ class FmmEvaluator:
         alloc = torch.zeros if sharded else torch.empty
         near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
         side = None
-        if self.overlap_near and not sharded:
-            # near field on a side stream, concurrent with the far field
+        if self.overlap_near or (sharded and self.overlap_near_sharded):
+            # near field on a side stream, concurrent with the far field (for
+            # a shard: computes while the level all-gathers are in flight)
             main = torch.cuda.current_stream()
             side = self._side_stream()
             side.wait_stream(main)
