@@ -171,17 +171,22 @@ m2l_ws_kernel(const double *__restrict__ z, double *__restrict__ lt, int level,
     const double *Bs = As + TM * LDK;
     const double *Aw = As + (warp * 8 * MW + g) * LDK + off;
     const double *Bw = Bs + g * LDK + off;
-    double2 a[MW];
+    double2 a[MW], b[NT8];
 #pragma unroll
     for (int i = 0; i < MW; ++i) a[i] = *reinterpret_cast<const double2 *>(Aw + i * 8 * LDK);
 #pragma unroll
-    for (int j = 0; j < NT8; ++j) {
-      const double2 b = *reinterpret_cast<const double2 *>(Bw + j * 8 * LDK);
+    for (int j = 0; j < NT8; ++j) b[j] = *reinterpret_cast<const double2 *>(Bw + j * 8 * LDK);
+    // both k4 halves of the step: all MW x NT8 accumulators with the first,
+    // then all with the second, so consecutive DMMAs on one accumulator are
+    // MW * NT8 instructions apart (back-to-back pairs stall on its latency)
 #pragma unroll
-      for (int i = 0; i < MW; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i].x, b.x);
+    for (int j = 0; j < NT8; ++j)
 #pragma unroll
-      for (int i = 0; i < MW; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i].y, b.y);
-    }
+      for (int i = 0; i < MW; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+    for (int j = 0; j < NT8; ++j)
+#pragma unroll
+      for (int i = 0; i < MW; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
