@@ -341,7 +341,10 @@ def run_ours(args, rank, world, local_rank):
             flops = pairs * fpp
             peak = dfma_tf
             roof = {"kernel": "p2p (near field, FP64 pipe)", "bound": "fp64",
-                    "flops_per_pair": fpp, "pair_interactions": pairs}
+                    "flops_per_pair": fpp, "pair_interactions": pairs,
+                    "pairs_per_s": pairs / (ms * 1e-3),
+                    "flops_note": "frozen algorithmic figure (profiles/r01_p2p_flops.txt); "
+                                  "the current kernel executes ~32 FP64 flops per pair"}
         else:
             lev = int(dom.split("_l")[1])
             flops = m2l_flops(ev, wl)[lev]
