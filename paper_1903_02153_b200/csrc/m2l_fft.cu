@@ -58,11 +58,14 @@ inline size_t fft_fwd_smem(const FftGeom &g, int G) {
 }
 
 // ---- 1. forward transform: X[col][f][lex] = rfftn(pad_q(M[cell, col]))[f] ---
+// P is a template parameter so the short DFT sums unroll and each thread's
+// independent outputs (2 per pass iteration) interleave their FMA chains.
+template <int P>
 __global__ void __launch_bounds__(128)
 fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
                int cc, FftGeom g, int G, double2 *__restrict__ X) {
   extern __shared__ double2 sm2[];
-  const int p = g.p, q = g.q, h = g.h, F = q * q * h;
+  constexpr int p = P, q = 2 * P - 1, h = q / 2 + 1, F = q * q * h;
   const int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
@@ -77,6 +80,7 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
     const int crel = (int)(w / ngroups);
     const int64_t lex0 = (w - crel * ngroups) * G;
     __syncthreads();
+    #pragma unroll 2
     for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
       const int gi = e / P3, r = e - gi * P3;
       const int64_t lex = lex0 + gi;
@@ -85,10 +89,12 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
     }
     __syncthreads();
     // z: real -> h complex bins, e^{-2 pi i k kz / q}
+    #pragma unroll 2
     for (int e = threadIdx.x; e < G * PPH; e += blockDim.x) {
       const int gi = e / PPH, r = e - gi * PPH, ij = r / h, kz = r - ij * h;
       const double *v = in + gi * P3 + ij * p;
       double re = 0.0, im = 0.0;
+#pragma unroll
       for (int k = 0; k < p; ++k) {
         const double2 t = tw[k * q + kz];
         re = fma(v[k], t.x, re);
@@ -98,11 +104,13 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
     }
     __syncthreads();
     // y: p inputs -> q bins
+    #pragma unroll 2
     for (int e = threadIdx.x; e < G * PQH; e += blockDim.x) {
       const int gi = e / PQH, r = e - gi * PQH;
       const int i = r / (q * h), rem = r - i * q * h, ky = rem / h, kz = rem - ky * h;
       const double2 *a = A + gi * PPH + i * p * h + kz;
       double re = 0.0, im = 0.0;
+#pragma unroll
       for (int j = 0; j < p; ++j) {
         const double2 t = tw[j * q + ky], v = a[j * h];
         re = fma(v.x, t.x, fma(v.y, t.y, re));  // (v.x + i v.y)(c - i s)
@@ -112,11 +120,13 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
     }
     __syncthreads();
     // x: p inputs -> q bins, into the [f][cell] staging tile
+    #pragma unroll 2
     for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
       const int f = e / G, gi = e - f * G;
       const int kx = f / (q * h), rem = f - kx * q * h;
       const double2 *b = B + gi * PQH + rem;
       double re = 0.0, im = 0.0;
+#pragma unroll
       for (int i = 0; i < p; ++i) {
         const double2 t = tw[i * q + kx], v = b[i * q * h];
         re = fma(v.x, t.x, fma(v.y, t.y, re));
@@ -126,6 +136,7 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
     }
     __syncthreads();
     double2 *dst = X + (int64_t)crel * F * ncell + lex0;
+    #pragma unroll 2
     for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
       const int f = e / G, gi = e - f * G;
       dst[(int64_t)f * ncell + gi] = stage[e];
@@ -246,12 +257,13 @@ inline int fft_group(const FftGeom &g) {
   return 1;
 }
 
+template <int P>
 __global__ void __launch_bounds__(128)
 fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_t cell_hi,
                int m, int c0, int cc, FftGeom g, int G, double scale,
                double *__restrict__ locals) {
   extern __shared__ double2 sm2[];
-  const int p = g.p, q = g.q, h = g.h, F = q * q * h;
+  constexpr int p = P, q = 2 * P - 1, h = q / 2 + 1, F = q * q * h;
   const int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
@@ -275,15 +287,18 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
     if (!any) continue;  // uniform across the CTA
     __syncthreads();
     const double2 *src = Y + (int64_t)crel * F * ncell + lex0;
+    #pragma unroll 2
     for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
       const int f = e / G, gi = e - f * G;
       stage[e] = src[(int64_t)f * ncell + gi];
     }
     __syncthreads();
     // x: q bins -> p outputs, e^{+2 pi i i kx / q}
+    #pragma unroll 2
     for (int e = threadIdx.x; e < G * PQH; e += blockDim.x) {
       const int gi = e / PQH, r = e - gi * PQH, i = r / (q * h), rem = r - i * q * h;
       double re = 0.0, im = 0.0;
+#pragma unroll
       for (int kx = 0; kx < q; ++kx) {
         const double2 t = tw[i * q + kx], v = stage[(kx * q * h + rem) * G + gi];
         re = fma(v.x, t.x, fma(-v.y, t.y, re));
@@ -293,11 +308,13 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
     }
     __syncthreads();
     // y: q bins -> p outputs
+    #pragma unroll 2
     for (int e = threadIdx.x; e < G * PPH; e += blockDim.x) {
       const int gi = e / PPH, r = e - gi * PPH, i = r / (p * h), rem = r - i * p * h;
       const int j = rem / h, kz = rem - j * h;
       const double2 *c = C + gi * PQH + i * q * h + kz;
       double re = 0.0, im = 0.0;
+#pragma unroll
       for (int ky = 0; ky < q; ++ky) {
         const double2 t = tw[j * q + ky], v = c[ky * h];
         re = fma(v.x, t.x, fma(-v.y, t.y, re));
@@ -308,12 +325,14 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
     __syncthreads();
     // z: Hermitian half spectrum -> p real outputs (irfft: DC imaginary
     // part dropped, bins 1..q/2 counted twice; q is odd so no Nyquist bin)
+    #pragma unroll 2
     for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
       const int gi = e / P3, r = e - gi * P3, ij = r / p, k = r - ij * p;
       const int64_t cell = (int64_t)morton3(x, y, z0 + gi);
       if (cell < cell_lo || cell >= cell_hi) continue;
       const double2 *d = D + gi * PPH + ij * h;
       double v = d[0].x;
+#pragma unroll
       for (int kz = 1; kz < h; ++kz) {
         const double2 t = tw[k * q + kz];
         v = fma(2.0 * d[kz].x, t.x, fma(-2.0 * d[kz].y, t.y, v));
@@ -400,21 +419,52 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
                          (int)smem_s);
     attr = true;
   }
-  cudaFuncSetAttribute(fft_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
-  cudaFuncSetAttribute(fft_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_i);
+  int rc = 0;
+  switch (p) {
+#define BFMM_FFT_ATTR(PP)                                                                      \
+  case PP:                                                                                     \
+    cudaFuncSetAttribute(fft_fwd_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                         (int)smem_f);                                                         \
+    cudaFuncSetAttribute(fft_inv_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                         (int)smem_i);                                                         \
+    break;
+    BFMM_FFT_ATTR(2) BFMM_FFT_ATTR(3) BFMM_FFT_ATTR(4) BFMM_FFT_ATTR(5) BFMM_FFT_ATTR(6)
+    BFMM_FFT_ATTR(7) BFMM_FFT_ATTR(8) BFMM_FFT_ATTR(9) BFMM_FFT_ATTR(10) BFMM_FFT_ATTR(11)
+    BFMM_FFT_ATTR(12)
+#undef BFMM_FFT_ATTR
+  }
+  (void)rc;
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
     const int64_t groups = ncell / G * ccur;
     const unsigned gcell = (unsigned)std::min<int64_t>(groups, kNumSMs * 16);
-    fft_fwd_kernel<<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, G, X);
+    switch (p) {
+#define BFMM_FFT_FWD(PP)                                                                       \
+  case PP:                                                                                     \
+    fft_fwd_kernel<PP><<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, G, X);      \
+    break;
+      BFMM_FFT_FWD(2) BFMM_FFT_FWD(3) BFMM_FFT_FWD(4) BFMM_FFT_FWD(5) BFMM_FFT_FWD(6)
+      BFMM_FFT_FWD(7) BFMM_FFT_FWD(8) BFMM_FFT_FWD(9) BFMM_FFT_FWD(10) BFMM_FFT_FWD(11)
+      BFMM_FFT_FWD(12)
+#undef BFMM_FFT_FWD
+    }
     if (check_launch("fft_fwd_kernel")) return 1;
     stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
         X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
         8 * (q_lo + nq));
     if (check_launch("stencil_kernel")) return 1;
     const unsigned gi = (unsigned)std::min<int64_t>(groups, kNumSMs * 16);
-    fft_inv_kernel<<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, 8 * (q_lo + nq), m, c0, ccur, g,
-                                            G, scale, locals);
+    switch (p) {
+#define BFMM_FFT_INV(PP)                                                                       \
+  case PP:                                                                                     \
+    fft_inv_kernel<PP><<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, 8 * (q_lo + nq), m, c0,     \
+                                                ccur, g, G, scale, locals);                    \
+    break;
+      BFMM_FFT_INV(2) BFMM_FFT_INV(3) BFMM_FFT_INV(4) BFMM_FFT_INV(5) BFMM_FFT_INV(6)
+      BFMM_FFT_INV(7) BFMM_FFT_INV(8) BFMM_FFT_INV(9) BFMM_FFT_INV(10) BFMM_FFT_INV(11)
+      BFMM_FFT_INV(12)
+#undef BFMM_FFT_INV
+    }
     if (check_launch("fft_inv_kernel")) return 1;
   }
   return 0;
