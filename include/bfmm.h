@@ -101,6 +101,15 @@ int bfmm_p2m(const double *pts4, const double *wsorted, int m,
              int64_t max_leaves, int levels, int p, int scheme,
              const double *interp, const double *geom, double *moments,
              int32_t *ref_flag, bfmm_stream_t stream);
+/* Same moments with one thread per (leaf, x-node) instead of a warp per
+ * leaf: for sparse clouds of a few points per leaf (same products and
+ * point order). */
+int bfmm_p2m_sparse(const double *pts4, const double *wsorted, int m,
+                    const int64_t *leaves, const int64_t *starts,
+                    const int64_t *counts, const int64_t *n_leaves,
+                    int64_t max_leaves, int levels, int p, int scheme,
+                    const double *interp, const double *geom, double *moments,
+                    int32_t *ref_flag, bfmm_stream_t stream);
 
 /* M2M ascend (engine.py:187-204): parent[q] = sum_o T[o] child[8q+o] with
  * T[o] = kron(Hx, Hy, Hz) (interpolation.py:136-155).  H (host) holds the

@@ -301,13 +301,13 @@ int grid_cap(int64_t work, int per_sm) {
 
 using namespace bfmm;
 
-extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
-                        const int64_t *leaves, const int64_t *starts,
-                        const int64_t *counts, const int64_t *n_leaves,
-                        int64_t max_leaves, int levels, int p, int scheme,
-                        const double *interp, const double *geom,
-                        double *moments, int32_t *ref_flag,
-                        bfmm_stream_t stream) {
+static int p2m_impl(const double *pts4, const double *wsorted, int m,
+                    const int64_t *leaves, const int64_t *starts,
+                    const int64_t *counts, const int64_t *n_leaves,
+                    int64_t max_leaves, int levels, int p, int scheme,
+                    const double *interp, const double *geom,
+                    double *moments, int32_t *ref_flag, bool per_thread,
+                    bfmm_stream_t stream) {
   if (p < 1 || p > kMaxP || m < 1) {
     set_error("bfmm_p2m: unsupported p=%d m=%d", p, m);
     return 2;
@@ -316,7 +316,7 @@ extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
   Interp ip = make_interp(p, scheme, interp);
   const LeafGeom g = make_leaf_geom(geom);
   if (p >= 2 && p <= 8) {
-    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, false, ip, g,
+    LeafCall a{pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, per_thread, ip, g,
                nullptr, moments, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, true, a);
   }
@@ -434,4 +434,26 @@ extern "C" int bfmm_l2p_points(const double *pts4, int m, const int64_t *leaves,
                                bfmm_stream_t stream) {
   return l2p_impl(pts4, m, leaves, starts, counts, n_leaves, max_leaves, levels, p, scheme,
                   interp, geom, locals, phi_sorted, ref_flag, true, stream);
+}
+
+extern "C" int bfmm_p2m(const double *pts4, const double *wsorted, int m,
+                        const int64_t *leaves, const int64_t *starts,
+                        const int64_t *counts, const int64_t *n_leaves,
+                        int64_t max_leaves, int levels, int p, int scheme,
+                        const double *interp, const double *geom,
+                        double *moments, int32_t *ref_flag,
+                        bfmm_stream_t stream) {
+  return p2m_impl(pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, p,
+                  scheme, interp, geom, moments, ref_flag, false, stream);
+}
+
+extern "C" int bfmm_p2m_sparse(const double *pts4, const double *wsorted, int m,
+                               const int64_t *leaves, const int64_t *starts,
+                               const int64_t *counts, const int64_t *n_leaves,
+                               int64_t max_leaves, int levels, int p, int scheme,
+                               const double *interp, const double *geom,
+                               double *moments, int32_t *ref_flag,
+                               bfmm_stream_t stream) {
+  return p2m_impl(pts4, wsorted, m, leaves, starts, counts, n_leaves, max_leaves, levels, p,
+                  scheme, interp, geom, moments, ref_flag, true, stream);
 }

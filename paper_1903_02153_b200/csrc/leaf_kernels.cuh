@@ -150,6 +150,64 @@ p2m_leaf_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
   }
 }
 
+// P2M for sparse leaves (a few points each): one thread per (leaf, x-node
+// i) accumulating the P x P moments M[i][j][k] over the leaf's points in
+// sorted order, with the same products as p2m_leaf_kernel -- no idle lanes,
+// and the threads of a leaf read its points as L1 broadcasts.
+template <int P>
+__global__ void __launch_bounds__(128)
+p2m_thread_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
+                  int m, const int64_t *__restrict__ leaves,
+                  const int64_t *__restrict__ starts,
+                  const int64_t *__restrict__ counts,
+                  const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
+                  double *__restrict__ moments, int32_t *flag) {
+  __shared__ double sS[P * P], sN[P];
+  stage_basis<P>(ip, sS, sN);
+  const int64_t nl = *n_leaves;
+  const double inv_hw = 1.0 / g.hw;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nl * P;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t leaf = t / P;
+    const int ii = (int)(t - leaf * P);
+    const int64_t cell = leaves[leaf];
+    if (cell < g.cell_lo || cell >= g.cell_hi) continue;  // other rank's shard
+    const int64_t s0 = starts[leaf], cnt = counts[leaf];
+    int cx, cy, cz;
+    unmorton3((uint64_t)cell, cx, cy, cz);
+    for (int c = 0; c < m; ++c) {
+      double acc[P][P];
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[j][k] = 0.0;
+      for (int64_t pt = 0; pt < cnt; ++pt) {
+        const int64_t i = s0 + pt;
+        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+        double wx[P], wy[P], wz[P];
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, inv_hw, cx, flag), wx);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.y, g.lo[1], g.h, inv_hw, cy, flag), wy);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
+        double wxi = wx[0];
+#pragma unroll
+        for (int u = 1; u < P; ++u) wxi = ii == u ? wx[u] : wxi;
+        const double v = ws[i * m + c];
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+          const double wxy = wxi * wy[j];
+#pragma unroll
+          for (int k = 0; k < P; ++k) acc[j][k] += (wxy * wz[k]) * v;
+        }
+      }
+      double *dst = moments + (cell * m + c) * (int64_t)(P * P * P) + ii * P * P;
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int k = 0; k < P; ++k) dst[j * P + k] = acc[j][k];
+    }
+  }
+}
+
 // L2P (engine.py:313-347), one warp per leaf: the leaf's locals (one column
 // at a time) are brought into the warp's shared slice with coalesced loads;
 // each lane evaluates its point's weights, parks the P^2 products wx wy in
@@ -286,6 +344,12 @@ struct LeafCall {
 template <int P>
 int launch_leaf(bool p2m, const LeafCall &a) {
   const unsigned grid = (unsigned)grid_cap(ceil_div(a.max_leaves, kLeafWarps), 16);
+  if (p2m && a.per_point) {
+    p2m_thread_kernel<P><<<(unsigned)grid_cap(ceil_div(a.max_leaves * P, 128), 16), 128, 0,
+                           a.st>>>(a.pts4, a.ws, a.m, a.leaves, a.starts, a.counts,
+                                   a.n_leaves, a.ip, a.g, a.out, a.flag);
+    return check_launch("p2m_thread_kernel");
+  }
   if (p2m) {
     p2m_leaf_kernel<P><<<grid, 32 * kLeafWarps, 0, a.st>>>(
         a.pts4, a.ws, a.m, a.leaves, a.starts, a.counts, a.n_leaves, a.ip, a.g, a.out,

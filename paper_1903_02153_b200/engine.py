@@ -117,8 +117,8 @@ class FmmEvaluator:
         # ... which is the default for sharded runs, where it hides the
         # far field's all-gathers (SURVEY §8(e) "overlap")
         self.overlap_near_sharded = True
-        # L2P: warp per leaf ("warp"), thread per point ("point"), or "auto"
-        # (point for sparse clouds); bitwise-identical results
+        # P2M / L2P: warp per leaf ("warp"), thread per (leaf, node) / point
+        # ("point"), or "auto" (thread-per-point L2P for sparse clouds)
         self.l2p_mode = "auto"
         # coarse far-field levels on a side stream (see _far_field)
         self.stream_levels = True
@@ -257,7 +257,10 @@ class FmmEvaluator:
         lo, hi = self._cells(L, shard)
         leaf_geom = np.ascontiguousarray(np.concatenate(
             [self.plan.domain.low, [self.plan.domain.length / (1 << L), float(lo), float(hi)]]))
-        _native.check(self.lib.bfmm_p2m(
+        # thread-per-(leaf, node) P2M only on request: measured 20 -> 18 ms on
+        # C5 but 5 -> 10 ms on C4, whose crowded leaves serialise one thread
+        p2m = self.lib.bfmm_p2m_sparse if self.l2p_mode == "point" else self.lib.bfmm_p2m
+        _native.check(p2m(
             tree.pts4.data_ptr(), ws.data_ptr(), m, tree.leaves.data_ptr(),
             tree.starts.data_ptr(), tree.counts.data_ptr(), tree.n_leaves.data_ptr(),
             tree.max_leaves, L, p, self._scheme_id, _native.dptr(self._interp),
