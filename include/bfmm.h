@@ -316,6 +316,11 @@ int bfmm_device_fp64_probe(double *gflops, bfmm_stream_t stream);
 
 /* Same for the FP64 tensor-core MMA (mma.sync m8n8k4 f64 -> DMMA). */
 int bfmm_device_dmma_probe(double *gflops, bfmm_stream_t stream);
+/* tcgen05 self-test (diagnostic): D (128 x 64, int32, row-major) = A (128 x K,
+ * int8, row-major) * B (64 x K, int8, row-major)^T on the 5th-gen tensor
+ * cores (kind::i8, TMEM accumulator); K a multiple of 32. */
+int bfmm_tc_i8_selftest(const int8_t *A, const int8_t *B, int K, int32_t *D,
+                        bfmm_stream_t stream);
 
 /* DMMA throughput with warps_per_sm resident warps x `chains` independent
  * accumulator chains (microarchitecture sweep behind the M2L tiling). */

@@ -43,6 +43,7 @@ SIGNATURES = {
     "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I, _I64]),
     "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _I64, _I64, _P, _P]),
     "bfmm_device_dmma_probe": (_I, [_DP, _P]),
+    "bfmm_tc_i8_selftest": (_I, [_P, _P, _I, _P, _P]),
     "bfmm_device_dmma_sweep": (_I, [_I, _I, _DP, _P]),
     "bfmm_launch_count": (C.c_longlong, []),
     "bfmm_m2l_fft_scratch_bytes": (_I, [_I, _I, _I, C.POINTER(_SZ)]),

@@ -5,6 +5,7 @@
 #include <atomic>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace bfmm {
 
@@ -195,4 +196,80 @@ extern "C" int bfmm_device_fp64_probe(double *gflops, bfmm_stream_t stream) {
   const double flops = 2.0 * 8.0 * iters * double(grid.x) * block.x;
   *gflops = flops / (best * 1e-3) / 1e9;
   return 0;
+}
+
+// ---- tcgen05 int8 self-test: D (128 x 64, int32) = A (128 x K) B (64 x K)^T ----
+namespace bfmm {
+namespace {
+__global__ void __launch_bounds__(128)
+tc_i8_selftest_kernel(const int8_t *__restrict__ A, const int8_t *__restrict__ B, int K,
+                      int32_t *__restrict__ D) {
+  using namespace bfmm;
+  __shared__ __align__(128) int8_t sA[128 * 32];
+  __shared__ __align__(128) int8_t sB[64 * 32];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t mbar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) tc::alloc(&tmem_base, 64);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = tc::idesc_i8(128, 64);
+  int phase = 0;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int e = tid; e < 128 * 2; e += 128) {
+      const int row = e >> 1, h = e & 1;
+      *reinterpret_cast<int4 *>(sA + tc::kmajor_off(row, 16 * h)) =
+          *reinterpret_cast<const int4 *>(A + (size_t)row * K + k0 + 16 * h);
+    }
+    for (int e = tid; e < 64 * 2; e += 128) {
+      const int row = e >> 1, h = e & 1;
+      *reinterpret_cast<int4 *>(sB + tc::kmajor_off(row, 16 * h)) =
+          *reinterpret_cast<const int4 *>(B + (size_t)row * K + k0 + 16 * h);
+    }
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      tc::mma_i8(tmem, tc::desc_kmajor(tc::smem_u32(sA), 128, 256),
+                 tc::desc_kmajor(tc::smem_u32(sB), 128, 256), idesc, k0 > 0 ? 1u : 0u);
+      tc::commit(&mbar);
+    }
+    // wait for the MMA before the tile is overwritten
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+            tc::smem_u32(&mbar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1;
+    tc::fence_after();
+  }
+  uint32_t v[16];
+  for (int c = 0; c < 64; c += 16) {
+    tc::ld16(tmem + ((uint32_t)(32 * warp) << 16) + c, v);
+    tc::wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) D[(32 * warp + lane) * 64 + c + j] = (int32_t)v[j];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 64);
+}
+}  // namespace
+}  // namespace bfmm
+
+extern "C" int bfmm_tc_i8_selftest(const int8_t *A, const int8_t *B, int K, int32_t *D,
+                                   bfmm_stream_t stream) {
+  if (K <= 0 || K % 32) {
+    set_error("bfmm_tc_i8_selftest: K=%d must be a positive multiple of 32", K);
+    return 2;
+  }
+  bfmm::tc_i8_selftest_kernel<<<1, 128, 0, as_stream(stream)>>>(A, B, K, D);
+  return check_launch("tc_i8_selftest_kernel");
 }
