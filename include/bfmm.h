@@ -162,6 +162,33 @@ int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m, int rp,
                         int nsplit, const int64_t *cells, const int64_t *oct_off,
                         const double *cores, bfmm_stream_t stream);
 
+/* Same translation on the int8 tensor cores (tcgen05.mma kind::i8, TMEM
+ * accumulators; csrc/m2l_i8.cuh), FP64-accurate by error-free splitting:
+ * z is cut into S signed 7-bit digit planes under one per-level power-of-two
+ * scale, the cores into S planes under one scale per rank row i, and the
+ * S(S+1)/2 digit products whose weights exceed 2^(-7S) are accumulated
+ * exactly in int32.  Same lt layout and meaning as bfmm_m2l_cheb /
+ * bfmm_m2l_cheb_cells (replaces engine.py:228-256, ops:217-237).
+ *  - bfmm_m2l_i8_slice_z: z (rows x rp, FP64, row = cell * m + column) ->
+ *    zs (bfmm_m2l_i8_zs_bytes bytes: [row][ceil(rp/32)][S][32] int8) and
+ *    zmax (device, m x 8 bytes: the bit pattern of max|z| per weight column,
+ *    the power-of-two scale of that column's digits).
+ *  - cs: core digits, [316][ceil(rp/64)][ceil(rp/32)][S][64 x 32 K-major
+ *    core-matrix image] int8; cpow: 2^(e_i) per rank row, ceil(rp/64)*64
+ *    doubles (built on the host, engine._i8_core_slices).
+ *  - S in 5..8, rp <= 256. */
+size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int S);
+int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int S,
+                        int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream);
+int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq);
+int bfmm_m2l_i8(const int8_t *zs, const unsigned long long *zmax, const int8_t *cs,
+                const double *cpow, double *lt, int level, int m, int rp, int S,
+                int nsplit, int64_t q_lo, int64_t nq, bfmm_stream_t stream);
+int bfmm_m2l_i8_cells(const int8_t *zs, const unsigned long long *zmax,
+                      const int8_t *cs, const double *cpow, double *lt, int level,
+                      int m, int rp, int S, int nsplit, const int64_t *cells,
+                      const int64_t *oct_off, bfmm_stream_t stream);
+
 /* M2L uniform / FFT (engine.py:258-292): locals[c] = scale * crop(
  * irfft( sum_t S_t * rfft(pad(moments[c + t])) ) ) over the valid far
  * offsets t.  symbols (device) (316, q, q, q//2+1) complex128 interleaved

@@ -42,6 +42,11 @@ SIGNATURES = {
     "bfmm_active_cells": (_I, [_P, _P, _I64, _I, _I64, _I64, _P, _SZ, _P, _P, _P]),
     "bfmm_m2l_cheb_splits": (_I, [_I, _I, _I, _I64]),
     "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _I64, _I64, _P, _P]),
+    "bfmm_m2l_i8_zs_bytes": (_SZ, [_I64, _I, _I]),
+    "bfmm_m2l_i8_slice_z": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P]),
+    "bfmm_m2l_i8_splits": (_I, [_I, _I, _I, _I64]),
+    "bfmm_m2l_i8": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _I64, _P]),
+    "bfmm_m2l_i8_cells": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "bfmm_device_dmma_probe": (_I, [_DP, _P]),
     "bfmm_tc_i8_selftest": (_I, [_P, _P, _I, _P, _P]),
     "bfmm_device_dmma_sweep": (_I, [_I, _I, _DP, _P]),

@@ -22,7 +22,7 @@ LIB = os.path.join(OUT_DIR, "libbfmm.so")
 OBJ_DIR = os.path.join(ROOT, "build", "obj")
 
 SOURCES = ["tree.cu", "interp.cu", "m2l_cheb.cu", "m2l_fft.cu", "p2p.cu", "misc.cu"]
-HEADERS = ["common.cuh", "p2p.cuh", "m2l_ws.cuh", "leaf_kernels.cuh", "transfer_kernels.cuh"]
+HEADERS = ["common.cuh", "p2p.cuh", "m2l_ws.cuh", "m2l_i8.cuh", "tcgen05.cuh", "leaf_kernels.cuh", "transfer_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace bfmm {
 namespace {
@@ -54,6 +55,10 @@ __global__ void reduce_splits_kernel(double *__restrict__ A, int64_t rows, int K
 // and, per child octant, the 189 of them its parity admits (in that order).
 __constant__ signed char c_offsets[316][3];
 __constant__ short c_valid[8][189];
+// offsets as dilated (Morton-interleaved) 10-bit two's-complement integers,
+// x / y / z in bit positions 3b+2 / 3b+1 / 3b: cell + t is one masked add
+// per axis for levels <= 10 (m2l_i8.cuh)
+__constant__ uint32_t c_dil[316][3];
 bool g_offsets_ready = false;
 
 void ensure_offsets() {
@@ -87,6 +92,11 @@ void ensure_offsets() {
   }
   cudaMemcpyToSymbol(c_offsets, h, sizeof(h));
   cudaMemcpyToSymbol(c_valid, v, sizeof(v));
+  uint32_t dl[316][3];
+  for (int t = 0; t < 316; ++t)
+    for (int a = 0; a < 3; ++a)
+      dl[t][a] = (uint32_t)(spread3((uint64_t)(h[t][a] & 1023)) << (2 - a));
+  cudaMemcpyToSymbol(c_dil, dl, sizeof(dl));
   g_offsets_ready = true;
 }
 
@@ -116,6 +126,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 #include "m2l_ws.cuh"
+#include "m2l_i8.cuh"
 
 // ----------------------------------------------------------------------------
 // Basis projections on the FP64 tensor cores: C = alpha * A @ B (+ beta C),
@@ -478,3 +489,114 @@ extern "C" int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m
   M2LCall a{z, lt, level, m, rp, nsplit, 0, 0, act, cores, as_stream(stream)};
   return dispatch_ws(m2l_mw(longest * m), m2l_nt8(rp), a);
 }
+
+// ---- int8 tensor-core M2L (m2l_i8.cuh) ----
+extern "C" size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int S) {
+  return (size_t)rows * ceil_div(rp, 32) * S * 32;
+}
+
+extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int S,
+                                   int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream) {
+  if (rp <= 0 || rp > 256 || S < 5 || S > 8 || rows < 0 || m < 1 || m > 65535 || rows % m) {
+    set_error("bfmm_m2l_i8_slice_z: rp=%d (1..256), S=%d (5..8), rows=%lld", rp, S,
+              (long long)rows);
+    return 2;
+  }
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(zmax, 0, sizeof(unsigned long long) * m, st);
+  if (rows == 0) return 0;
+  const int64_t n = rows / m * rp;
+  absmax_bits_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs), m), 256,
+                       0, st>>>(z, rows, rp, m, zmax);
+  if (check_launch("absmax_bits_kernel")) return 1;
+  const int kc_n = (int)ceil_div(rp, 32);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows * kc_n * 2, 256), 16 * kNumSMs);
+  switch (S) {
+    case 5: z_slice_kernel<5><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+    case 6: z_slice_kernel<6><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+    case 7: z_slice_kernel<7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+    default: z_slice_kernel<8><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+  }
+  return check_launch("z_slice_kernel");
+}
+
+extern "C" int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq) {
+  (void)level;
+  const int64_t ctas = ceil_div(nq * m, kI8TM) * ceil_div(rp, kI8TN) * 8;
+  const double slots = kNumSMs;  // one CTA per SM (TMEM 512 columns, ~215 KB smem)
+  if (ctas * 4 < slots) return (int)std::min<int64_t>(189, ceil_div(4 * (int64_t)slots, ctas));
+  int best = 1;
+  double best_score = -1e30;
+  for (int s = 1; s <= 16; ++s) {
+    const double waves = ctas * s / slots;
+    const double score = waves / std::ceil(waves) - 0.006 * s;
+    if (score > best_score + 1e-12) {
+      best_score = score;
+      best = s;
+    }
+  }
+  return best;
+}
+
+static int i8_check(const char *fn, int level, int m, int rp, int S, int nsplit) {
+  if (m < 1 || (int64_t(1) << (3 * level)) * m >= (int64_t(1) << 31)) {
+    set_error("%s: 8^%d cells x %d columns exceed the 32-bit row index", fn, level, m);
+    return 2;
+  }
+  if (rp % 8 != 0 || rp <= 0 || rp > 256 || level < 2 || level > 10 || S < 5 || S > 8) {
+    set_error("%s: rp=%d (multiple of 8, <= 256), level=%d, S=%d (5..8)", fn, rp, level, S);
+    return 2;
+  }
+  if (nsplit < 1 || nsplit > 189) {
+    set_error("%s: nsplit=%d outside [1, 189]", fn, nsplit);
+    return 2;
+  }
+  return 0;
+}
+
+extern "C" int bfmm_m2l_i8(const int8_t *zs, const unsigned long long *zmax, const int8_t *cs,
+                           const double *cpow, double *lt, int level, int m, int rp, int S,
+                           int nsplit, int64_t q_lo, int64_t nq, bfmm_stream_t stream) {
+  if (int rc = i8_check("bfmm_m2l_i8", level, m, rp, S, nsplit)) return rc;
+  const int64_t nparent = int64_t(1) << (3 * level - 3);
+  if (q_lo < 0 || nq < 0 || q_lo + nq > nparent) {
+    set_error("bfmm_m2l_i8: parent range [%lld, %lld) outside [0, %lld)", (long long)q_lo,
+              (long long)(q_lo + nq), (long long)nparent);
+    return 2;
+  }
+  ensure_offsets();
+  I8Call a{zs, zmax, cs, cpow, lt, level, m, rp, (int)ceil_div(rp, 32), (int)ceil_div(rp, kI8TN),
+           nsplit, q_lo, nq, OctList{nullptr, {}}, as_stream(stream)};
+  return dispatch_i8(S, a);
+}
+
+extern "C" int bfmm_m2l_i8_cells(const int8_t *zs, const unsigned long long *zmax,
+                                 const int8_t *cs, const double *cpow, double *lt, int level,
+                                 int m, int rp, int S, int nsplit, const int64_t *cells,
+                                 const int64_t *oct_off, bfmm_stream_t stream) {
+  if (int rc = i8_check("bfmm_m2l_i8_cells", level, m, rp, S, nsplit)) return rc;
+  OctList act{cells, {}};
+  for (int o = 0; o <= 8; ++o) {
+    act.off[o] = oct_off[o];
+    if (o > 0 && oct_off[o] < oct_off[o - 1]) {
+      set_error("bfmm_m2l_i8_cells: octant offsets not ascending");
+      return 2;
+    }
+  }
+  if (oct_off[8] > (int64_t(1) << (3 * level)) || (oct_off[8] > 0 && !cells)) {
+    set_error("bfmm_m2l_i8_cells: %lld listed cells invalid at level %d", (long long)oct_off[8],
+              level);
+    return 2;
+  }
+  if (oct_off[8] == 0) return 0;
+  ensure_offsets();
+  I8Call a{zs, zmax, cs, cpow, lt, level, m, rp, (int)ceil_div(rp, 32), (int)ceil_div(rp, kI8TN),
+           nsplit, 0, 0, act, as_stream(stream)};
+  return dispatch_i8(S, a);
+}
+
+#ifdef BFMM_I8_TRACE
+extern "C" int bfmm_i8_trace_read(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, bfmm::g_i8_trace, sizeof(long long) * 8192);
+}
+#endif

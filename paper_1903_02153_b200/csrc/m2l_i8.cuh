@@ -1,0 +1,426 @@
+// M2L (Chebyshev, engine.py:228-256) on the int8 tensor cores (tcgen05),
+// FP64-exact to ~2^-46 of the operand scales (included by m2l_cheb.cu).
+//
+// B200's tcgen05 has no FP64 kind, but it multiplies int8 at 4.5 POPS.  The
+// translation lt[c, i] = sum_{t in valid(o)} sum_k C_t[i, k] z[c + t, k] is
+// run as an error-free sum of int8 GEMMs (Ozaki-style splitting):
+//   z / 2^ez      = sum_a 2^(-6-7a) Za,  Za in [-64, 64]   (per level ez)
+//   C_t[i] / 2^ei = sum_b 2^(-6-7b) Cb,  Cb in [-64, 64]   (per rank row ei)
+// so  lt[c, i] = 2^(ez+ei) sum_{a+b<S} 2^(-12-7(a+b)) (Za Cb^T)[c, i]  plus a
+// truncation below 2^(-7S) of the scales.  Every int8 product Za Cb^T is
+// accumulated EXACTLY in int32 TMEM (|digit product| <= 2^12, K <= 189 * 256
+// and at most S products per accumulator stay below 2^31), pairs with the
+// same a + b share one accumulator, and only the S accumulators are
+// converted to FP64 at the end -- the result is bitwise independent of the
+// summation order.
+//
+// Tile: 128 target rows (cells of one child octant, or (cell, column) rows
+// when m > 1) x 64 rank rows.  Stage = one (offset, 32-wide k chunk): the
+// four producer warps gather the S digit planes of the 128 source rows
+// z[c + t] (zero-filled where c + t leaves the grid -- exactly the pairs
+// cell_pairs_for_offset omits, octree.py:202-221) and copy the matching
+// pre-sliced core block, all with cp.async into the K-major no-swizzle
+// layout the MMA descriptor reads; one elected thread issues the
+// S(S+1)/2 tcgen05.mma.kind::i8 per stage and releases the stage with
+// tcgen05.commit.  The same four warps then drain TMEM.
+#pragma once
+
+// tcgen05.cuh is included at file scope by m2l_cheb.cu
+
+constexpr int kI8TM = 128, kI8TN = 64;
+#ifdef BFMM_I8_TRACE
+__device__ long long g_i8_trace[8192];
+#endif
+constexpr int kI8Threads = 160;  // warp 0: TMEM + MMA issue; warps 1-4: producers/epilogue
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void mbar_spin(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nSPIN_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra SPIN_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global -> shared on the TMA engine, completing on *bar.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <int S>
+struct I8Shape {
+  static constexpr int A_SLICE = kI8TM * 32, B_SLICE = kI8TN * 32;
+  static constexpr int STAGE = S * (A_SLICE + B_SLICE);
+  static constexpr int NS = (S >= 8 ? 4 : (S >= 7 ? 5 : 6));
+  static constexpr int LAG = NS - 3;  // cp.async groups a producer keeps in flight
+  static constexpr size_t smem = (size_t)NS * STAGE + (2 * NS + 1) * 8 + 16;
+};
+
+template <int S>
+__global__ void __launch_bounds__(kI8Threads, 1)
+m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
+              const int8_t *__restrict__ cs, const double *__restrict__ cpow,
+              double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
+              int nsplit, int64_t q_lo, int64_t nq, OctList act) {
+  using Sh = I8Shape<S>;
+  constexpr int NS = Sh::NS;
+  extern __shared__ __align__(1024) uint8_t smi[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smi + NS * Sh::STAGE);
+  uint64_t *empty = full + NS;
+  uint64_t *done = empty + NS;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+  const int o = blockIdx.z & 7;
+  const int split = blockIdx.z >> 3;
+  const int per = (189 + nsplit - 1) / nsplit;
+  const int v_lo = split * per, v_hi = min(189, v_lo + per);
+  const int nt = blockIdx.y;
+  const int n = 1 << level;
+  const int64_t *ocells = act.cells ? act.cells + act.off[o] : nullptr;
+  const int64_t rows = (act.cells ? act.off[o + 1] - act.off[o] : nq) * m;
+  const int64_t row0 = int64_t(blockIdx.x) * kI8TM;
+  if (row0 >= rows) return;  // whole CTA
+  // (cell indices are 30-bit Morton codes: levels <= 10, checked by the caller)
+  const int nsteps = (v_hi - v_lo) * kc_n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (nsteps <= 0) {  // a split past the last offset: its lt block is zero
+    for (int e = threadIdx.x; e < kI8TM * kI8TN; e += kI8Threads) {
+      const int64_t r = row0 + e / kI8TN;
+      const int col = nt * kI8TN + e % kI8TN;
+      if (r >= rows || col >= rp) continue;
+      const int64_t q = r / m;
+      const int c = (int)(r - q * m);
+      const int64_t orow = ocells ? act.off[o] + q : 8 * (q_lo + q) + o;
+      lt[((orow * m + c) * nsplit + split) * rp + col] = 0.0;
+    }
+    return;
+  }
+
+  if (warp == 0) bfmm::tc::alloc(tmem_slot, 512);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 5);  // one arrival per producer warp + the bulk copy's expect_tx
+      mbar_init(&empty[s], 1);   // tcgen05.commit
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  bfmm::tc::fence_before();
+  __syncthreads();
+  bfmm::tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- MMA issue (warp 0, one elected lane) ----------------
+    // The whole warp runs the loop so the descriptors stay warp-uniform
+    // (uniform datapath, no per-MMA register -> uniform moves); a descriptor
+    // for smem address x + d is desc(x) + d / 16, so each MMA costs one add.
+    const uint64_t dbase = bfmm::tc::desc_kmajor(bfmm::tc::smem_u32(smi), 128, 256);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int step = 0; step < nsteps; ++step) {
+      if (lane == 0) mbar_wait(&full[s], ph);
+      __syncwarp();
+#ifdef BFMM_I8_TRACE
+      if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && step < 1024)
+        g_i8_trace[step] = clock64();
+#endif
+      bfmm::tc::fence_after();
+      const uint64_t dA = dbase + (uint64_t)((s * Sh::STAGE) >> 4);
+      const uint64_t dB = dA + (uint64_t)((S * Sh::A_SLICE) >> 4);
+      if (elect_one()) {
+        // pairs (a, b) with a + b < S: for fixed a the accumulators a + b of
+        // b = b0 .. b0 + nb - 1 are contiguous TMEM columns and the planes
+        // B_b contiguous smem rows, so ONE MMA with N = 64 nb covers them
+        // (N <= 256): 10 MMAs per stage at S = 7 instead of 28, and each A
+        // plane is read from shared memory once or twice instead of S - a times
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+#pragma unroll
+          for (int b0 = 0; b0 < S - a; b0 += 4) {
+            const int nb = min(4, S - a - b0);
+            // accumulators a + b are first written by a = 0 in step 0
+            bfmm::tc::mma_i8(tmem + (uint32_t)((a + b0) * kI8TN),
+                             dA + (uint64_t)((a * Sh::A_SLICE) >> 4),
+                             dB + (uint64_t)((b0 * Sh::B_SLICE) >> 4),
+                             bfmm::tc::idesc_i8(kI8TM, kI8TN * nb),
+                             (step > 0 || a > 0) ? 1u : 0u);
+          }
+        }
+        bfmm::tc::commit(&empty[s]);
+      }
+      __syncwarp();
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    if (elect_one()) bfmm::tc::commit(done);
+    __syncwarp();
+  } else {
+    // ---------------- producers: gather z digits + copy core digits ----------------
+    // thread p computes the source row of tile row p.  Its warp copies the
+    // S digit planes of its 32 rows: instruction (j, half) moves plane j
+    // (32 contiguous bytes = one sector per row) of 16 rows, lanes l and
+    // l + 16 taking the two 16-byte K halves -- 16 sectors per instruction and
+    // conflict-free shared-memory writes (bank group = row & 7).  The core
+    // block of the stage (S * 2 KB, contiguous in cs) is one bulk copy
+    // (TMA engine) issued by thread 32 and tracked by the same mbarrier.
+    const int p = threadIdx.x - 32;  // tile row 0..127
+    const int wrow = p & ~31;        // first tile row of this warp
+    const int64_t r = row0 + p;
+    const bool rok = r < rows;
+    int cx = 0, cy = 0, cz = 0, colm = 0;
+    uint32_t cd = 0;  // the row's cell as a 30-bit Morton code
+    if (rok) {
+      const int64_t q = r / m;
+      colm = (int)(r - q * m);
+      const int64_t cell = ocells ? ocells[q] : 8 * (q_lo + q) + o;
+      cd = (uint32_t)cell;
+      unmorton3((uint64_t)cell, cx, cy, cz);
+    }
+    constexpr uint32_t MX = 0x24924924u, MY = 0x12492492u, MZ = 0x09249249u;
+    const int hl = lane >> 4;  // K half of this lane
+    // this lane's shared-memory slot in a stage: row wrow + (lane & 15) (+ 16)
+    uint8_t *const dstA0 = smi + bfmm::tc::kmajor_off(wrow + (lane & 15), 16 * hl);
+    const int64_t rowbytes = (int64_t)kc_n * S * 32;
+    int s = 0, sl = 0, step = 0;
+    uint32_t ph = 0;
+    for (int vi = v_lo; vi < v_hi; ++vi) {
+      const int t = c_valid[o][vi];
+      // the octant's parity already admits t; only the grid bounds remain
+      const int sx = cx + c_offsets[t][0], sy = cy + c_offsets[t][1], sz = cz + c_offsets[t][2];
+      int srow = -1;
+      if (rok && (unsigned)sx < (unsigned)n && (unsigned)sy < (unsigned)n && (unsigned)sz < (unsigned)n) {
+        const uint32_t sc = (((cd | ~MX) + c_dil[t][0]) & MX) | (((cd | ~MY) + c_dil[t][1]) & MY) |
+                            (((cd | ~MZ) + c_dil[t][2]) & MZ);
+        srow = (int)sc * m + colm;
+      }
+      const int sr0 = __shfl_sync(0xffffffffu, srow, lane & 15);
+      const int sr1 = __shfl_sync(0xffffffffu, srow, 16 + (lane & 15));
+      const int8_t *src0 = zs + (sr0 >= 0 ? (int64_t)sr0 * rowbytes + 16 * hl : 0);
+      const int8_t *src1 = zs + (sr1 >= 0 ? (int64_t)sr1 * rowbytes + 16 * hl : 0);
+      const int8_t *bsrc = cs + ((int64_t)t * ntn + nt) * kc_n * (int64_t)(S * Sh::B_SLICE);
+      for (int kc = 0; kc < kc_n; ++kc, ++step) {
+        if (step >= NS) {  // one waiter per warp (mbarrier ops are per thread)
+          if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
+          __syncwarp();
+        }
+        uint8_t *sA = smi + s * Sh::STAGE;
+#ifdef BFMM_I8_TRACE
+        if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && step < 1024)
+          g_i8_trace[1024 * (1 + (p >> 5)) + step] = clock64();
+#endif
+        if (p == 0) {
+          mbar_expect_tx(&full[s], S * Sh::B_SLICE);
+          bulk_g2s(sA + S * Sh::A_SLICE, bsrc + kc * (S * Sh::B_SLICE), S * Sh::B_SLICE, &full[s]);
+        }
+        uint8_t *d0 = dstA0 + s * Sh::STAGE;
+        const int8_t *a0 = src0 + kc * (S * 32), *a1 = src1 + kc * (S * 32);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          cp_async16(d0 + j * Sh::A_SLICE, a0 + 32 * j, sr0 >= 0);
+          cp_async16(d0 + j * Sh::A_SLICE + 512, a1 + 32 * j, sr1 >= 0);
+        }
+        // stage step - LAG has landed for this thread once at most LAG newer
+        // groups are pending; the warp then arrives once (an arrival per
+        // thread would serialise 128 mbarrier operations per stage).  As in
+        // CUTLASS's sm100 cp.async + UMMA mainloop, the mbarrier completion
+        // orders the copies before the MMA's shared-memory reads.
+        cp_async_commit();
+        if (step >= Sh::LAG) {
+          cp_async_wait<Sh::LAG>();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[sl]);
+          if (++sl == NS) sl = 0;
+        }
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (lane == 0)
+      for (int k = max(0, nsteps - Sh::LAG); k < nsteps; ++k) mbar_arrive(&full[k % NS]);
+
+    // ---------------- epilogue: S int32 accumulators -> FP64 ----------------
+    mbar_wait(done, 0);
+    bfmm::tc::fence_after();
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+    const int er = 32 * quarter + lane;
+    const int64_t orr = row0 + er;
+    double *dst = nullptr;
+    double zsc = 0.0;
+    if (orr < rows) {
+      const int64_t q = orr / m;
+      const int c = (int)(orr - q * m);
+      const int64_t orow = ocells ? act.off[o] + q : 8 * (q_lo + q) + o;
+      dst = lt + ((orow * m + c) * nsplit + split) * rp;
+      const double amax = __longlong_as_double((long long)zmax[c]);
+      if (!(amax <= 1.7976931348623157e308)) {
+        zsc = __longlong_as_double(0x7ff8000000000000ll);  // non-finite z: NaN out
+      } else {
+        int ez = 0;
+        if (amax > 0) frexp(amax, &ez);
+        zsc = ldexp(1.0, ez - 12);
+      }
+    }
+    const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < kI8TN; c0 += 16) {
+      uint32_t acc[S][16];
+#pragma unroll
+      for (int d = 0; d < S; ++d) bfmm::tc::ld16(tl + d * kI8TN + c0, acc[d]);
+      bfmm::tc::wait_ld();
+      const int colb = nt * kI8TN + c0;
+      if (dst && colb < rp) {
+#pragma unroll
+        for (int jj = 0; jj < 16; jj += 2) {
+          double x2[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            double x = (double)(int32_t)acc[S - 1][jj + u];
+#pragma unroll
+            for (int d = S - 2; d >= 0; --d) x = fma(x, 0.0078125, (double)(int32_t)acc[d][jj + u]);
+            x2[u] = x * zsc * cpow[colb + jj + u];
+          }
+          if (colb + jj < rp)
+            *reinterpret_cast<double2 *>(dst + colb + jj) = make_double2(x2[0], x2[1]);
+        }
+      }
+    }
+  }
+  bfmm::tc::fence_before();
+  __syncthreads();
+  if (warp == 0) bfmm::tc::dealloc(tmem, 512);
+}
+
+// max |z| over n doubles as the bit pattern of a non-negative double
+// (order-preserving as an unsigned integer, so atomicMax is exact).
+__global__ void absmax_bits_kernel(const double *__restrict__ z, int64_t rows, int rp, int m,
+                                   unsigned long long *__restrict__ out) {
+  // block column blockIdx.y = weight column c: rows c, c + m, c + 2m, ...
+  const int c = blockIdx.y;
+  const int64_t nr = (rows - c + m - 1) / m;
+  const int64_t n = nr * rp;
+  unsigned long long mx = 0;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / rp;
+    const int k = (int)(e - i * rp);
+    const unsigned long long b =
+        (unsigned long long)__double_as_longlong(z[(c + i * m) * rp + k]) & 0x7fffffffffffffffull;
+    mx = b > mx ? b : mx;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, mx, s);
+    mx = o2 > mx ? o2 : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out + c, mx);
+}
+
+// z (rows x rp) -> S signed 7-bit digit planes, zs[row][kc][j][32]; digit j
+// of x is taken from x / 2^ez exactly, ez the exponent of the row's weight
+// column (row % m) -- every A row of the M2L gathers one column only, so a
+// per-column scale is a per-row scale of the GEMM and each right-hand side
+// is cut independently of the others (scalings by powers of two and
+// x - rint(x) are exact in FP64).  k >= rp is zero padding.
+template <int S>
+__global__ void z_slice_kernel(const double *__restrict__ z, int64_t rows, int rp, int kc_n,
+                               int m, const unsigned long long *__restrict__ zmax,
+                               int8_t *__restrict__ zs) {
+  const int64_t total = rows * kc_n * 2;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = e / (kc_n * 2);
+    const int rem = (int)(e - row * (kc_n * 2));
+    const int kc = rem >> 1, h = rem & 1;
+    const int k0 = kc * 32 + h * 16;
+    const double amax = __longlong_as_double((long long)zmax[row % m]);
+    int ez = 0;
+    if (amax > 0 && amax <= 1.7976931348623157e308) frexp(amax, &ez);
+    const double inv = ldexp(1.0, 6 - ez);  // first digit: x * 2^(6 - ez) in [-64, 64]
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int k = k0 + u;
+      const double v = k < rp ? z[row * rp + k] : 0.0;
+      x[u] = (v == v && fabs(v) <= 1.7976931348623157e308) ? v * inv : 0.0;
+    }
+    int8_t *dst = zs + ((row * kc_n + kc) * S) * 32 + 16 * h;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const double dg = rint(x[u]);
+        x[u] = (x[u] - dg) * 128.0;
+        w[u >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)dg) << (8 * (u & 3));
+      }
+      *reinterpret_cast<uint4 *>(dst + j * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+struct I8Call {
+  const int8_t *zs;
+  const unsigned long long *zmax;
+  const int8_t *cs;
+  const double *cpow;
+  double *lt;
+  int level, m, rp, kc_n, ntn, nsplit;
+  int64_t q_lo, nq;
+  OctList act;
+  cudaStream_t st;
+};
+
+template <int S>
+int launch_i8(const I8Call &a) {
+  using Sh = I8Shape<S>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(m2l_i8_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Sh::smem);
+    attr_set = true;
+  }
+  int64_t rows = a.nq * a.m;
+  if (a.act.cells) {
+    rows = 0;
+    for (int o = 0; o < 8; ++o) rows = std::max(rows, (a.act.off[o + 1] - a.act.off[o]) * a.m);
+  }
+  if (rows <= 0) return 0;
+  dim3 grid((unsigned)ceil_div(rows, kI8TM), (unsigned)a.ntn, 8 * a.nsplit);
+  m2l_i8_kernel<S><<<grid, kI8Threads, Sh::smem, a.st>>>(
+      a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, a.q_lo,
+      a.nq, a.act);
+  return check_launch("m2l_i8_kernel");
+}
+
+inline int dispatch_i8(int S, const I8Call &a) {
+  switch (S) {
+    case 5: return launch_i8<5>(a);
+    case 6: return launch_i8<6>(a);
+    case 7: return launch_i8<7>(a);
+    default: return launch_i8<8>(a);
+  }
+}

@@ -48,6 +48,30 @@ def _rank_interleave(rp: int) -> np.ndarray:
     return (k // 8) * 8 + 2 * (k % 4) + (k // 4) % 2
 
 
+def _i8_core_slices(CP: np.ndarray, S: int):
+    """Cores (316, rp, rp) [t][i][k] -> the digit planes bfmm_m2l_i8 reads
+    (csrc/m2l_i8.cuh): row i is scaled by 2^-e_i (e_i the exponent of
+    max_{t,k} |C_t[i, k]|) and cut into S signed 7-bit digits,
+    C_t[i, k] = 2^e_i sum_j 2^(-6-7j) D_j[t, i, k] + O(2^(e_i - 7S)), every
+    step exact in FP64.  Returns the int8 image
+    [t][i // 64][k // 32][j][64 x 32 K-major core matrices] and 2^e_i."""
+    T, rp, _ = CP.shape
+    kc, nt = -(-rp // 32), -(-rp // 64)
+    C = np.zeros((T, nt * 64, kc * 32))
+    C[:, :rp, :rp] = CP
+    amax = np.abs(C).max(axis=(0, 2))
+    e = np.where(amax > 0, np.frexp(amax)[1], 0).astype(np.int64)
+    x = C * np.ldexp(1.0, 6 - e)[None, :, None]
+    D = np.empty((S,) + C.shape, dtype=np.int8)
+    for j in range(S):
+        d = np.rint(x)
+        D[j] = d
+        x = (x - d) * 128.0
+    # [j][t][n][k] -> [t][n // 64][k // 32][j][n>>3 & 7][k>>4 & 1][n & 7][k & 15]
+    D = D.reshape(S, T, nt, 8, 8, kc, 2, 16).transpose(1, 2, 5, 0, 3, 6, 4, 7)
+    return np.ascontiguousarray(D), np.ldexp(1.0, e)
+
+
 @dataclass
 class _Tree:
     """A point set binned by leaf on the device (reference _Partition)."""
@@ -110,6 +134,11 @@ class FmmEvaluator:
         # sparse clouds (fewer than 8 points per leaf cell), per level only
         # where they cut the target rows below 3/4
         self.far_mode = "auto"
+        # Chebyshev M2L engine: FP64 tensor cores ("dmma", mma.sync f64) or
+        # the int8 tcgen05 tensor cores with error-free digit splitting
+        # ("i8", csrc/m2l_i8.cuh; i8_slices digits of 7 bits per operand)
+        self.m2l_mode = "i8"
+        self.i8_slices = 7
         # run the near field on a second stream, concurrent with the far
         # field.  Measured on C2 (B200): 4.95 -> 4.90 ms only -- the DMMA M2L
         # and the DFMA P2P contend for the same SMs -- so it is opt-in.
@@ -164,6 +193,57 @@ class FmmEvaluator:
                 sym = np.ascontiguousarray(blk.symbols).view(np.float64)
                 self._dev_blocks[key] = {"kind": "fft",
                                          "symbols": torch.from_numpy(sym.copy()).to(dev)}
+
+    def _i8_tables(self, blk, S):
+        key = ("i8", S)
+        if key not in blk:
+            torch = _torch()
+            cs, cpow = _i8_core_slices(blk["cores"].cpu().numpy(), S)
+            blk[key] = (torch.from_numpy(cs.reshape(-1)).to(self.device),
+                        torch.from_numpy(cpow).to(self.device))
+        return blk[key]
+
+    def _m2l_translate(self, z, lt, lev, m, rp, ns, blk, st, q_lo=0, nq=0, cells=None, off=None):
+        """lt = the 189-offset translation of z (engine.py:228-256), on the
+        engine self.m2l_mode selects; cells/off: listed active targets."""
+        torch = _torch()
+        if self.m2l_mode == "i8":
+            S = int(self.i8_slices)
+            cs, cpow = self._i8_tables(blk, S)
+            rows = z.numel() // rp
+            zs = torch.empty(int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, S)), dtype=torch.int8,
+                             device=self.device)
+            zmax = torch.empty(m, dtype=torch.int64, device=self.device)
+            _native.check(self.lib.bfmm_m2l_i8_slice_z(z.data_ptr(), rows, m, rp, S,
+                                                       zs.data_ptr(), zmax.data_ptr(), st),
+                          "bfmm_m2l_i8_slice_z")
+            e0 = self._kevent()
+            if cells is not None:
+                _native.check(self.lib.bfmm_m2l_i8_cells(
+                    zs.data_ptr(), zmax.data_ptr(), cs.data_ptr(), cpow.data_ptr(),
+                    lt.data_ptr(), lev, m, rp, S, ns, cells.data_ptr(), off.ctypes.data, st),
+                    "bfmm_m2l_i8_cells")
+            else:
+                _native.check(self.lib.bfmm_m2l_i8(
+                    zs.data_ptr(), zmax.data_ptr(), cs.data_ptr(), cpow.data_ptr(),
+                    lt.data_ptr(), lev, m, rp, S, ns, q_lo, nq, st), "bfmm_m2l_i8")
+            self._kspan(f"m2l_l{lev}", e0)
+            return
+        e0 = self._kevent()
+        if cells is not None:
+            _native.check(self.lib.bfmm_m2l_cheb_cells(
+                z.data_ptr(), lt.data_ptr(), lev, m, rp, ns, cells.data_ptr(),
+                off.ctypes.data, blk["cores"].data_ptr(), st), "bfmm_m2l_cheb_cells")
+        else:
+            _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
+                                                 q_lo, nq, blk["cores"].data_ptr(),
+                                                 st), "bfmm_m2l_cheb")
+        self._kspan(f"m2l_l{lev}", e0)
+
+    def _m2l_splits(self, lev, m, rp, nq):
+        if self.m2l_mode == "i8":
+            return int(self.lib.bfmm_m2l_i8_splits(lev, m, rp, nq))
+        return int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nq))
 
     def _dev_block(self, level):
         return self._dev_blocks[0] if self.table.single_level else self._dev_blocks[level]
@@ -367,7 +447,7 @@ class FmmEvaluator:
             cells, off, nact = active[lev]
             rp = blk["rp"]
             longest = int(np.max(off[1:] - off[:-1]))
-            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, max(longest, 1)))
+            ns = self._m2l_splits(lev, m, rp, max(longest, 1))
             z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((max(nact, 1) * m * ns * rp,), dtype=torch.float64,
                              device=self.device)
@@ -377,18 +457,14 @@ class FmmEvaluator:
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
                 shard[1].allgather_cells(z, m * rp, lev, shard[0])
-            e0 = self._kevent()
-            _native.check(self.lib.bfmm_m2l_cheb_cells(
-                z.data_ptr(), lt.data_ptr(), lev, m, rp, ns, cells.data_ptr(),
-                off.ctypes.data, blk["cores"].data_ptr(), st), "bfmm_m2l_cheb_cells")
-            self._kspan(f"m2l_l{lev}", e0)
+            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, cells=cells, off=off)
             if nact:
                 _native.check(self.lib.bfmm_rows_gemm_scatter(
                     lt.data_ptr(), nact * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
                     scale, 0.0, ns, cells.data_ptr(), m, st), "bfmm_rows_gemm_scatter(U)")
         elif blk["kind"] == "cheb":
             rp = blk["rp"]
-            ns = int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nq))
+            ns = self._m2l_splits(lev, m, rp, nq)
             z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
             _native.check(self.lib.bfmm_rows_gemm(
@@ -396,11 +472,7 @@ class FmmEvaluator:
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
                 shard[1].allgather_cells(z, m * rp, lev, shard[0])  # sources from every shard
-            e0 = self._kevent()
-            _native.check(self.lib.bfmm_m2l_cheb(z.data_ptr(), lt.data_ptr(), lev, m, rp, ns,
-                                                 q_lo, nq, blk["cores"].data_ptr(),
-                                                 st), "bfmm_m2l_cheb")
-            self._kspan(f"m2l_l{lev}", e0)
+            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq)
             _native.check(self.lib.bfmm_rows_gemm(
                 lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
                 out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")

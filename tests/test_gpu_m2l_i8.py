@@ -1,0 +1,107 @@
+"""The int8 tensor-core M2L (csrc/m2l_i8.cuh, m2l_mode "i8") against the
+FP64 tensor-core M2L (m2l_mode "dmma") and the reference fixtures.
+
+The i8 path is exact integer arithmetic on digit planes, so its error
+against FP64 is the digit truncation: about 2^(-7S) of the operand scales
+(S digits of 7 bits), and it is bitwise repeatable.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1903_02153_b200 as bf  # noqa: E402
+from paper_1903_02153_b200 import _native, workloads  # noqa: E402
+from paper_1903_02153_b200.engine import _i8_core_slices  # noqa: E402
+from paper_1903_02153_b200.kernel import workload_kernel  # noqa: E402
+
+PHI_TOL = 1e-10
+
+
+def _run_both(level, rp, m, S, ns, seed=0):
+    lib = _native.load()
+    st = _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    g = np.random.default_rng(seed)
+    ncell = 8 ** level
+    # rows of very different magnitude (as z of empty vs crowded cells)
+    z = g.standard_normal((ncell * m, rp)) * np.exp(g.uniform(-4, 0, (ncell * m, 1)))
+    cores = g.standard_normal((316, rp, rp)) * np.logspace(0, -7, rp)[None, :, None]
+    dz, dc = torch.from_numpy(z).cuda(), torch.from_numpy(cores).cuda()
+    nq = ncell // 8
+    ref = torch.zeros(ncell * m * rp, dtype=torch.float64, device="cuda")
+    _native.check(lib.bfmm_m2l_cheb(dz.data_ptr(), ref.data_ptr(), level, m, rp, 1, 0, nq,
+                                    dc.data_ptr(), st), "cheb")
+    cs, cpow = _i8_core_slices(cores, S)
+    dcs, dcp = torch.from_numpy(cs.reshape(-1)).cuda(), torch.from_numpy(cpow).cuda()
+    rows = ncell * m
+    zs = torch.empty(int(lib.bfmm_m2l_i8_zs_bytes(rows, rp, S)), dtype=torch.int8, device="cuda")
+    zmax = torch.empty(m, dtype=torch.int64, device="cuda")
+    _native.check(lib.bfmm_m2l_i8_slice_z(dz.data_ptr(), rows, m, rp, S, zs.data_ptr(),
+                                          zmax.data_ptr(), st), "slice")
+    outs = []
+    for _ in range(2):
+        lt = torch.full((rows * ns * rp,), float("nan"), dtype=torch.float64, device="cuda")
+        _native.check(lib.bfmm_m2l_i8(zs.data_ptr(), zmax.data_ptr(), dcs.data_ptr(),
+                                      dcp.data_ptr(), lt.data_ptr(), level, m, rp, S, ns, 0, nq,
+                                      st), "i8")
+        outs.append(lt)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]), "i8 M2L not bitwise repeatable"
+    got = outs[0].view(rows, ns, rp).sum(1).cpu().numpy()
+    return got, ref.view(rows, rp).cpu().numpy()
+
+
+@pytest.mark.parametrize("level,rp,m,S,ns", [(3, 56, 1, 7, 1), (3, 104, 1, 7, 3),
+                                             (3, 64, 3, 6, 2), (2, 168, 1, 8, 1),
+                                             (4, 56, 1, 5, 4), (2, 8, 2, 7, 189)])
+def test_i8_translation_matches_dmma(level, rp, m, S, ns):
+    got, ref = _run_both(level, rp, m, S, ns)
+    assert np.all(np.isfinite(got))
+    # per weight column (each has its own digit scale)
+    for c in range(m):
+        err = rel_l2(got[c::m], ref[c::m])
+        print(f"S={S} column {c}: rel-L2 {err:.3e}")
+        # digit truncation (one scale for rows spanning e^-4 costs ~6 bits)
+        # or the FP64 floor
+        assert err < max(2.0 ** (7 - 7 * S), 1e-14), (c, err)
+
+
+def test_i8_split_blocks_past_the_last_offset_are_zero():
+    # 189 offsets over 100 splits of 2: splits 95..99 have no offsets
+    got, ref = _run_both(2, 56, 1, 7, 100)
+    assert np.abs(got - ref).max() < 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2)])
+@pytest.mark.parametrize("mode,S", [("dmma", 7), ("i8", 6), ("i8", 8)])
+def test_m2l_engines_match_reference(name, scale, mode, S, cache_dir):
+    """Both M2L engines (and other digit counts than the default) meet the
+    phi bar against the reference fixtures."""
+    g = golden(f"{name.lower()}_s{scale}")
+    wl = workloads.make(name, scale)
+    plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"], eps=wl["eps"],
+                      domain_center=wl["center"], domain_length=wl["length"], n_cols=wl["ncols"])
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir=cache_dir)
+    ev.m2l_mode, ev.i8_slices = mode, S
+    phi = ev.evaluate(wl["points"], weights=wl["weights"])
+    idx = wl["check_idx"]
+    assert rel_l2(phi[idx], g["phi_idx"]) < PHI_TOL
+
+
+def test_i8_and_dmma_agree_on_c2_scaled(cache_dir):
+    wl = workloads.make("C2", 1)
+    plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], eps=wl["eps"],
+                      domain_center=wl["center"], domain_length=wl["length"])
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir=cache_dir)
+    res = {}
+    for mode in ("dmma", "i8"):
+        ev.m2l_mode = mode
+        res[mode] = ev.evaluate(wl["points"], weights=wl["weights"])
+    assert rel_l2(res["i8"], res["dmma"]) < 1e-12

@@ -176,3 +176,27 @@ def test_evaluator_refuses_kernels_without_device_form():
     k = bf.KernelSpec("hostonly", profile=np.exp)
     with pytest.raises(bf.ConfigurationError):
         bf.FmmEvaluator(k, bf.FmmPlan(levels=2, order=2))
+
+
+def test_i8_core_slices_reconstruct_the_cores():
+    """Host digit planes for the int8 M2L (engine._i8_core_slices): digits in
+    [-64, 64], and sum_j 2^(-6-7j) D_j * 2^e_i rebuilds C_t[i, k] to the
+    truncation 2^(1 - 7S) of the row scale."""
+    from paper_1903_02153_b200.engine import _i8_core_slices
+    g = np.random.default_rng(0)
+    rp = 104
+    C = g.standard_normal((316, rp, rp)) * np.logspace(0, -7, rp)[None, :, None]
+    C[:, 5] = 0.0  # an all-zero rank row
+    for S in (5, 7, 8):
+        D, cpow = _i8_core_slices(C, S)
+        assert D.dtype == np.int8 and D.min() >= -64 and D.max() <= 64
+        nt, kc = -(-rp // 64), -(-rp // 32)
+        assert D.shape == (316, nt, kc, S, 8, 2, 8, 16)
+        Dr = D.transpose(3, 0, 1, 4, 6, 2, 5, 7).reshape(S, 316, nt * 64, kc * 32)
+        rec = sum(Dr[j].astype(np.float64) * 2.0 ** (-6 - 7 * j) for j in range(S))
+        rec = rec * cpow[None, :, None]
+        scale = np.abs(C).max(axis=(0, 2))
+        err = np.abs(rec[:, :rp, :rp] - C).max(axis=(0, 2))
+        assert np.all(err <= 2.0 ** (1 - 7 * S) * scale)
+        assert np.all(rec[:, rp:, :] == 0) and np.all(rec[:, :, rp:] == 0)
+        assert cpow[5] == 1.0 and np.all(Dr[:, :, 5] == 0)
