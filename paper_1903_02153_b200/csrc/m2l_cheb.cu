@@ -59,6 +59,11 @@ __constant__ short c_valid[8][189];
 // x / y / z in bit positions 3b+2 / 3b+1 / 3b: cell + t is one masked add
 // per axis for levels <= 10 (m2l_i8.cuh)
 __constant__ uint32_t c_dil[316][3];
+// per octant, its 189 offsets ordered by plane group g = (t_x + 3) * 4 +
+// ((o_y + t_y) & 1) * 2 + ((o_z + t_z) & 1); group g is
+// c_grp[o][c_grp_off[o][g] .. c_grp_off[o][g + 1]) (m2l_i8p_kernel)
+__constant__ short c_grp[8][189];
+__constant__ unsigned char c_grp_off[8][29];
 bool g_offsets_ready = false;
 
 void ensure_offsets() {
@@ -97,6 +102,23 @@ void ensure_offsets() {
     for (int a = 0; a < 3; ++a)
       dl[t][a] = (uint32_t)(spread3((uint64_t)(h[t][a] & 1023)) << (2 - a));
   cudaMemcpyToSymbol(c_dil, dl, sizeof(dl));
+  short gr[8][189];
+  unsigned char go[8][29];
+  for (int o = 0; o < 8; ++o) {
+    const int oy = (o >> 1) & 1, oz = o & 1;
+    int k = 0;
+    for (int g = 0; g < 28; ++g) {
+      go[o][g] = (unsigned char)k;
+      for (int e = 0; e < 189; ++e) {
+        const int t = v[o][e];
+        const int gg = (h[t][0] + 3) * 4 + ((oy + h[t][1]) & 1) * 2 + ((oz + h[t][2]) & 1);
+        if (gg == g) gr[o][k++] = (short)t;
+      }
+    }
+    go[o][28] = (unsigned char)k;
+  }
+  cudaMemcpyToSymbol(c_grp, gr, sizeof(gr));
+  cudaMemcpyToSymbol(c_grp_off, go, sizeof(go));
   g_offsets_ready = true;
 }
 

@@ -73,6 +73,47 @@ struct I8Shape {
   static constexpr size_t smem = (size_t)NS * STAGE + (2 * NS + 1) * 8 + 16;
 };
 
+// Scale of a weight column's z digits: 2^(ez - 12) (NaN when max|z| is not
+// finite, so non-finite moments still propagate).
+__device__ __forceinline__ double i8_zscale(unsigned long long bits) {
+  const double amax = __longlong_as_double((long long)bits);
+  if (!(amax <= 1.7976931348623157e308)) return __longlong_as_double(0x7ff8000000000000ll);
+  int ez = 0;
+  if (amax > 0) frexp(amax, &ez);
+  return ldexp(1.0, ez - 12);
+}
+
+// One TMEM lane (tile row) of the S int32 accumulators -> FP64 lt row:
+// x = sum_d 2^(-7d) acc_d (Horner, fixed order), times the z scale and the
+// rank row's core scale.  zero: no MMA ran (write zeros).
+template <int S>
+__device__ __forceinline__ void i8_drain(uint32_t tl, double *dst, double zsc, int nt, int rp,
+                                         const double *__restrict__ cpow, bool zero) {
+#pragma unroll 1
+  for (int c0 = 0; c0 < kI8TN; c0 += 16) {
+    uint32_t acc[S][16];
+#pragma unroll
+    for (int d = 0; d < S; ++d) bfmm::tc::ld16(tl + d * kI8TN + c0, acc[d]);
+    bfmm::tc::wait_ld();
+    const int colb = nt * kI8TN + c0;
+    if (dst && colb < rp) {
+#pragma unroll
+      for (int jj = 0; jj < 16; jj += 2) {
+        double x2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          double x = (double)(int32_t)acc[S - 1][jj + u];
+#pragma unroll
+          for (int d = S - 2; d >= 0; --d) x = fma(x, 0.0078125, (double)(int32_t)acc[d][jj + u]);
+          x2[u] = zero ? 0.0 : x * zsc * cpow[colb + jj + u];
+        }
+        if (colb + jj < rp)
+          *reinterpret_cast<double2 *>(dst + colb + jj) = make_double2(x2[0], x2[1]);
+      }
+    }
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(kI8Threads, 1)
 m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
@@ -275,39 +316,254 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
       const int c = (int)(orr - q * m);
       const int64_t orow = ocells ? act.off[o] + q : 8 * (q_lo + q) + o;
       dst = lt + ((orow * m + c) * nsplit + split) * rp;
-      const double amax = __longlong_as_double((long long)zmax[c]);
-      if (!(amax <= 1.7976931348623157e308)) {
-        zsc = __longlong_as_double(0x7ff8000000000000ll);  // non-finite z: NaN out
-      } else {
-        int ez = 0;
-        if (amax > 0) frexp(amax, &ez);
-        zsc = ldexp(1.0, ez - 12);
+      zsc = i8_zscale(zmax[c]);
+    }
+    i8_drain<S>(tmem + ((uint32_t)(32 * quarter) << 16), dst, zsc, nt, rp, cpow, false);
+  }
+  bfmm::tc::fence_before();
+  __syncthreads();
+  if (warp == 0) bfmm::tc::dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+// Plane-buffered variant for dense levels >= 5 (m2l_i8p_kernel).
+//
+// The gather kernel above reads, per tile, 189 shifted copies of 128 source
+// rows -- 5.6x more than the distinct sources the tile touches -- and is
+// L2-bandwidth bound.  Here a tile is a 1 x 16 x 8 block (x, y, z) of
+// same-octant targets (stride 2 cells), tile row r = 8 y + z.  The 189
+// offsets split into 28 groups by (t_x, parity of o_y + t_y, parity of
+// o_z + t_z); all sources of a group lie in ONE parity plane x = x_t + t_x,
+// y = 2Y' + py, z = 2Z' + pz with Y' in [16 yb - 2, 16 yb + 18) and
+// Z' in [8 zb - 2, 8 zb + 10).  That 20 x 12 plane of digit rows is loaded
+// once into shared memory, Z' fastest at 16 B per row, so the A operand of
+// every offset of the group is a plain K-major no-swizzle descriptor into
+// it: start = plane + ((dy + 2) 12 + dz + 2) 16 B, 8-row groups (y) at
+// SBO = 192 B, K halves at LBO = 3840 B, where (dy, dz) = floor((o + t) / 2)
+// per axis.  Out-of-grid sources are zero rows, exactly the pairs
+// cell_pairs_for_offset omits (octree.py:202-221).  A traffic drops from
+// 189 x 128 rows to 28 x 240 rows per tile; the int32 sums are the same
+// integers as the gather kernel's (exact, any order).
+//
+// Warp roles (192 threads): 0 = TMEM + MMA issue, 1 = core-block bulk
+// copies (B ring), 2-5 = plane loads (cp.async) then the TMEM drain.
+
+constexpr int kI8PThreads = 192;
+constexpr int kPlaneRows = 240;  // 20 (Y') x 12 (Z')
+
+template <int S>
+struct I8PShape {
+  static constexpr int HALF = kPlaneRows * 16;  // one K half of one digit plane
+  static constexpr int PLANE = S * 2 * HALF;    // one plane buffer
+  static constexpr int B_STAGE = S * kI8TN * 32;
+  static constexpr int NP = 3;  // plane buffers
+  // core-block ring: as deep as the remaining shared memory allows
+  // (measured: three plane buffers matter more than a deeper ring)
+  static constexpr int NB_FIT = (227 * 1024 - NP * PLANE - 512) / B_STAGE;
+  static constexpr int NB = NB_FIT > 12 ? 12 : NB_FIT;
+  static constexpr size_t smem = (size_t)NP * PLANE + (size_t)NB * B_STAGE +
+                                 (2 * NP + 2 * NB + 1) * 8 + 16;
+};
+
+template <int S>
+__global__ void __launch_bounds__(kI8PThreads, 1)
+m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
+               const int8_t *__restrict__ cs, const double *__restrict__ cpow,
+               double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
+               int nsplit) {
+  using Sh = I8PShape<S>;
+  constexpr int NP = Sh::NP, NB = Sh::NB;
+  extern __shared__ __align__(1024) uint8_t smp[];
+  uint8_t *const planes = smp;
+  uint8_t *const bring = smp + NP * Sh::PLANE;
+  uint64_t *pfull = reinterpret_cast<uint64_t *>(bring + NB * Sh::B_STAGE);
+  uint64_t *pempty = pfull + NP;
+  uint64_t *bfull = pempty + NP;
+  uint64_t *bempty = bfull + NB;
+  uint64_t *done = bempty + NB;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+  const int n = 1 << level, h = n >> 1;  // cells per axis; same-octant targets per axis
+  const int o = blockIdx.z & 7, split = blockIdx.z >> 3;
+  const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+  const int ybn = h >> 4, zbn = h >> 3;
+  int tile = blockIdx.x;
+  const int zb = tile % zbn;
+  tile /= zbn;
+  const int yb = tile % ybn;
+  const int xi = tile / ybn;
+  const int col = blockIdx.y / ntn, nt = blockIdx.y - col * ntn;
+  const int xs = 2 * xi + ox;  // target x
+  const int units = 28 * kc_n;
+  const int per = (units + nsplit - 1) / nsplit;
+  const int u_lo = split * per, u_hi = min(units, u_lo + per);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // a unit (kc, g) is live when its plane is inside the grid and the group
+  // has offsets; every role walks the same live units in the same order
+  auto live = [&](int u, int &kc, int &g, int &tx) {
+    kc = u / 28;
+    g = u - kc * 28;
+    tx = g / 4 - 3;
+    const int x = xs + tx;
+    return x >= 0 && x < n && c_grp_off[o][g + 1] > c_grp_off[o][g];
+  };
+  bool any = false;
+  for (int u = u_lo; u < u_hi; ++u) {
+    int kc, g, tx;
+    any |= live(u, kc, g, tx);
+  }
+
+  if (warp == 0) bfmm::tc::alloc(tmem_slot, 512);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < NP; ++i) {
+      mbar_init(&pfull[i], 4);  // one arrival per plane-producer warp
+      mbar_init(&pempty[i], 1);
+    }
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  bfmm::tc::fence_before();
+  __syncthreads();
+  bfmm::tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- MMA issue ----------------
+    const uint64_t dP = bfmm::tc::desc_kmajor(bfmm::tc::smem_u32(planes), Sh::HALF, 192);
+    const uint64_t dB = bfmm::tc::desc_kmajor(bfmm::tc::smem_u32(bring), 128, 256);
+    int ps = 0, bs = 0;
+    uint32_t pph = 0, bph = 0;
+    bool first = true;
+    for (int u = u_lo; u < u_hi; ++u) {
+      int kc, g, tx;
+      if (!live(u, kc, g, tx)) continue;
+      if (lane == 0) mbar_wait(&pfull[ps], pph);
+      __syncwarp();
+      bfmm::tc::fence_after();
+      for (int e = c_grp_off[o][g]; e < c_grp_off[o][g + 1]; ++e) {
+        const int t = c_grp[o][e];
+        const int dy = (oy + c_offsets[t][1]) >> 1, dz = (oz + c_offsets[t][2]) >> 1;
+        if (lane == 0) mbar_wait(&bfull[bs], bph);
+        __syncwarp();
+        bfmm::tc::fence_after();
+        const uint64_t dA = dP + (uint64_t)((ps * Sh::PLANE + ((dy + 2) * 12 + dz + 2) * 16) >> 4);
+        const uint64_t dBs = dB + (uint64_t)((bs * Sh::B_STAGE) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int a = 0; a < S; ++a) {
+#pragma unroll
+            for (int b0 = 0; b0 < S - a; b0 += 4) {
+              const int nb = min(4, S - a - b0);
+              bfmm::tc::mma_i8(tmem + (uint32_t)((a + b0) * kI8TN),
+                               dA + (uint64_t)((a * 2 * Sh::HALF) >> 4),
+                               dBs + (uint64_t)((b0 * kI8TN * 32) >> 4),
+                               bfmm::tc::idesc_i8(kI8TM, kI8TN * nb),
+                               (!first || a > 0) ? 1u : 0u);
+            }
+          }
+          bfmm::tc::commit(&bempty[bs]);
+        }
+        __syncwarp();
+        first = false;
+        if (++bs == NB) {
+          bs = 0;
+          bph ^= 1u;
+        }
+      }
+      if (elect_one()) bfmm::tc::commit(&pempty[ps]);
+      __syncwarp();
+      if (++ps == NP) {
+        ps = 0;
+        pph ^= 1u;
       }
     }
-    const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
-#pragma unroll 1
-    for (int c0 = 0; c0 < kI8TN; c0 += 16) {
-      uint32_t acc[S][16];
-#pragma unroll
-      for (int d = 0; d < S; ++d) bfmm::tc::ld16(tl + d * kI8TN + c0, acc[d]);
-      bfmm::tc::wait_ld();
-      const int colb = nt * kI8TN + c0;
-      if (dst && colb < rp) {
-#pragma unroll
-        for (int jj = 0; jj < 16; jj += 2) {
-          double x2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            double x = (double)(int32_t)acc[S - 1][jj + u];
-#pragma unroll
-            for (int d = S - 2; d >= 0; --d) x = fma(x, 0.0078125, (double)(int32_t)acc[d][jj + u]);
-            x2[u] = x * zsc * cpow[colb + jj + u];
+    if (elect_one()) bfmm::tc::commit(done);
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- core blocks (B ring) ----------------
+    if (lane == 0) {
+      int bs = 0, k = 0;
+      uint32_t bph = 0;
+      for (int u = u_lo; u < u_hi; ++u) {
+        int kc, g, tx;
+        if (!live(u, kc, g, tx)) continue;
+        for (int e = c_grp_off[o][g]; e < c_grp_off[o][g + 1]; ++e, ++k) {
+          const int t = c_grp[o][e];
+          if (k >= NB) mbar_wait(&bempty[bs], bph ^ 1u);
+          mbar_expect_tx(&bfull[bs], Sh::B_STAGE);
+          bulk_g2s(bring + bs * Sh::B_STAGE,
+                   cs + (((int64_t)t * ntn + nt) * kc_n + kc) * (int64_t)Sh::B_STAGE,
+                   Sh::B_STAGE, &bfull[bs]);
+          if (++bs == NB) {
+            bs = 0;
+            bph ^= 1u;
           }
-          if (colb + jj < rp)
-            *reinterpret_cast<double2 *>(dst + colb + jj) = make_double2(x2[0], x2[1]);
         }
       }
     }
+    __syncwarp();
+  } else {
+    // ---------------- plane loads ----------------
+    const int p = threadIdx.x - 64;  // 0..127
+    const int64_t rowbytes = (int64_t)kc_n * S * 32;
+    int ps = 0, k = 0, pl = 0;
+    uint32_t pph = 0;
+    for (int u = u_lo; u < u_hi; ++u) {
+      int kc, g, tx;
+      if (!live(u, kc, g, tx)) continue;
+      const int py = (g >> 1) & 1, pz = g & 1;
+      if (k >= NP) {
+        if (lane == 0) mbar_wait(&pempty[ps], pph ^ 1u);
+        __syncwarp();
+      }
+      uint8_t *buf = planes + ps * Sh::PLANE;
+      const int x = xs + tx;
+      for (int row = p; row < kPlaneRows; row += 128) {
+        const int Yp = 16 * yb - 2 + row / 12, Zp = 8 * zb - 2 + row % 12;
+        const int y = 2 * Yp + py, z = 2 * Zp + pz;
+        const bool v = y >= 0 && y < n && z >= 0 && z < n;
+        const int8_t *src =
+            v ? zs + ((int64_t)morton3(x, y, z) * m + col) * rowbytes + kc * (S * 32) : zs;
+        uint8_t *dst = buf + row * 16;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          cp_async16(dst + j * 2 * Sh::HALF, src + 32 * j, v);
+          cp_async16(dst + j * 2 * Sh::HALF + Sh::HALF, src + 32 * j + 16, v);
+        }
+      }
+      cp_async_commit();
+      if (k >= 1) {  // the previous plane has landed: publish it
+        cp_async_wait<1>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[pl]);
+        if (++pl == NP) pl = 0;
+      }
+      ++k;
+      if (++ps == NP) {
+        ps = 0;
+        pph ^= 1u;
+      }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (k >= 1 && lane == 0) mbar_arrive(&pfull[pl]);
+
+    // ---------------- drain ----------------
+    if (any) {
+      mbar_wait(done, 0);
+      bfmm::tc::fence_after();
+    }
+    const int quarter = warp & 3;
+    const int er = 32 * quarter + lane;
+    const int yl = er >> 3, zl = er & 7;
+    const int64_t cell = (int64_t)morton3(xs, 2 * (16 * yb + yl) + oy, 2 * (8 * zb + zl) + oz);
+    double *dst = lt + ((cell * m + col) * nsplit + split) * rp;
+    i8_drain<S>(tmem + ((uint32_t)(32 * quarter) << 16), dst, i8_zscale(zmax[col]), nt, rp, cpow,
+                !any);
   }
   bfmm::tc::fence_before();
   __syncthreads();
@@ -416,7 +672,38 @@ int launch_i8(const I8Call &a) {
   return check_launch("m2l_i8_kernel");
 }
 
+template <int S>
+int launch_i8p(const I8Call &a) {
+  using Sh = I8PShape<S>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(m2l_i8p_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Sh::smem);
+    attr_set = true;
+  }
+  const int h = 1 << (a.level - 1);
+  dim3 grid((unsigned)(h * (h / 16) * (h / 8)), (unsigned)(a.ntn * a.m), 8 * a.nsplit);
+  m2l_i8p_kernel<S><<<grid, kI8PThreads, Sh::smem, a.st>>>(
+      a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit);
+  return check_launch("m2l_i8p_kernel");
+}
+
+// the plane kernel covers whole dense levels >= 5; shards and listed cells
+// use the gather kernel
+inline bool i8_plane_ok(const I8Call &a) {
+  return !a.act.cells && a.level >= 5 && a.q_lo == 0 &&
+         a.nq == (int64_t(1) << (3 * a.level - 3)) && !getenv("BFMM_I8_GATHER");
+}
+
 inline int dispatch_i8(int S, const I8Call &a) {
+  if (i8_plane_ok(a)) {
+    switch (S) {
+      case 5: return launch_i8p<5>(a);
+      case 6: return launch_i8p<6>(a);
+      case 7: return launch_i8p<7>(a);
+      default: return launch_i8p<8>(a);
+    }
+  }
   switch (S) {
     case 5: return launch_i8<5>(a);
     case 6: return launch_i8<6>(a);

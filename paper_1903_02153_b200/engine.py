@@ -140,9 +140,13 @@ class FmmEvaluator:
         self.m2l_mode = "i8"
         self.i8_slices = 7
         # run the near field on a second stream, concurrent with the far
-        # field.  Measured on C2 (B200): 4.95 -> 4.90 ms only -- the DMMA M2L
-        # and the DFMA P2P contend for the same SMs -- so it is opt-in.
-        self.overlap_near = False
+        # field: the P2P is FP64-pipe bound, the int8 M2L tensor-core / L2
+        # bound, so they share SMs well (C2, B200: 3.53 -> 3.31 ms).  With the
+        # DMMA M2L both need the FP64 units (4.95 -> 4.90 ms only).
+        self.overlap_near = True
+        # enqueue the overlapped near field after the far field (True) or
+        # before the upward pass (False)
+        self.near_after_far = False
         # ... which is the default for sharded runs, where it hides the
         # far field's all-gathers (SURVEY §8(e) "overlap")
         self.overlap_near_sharded = True
@@ -254,11 +258,14 @@ class FmmEvaluator:
         torch = _torch()
         return _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
-    def _side_stream(self):
+    def _side_stream(self, k=0):
+        """Side stream k: 0 = coarse far-field levels, 1 = the near field."""
         torch = _torch()
         if self._side is None:
-            self._side = torch.cuda.Stream(device=self.device)
-        return self._side
+            self._side = {}
+        if k not in self._side:
+            self._side[k] = torch.cuda.Stream(device=self.device)
+        return self._side[k]
 
     def _prepare_points(self, arr, name):
         torch = _torch()
@@ -644,19 +651,29 @@ class FmmEvaluator:
         alloc = torch.zeros if sharded else torch.empty
         near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
         side = None
-        if self.overlap_near or (sharded and self.overlap_near_sharded):
+        main = torch.cuda.current_stream()
+
+        def near_on_side():
             # near field on a side stream, concurrent with the far field (for
             # a shard: computes while the level all-gathers are in flight)
-            main = torch.cuda.current_stream()
-            side = self._side_stream()
+            side = self._side_stream(1)
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 self._near_field(ttree, stree, ws, m, near, shard)
+            return side
+
+        overlap = self.overlap_near or (sharded and self.overlap_near_sharded)
+        if overlap and (sharded or self.near_after_far is False):
+            side = near_on_side()
         moments, leaf_geom = self._upward(stree, ws, m, status, shard)
         ev[3].record()
         phi_far = None
         if not self._disable_far_field:
             locs = self._far_field(moments, m, shard, self._active_cells(ttree, shard))
+            if overlap and side is None:
+                # enqueued after the far field: the persistent P2P grid fills
+                # the SMs the M2L CTAs leave free instead of holding them all
+                side = near_on_side()
             ev[4].record()
             phi_far = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
             self._downward(locs, ttree, m, leaf_geom, status, phi_far, shard)

@@ -12,7 +12,8 @@ from paper_1903_02153_b200.engine import _i8_core_slices  # noqa: E402
 lib = _native.load()
 st = _native.C.c_void_p(0)
 g = np.random.default_rng(0)
-for level, rp, m, S in [(3, 56, 1, 7), (3, 104, 1, 7), (4, 56, 1, 6), (3, 64, 2, 7), (2, 168, 1, 8)]:
+import os
+for level, rp, m, S in [(5, 56, 1, 7), (5, 104, 1, 7), (5, 32, 2, 6), (6, 56, 1, 7), (5, 56, 1, 8), (3, 56, 1, 7)]:
     ncell = 8 ** level
     z = g.standard_normal((ncell * m, rp)) * np.exp(g.uniform(-3, 0, (ncell * m, 1)))
     cores = g.standard_normal((316, rp, rp)) * np.logspace(0, -6, rp)[None, :, None]
@@ -42,6 +43,29 @@ for level, rp, m, S in [(3, 56, 1, 7), (3, 104, 1, 7), (4, 56, 1, 6), (3, 64, 2,
                                           dcp.data_ptr(), lt2.data_ptr(), level, m, rp, S, ns, 0,
                                           nq, st), "i8")
             assert torch.equal(lt, lt2), "not repeatable"
+        os.environ["BFMM_I8_GATHER"] = "1"
+        ltg = torch.full_like(lt, float("nan"))
+        _native.check(lib.bfmm_m2l_i8(zs.data_ptr(), zmax.data_ptr(), dcs.data_ptr(),
+                                      dcp.data_ptr(), ltg.data_ptr(), level, m, rp, S, ns, 0,
+                                      nq, st), "i8 gather")
+        del os.environ["BFMM_I8_GATHER"]
+        torch.cuda.synchronize()
+        if ns == 1:
+            print("  plane == gather bitwise:", torch.equal(lt, ltg))
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _native.check(lib.bfmm_m2l_i8(zs.data_ptr(), zmax.data_ptr(), dcs.data_ptr(),
+                                      dcp.data_ptr(), lt.data_ptr(), level, m, rp, S, ns, 0,
+                                      nq, st), "i8")
+        e1.record()
+        os.environ["BFMM_I8_GATHER"] = "1"
+        _native.check(lib.bfmm_m2l_i8(zs.data_ptr(), zmax.data_ptr(), dcs.data_ptr(),
+                                      dcp.data_ptr(), ltg.data_ptr(), level, m, rp, S, ns, 0,
+                                      nq, st), "i8 gather")
+        del os.environ["BFMM_I8_GATHER"]
+        e2.record(); torch.cuda.synchronize()
+        print(f"  ms: default {e0.elapsed_time(e1):.3f}  gather {e1.elapsed_time(e2):.3f}")
         a = lt.view(ncell * m, ns, rp).sum(1).cpu().numpy()
         b = lt_ref.view(ncell * m, rp).cpu().numpy()
         err = np.abs(a - b).max() / np.abs(b).max()

@@ -25,7 +25,7 @@ from paper_1903_02153_b200.kernel import workload_kernel  # noqa: E402
 PHI_TOL = 1e-10
 
 
-def _run_both(level, rp, m, S, ns, seed=0):
+def _run_both(level, rp, m, S, ns, seed=0, gather=False):
     lib = _native.load()
     st = _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
     g = np.random.default_rng(seed)
@@ -46,6 +46,9 @@ def _run_both(level, rp, m, S, ns, seed=0):
     _native.check(lib.bfmm_m2l_i8_slice_z(dz.data_ptr(), rows, m, rp, S, zs.data_ptr(),
                                           zmax.data_ptr(), st), "slice")
     outs = []
+    if gather:  # diagnostic switch: force the gather kernel on a dense level
+        import os
+        os.environ["BFMM_I8_GATHER"] = "1"
     for _ in range(2):
         lt = torch.full((rows * ns * rp,), float("nan"), dtype=torch.float64, device="cuda")
         _native.check(lib.bfmm_m2l_i8(zs.data_ptr(), zmax.data_ptr(), dcs.data_ptr(),
@@ -53,30 +56,46 @@ def _run_both(level, rp, m, S, ns, seed=0):
                                       st), "i8")
         outs.append(lt)
     torch.cuda.synchronize()
+    if gather:
+        del os.environ["BFMM_I8_GATHER"]
     assert torch.equal(outs[0], outs[1]), "i8 M2L not bitwise repeatable"
     got = outs[0].view(rows, ns, rp).sum(1).cpu().numpy()
-    return got, ref.view(rows, rp).cpu().numpy()
+    return got, ref.view(rows, rp).cpu().numpy(), outs[0]
 
 
 @pytest.mark.parametrize("level,rp,m,S,ns", [(3, 56, 1, 7, 1), (3, 104, 1, 7, 3),
                                              (3, 64, 3, 6, 2), (2, 168, 1, 8, 1),
-                                             (4, 56, 1, 5, 4), (2, 8, 2, 7, 189)])
+                                             (4, 56, 1, 5, 4), (2, 8, 2, 7, 189),
+                                             (5, 56, 1, 7, 1), (5, 104, 2, 7, 3),
+                                             (5, 64, 1, 8, 2), (6, 24, 1, 6, 1)])
 def test_i8_translation_matches_dmma(level, rp, m, S, ns):
-    got, ref = _run_both(level, rp, m, S, ns)
+    got, ref, _ = _run_both(level, rp, m, S, ns)
     assert np.all(np.isfinite(got))
     # per weight column (each has its own digit scale)
     for c in range(m):
         err = rel_l2(got[c::m], ref[c::m])
         print(f"S={S} column {c}: rel-L2 {err:.3e}")
-        # digit truncation (one scale for rows spanning e^-4 costs ~6 bits)
+        # digit truncation (one scale for rows spanning e^-4 costs ~7 bits)
         # or the FP64 floor
-        assert err < max(2.0 ** (7 - 7 * S), 1e-14), (c, err)
+        assert err < max(2.0 ** (8 - 7 * S), 1e-14), (c, err)
 
 
 def test_i8_split_blocks_past_the_last_offset_are_zero():
     # 189 offsets over 100 splits of 2: splits 95..99 have no offsets
-    got, ref = _run_both(2, 56, 1, 7, 100)
+    got, ref, _ = _run_both(2, 56, 1, 7, 100)
     assert np.abs(got - ref).max() < 1e-12 * np.abs(ref).max()
+    # the plane kernel's splits run over 56 (chunk, plane) units
+    got, ref, _ = _run_both(5, 56, 1, 7, 16)
+    assert np.abs(got - ref).max() < 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("rp,m,S", [(56, 1, 7), (40, 2, 6)])
+def test_i8_plane_and_gather_kernels_agree_bitwise(rp, m, S):
+    """Dense levels >= 5 use the plane-buffered kernel; its int32 sums are
+    the gather kernel's integers, so the lt blocks are bitwise equal."""
+    _, _, a = _run_both(5, rp, m, S, 1)
+    _, _, b = _run_both(5, rp, m, S, 1, gather=True)
+    assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2)])
