@@ -221,6 +221,42 @@ def m2l_flops(ev, wl):
     return out
 
 
+def _valid_offsets(o):
+    """The 189 offsets a child octant admits (octree.py:128-145 parity rule)."""
+    from paper_1903_02153_b200.tables import OFFSETS
+    bits = ((o >> 2) & 1, (o >> 1) & 1, o & 1)
+    out = []
+    for t in OFFSETS:
+        if all(not ((int(t[a]) == 3 and bits[a]) or (int(t[a]) == -3 and not bits[a]))
+               for a in range(3)):
+            out.append(tuple(int(x) for x in t))
+    return out
+
+
+def m2l_i8_ops(lev, rp, m, S):
+    """int8 operations the tcgen05 M2L executes at one level: per (tile,
+    offset, 32-wide k chunk, 64-wide rank tile) stage, S(S+1)/2 digit
+    products of 128 x 64 x 32 (csrc/m2l_i8.cuh).  Dense levels >= 5 use the
+    plane kernel, which skips offsets whose source plane leaves the grid;
+    the gather kernel runs all 189 (zero rows)."""
+    n = 1 << lev
+    kc, ntn = -(-rp // 32), -(-rp // 64)
+    per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
+    if lev >= 5:
+        h = n // 2
+        stages = 0
+        for o in range(8):
+            ox = (o >> 2) & 1
+            offs = _valid_offsets(o)
+            for xi in range(h):
+                xs = 2 * xi + ox
+                live = sum(1 for t in offs if 0 <= xs + t[0] < n)
+                stages += live * (h // 16) * (h // 8)
+    else:
+        stages = -(-(n ** 3 // 8 * m) // 128) * 8 * 189
+    return stages * kc * ntn * m * per_stage if lev >= 5 else stages * kc * ntn * per_stage
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
     import torch
@@ -260,7 +296,6 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step(X, W)
     torch.cuda.synchronize()
-    ev.profile_kernels = True
     clocks = ClockSampler(local_rank)
     clocks.start()
     if dist is not None:
@@ -277,7 +312,6 @@ def run_ours(args, rank, world, local_rank):
         e1.record()
         e1.synchronize()
         spans.append(e0.elapsed_time(e1))
-        kms.append(dict(ev.kernel_ms))
         for k, v in ev.timings.items():
             if isinstance(v, float):
                 stage_sum[k] = stage_sum.get(k, 0.0) + v
@@ -286,8 +320,19 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
-    ev.profile_kernels = False
     total_ms = float(sum(spans))
+    # per-kernel times for the roofline: a separate pass with CUDA events
+    # around each launch on its own stream, near field NOT overlapped (the
+    # timed steps above overlap it with the far field, which would charge
+    # the SM sharing to both kernels)
+    ov = ev.overlap_near
+    ev.overlap_near, ev.profile_kernels = False, True
+    for _ in range(args.steps):
+        flush.zero_()
+        step(X, W)
+        torch.cuda.synchronize()
+        kms.append(dict(ev.kernel_ms))
+    ev.overlap_near, ev.profile_kernels = ov, False
     if dist is not None:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -349,7 +394,8 @@ def run_ours(args, rank, world, local_rank):
             lev = int(dom.split("_l")[1])
             flops = m2l_flops(ev, wl)[lev]
             peak = dmma_tf
-            roof = {"kernel": f"m2l level {lev} (DMMA implicit GEMM)", "bound": "fp64-tensor"}
+            roof = {"kernel": f"m2l level {lev} ({ev.m2l_mode} implicit GEMM)",
+                    "bound": "fp64-tensor"}
         achieved = flops / (ms * 1e-3) / 1e12
         roof.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": committed_traffic(args.config, dom),
@@ -360,6 +406,29 @@ def run_ours(args, rank, world, local_rank):
     kernels = {k: round(v, 4) for k, v in sorted(avg.items())}
     m2l_frac = {k: (m2l[int(k.split("_l")[1])] / (v * 1e-3) / 1e12) / dmma_tf
                 for k, v in avg.items() if k.startswith("m2l_l")}
+    # the int8 tensor-core M2L against its own roofline: executed int8 ops
+    # per launch / launch time vs the measured tcgen05 kind::i8 peak
+    m2l_roof = None
+    if ev.m2l_mode == "i8" and wl["scheme"] == "chebyshev":
+        i8_peak = C.c_double(0)
+        lib.bfmm_device_i8_probe(C.byref(i8_peak), stream)
+        S = int(ev.i8_slices)
+        m2l_roof = {"engine": f"int8 tcgen05, {S} digits per operand",
+                    "peak_int8_tops": i8_peak.value,
+                    "peak_source": "measured live: bfmm_device_i8_probe (128x256x32 MMAs "
+                                   "back to back)", "levels": {}}
+        for k, v in avg.items():
+            if not k.startswith("m2l_l"):
+                continue
+            lev = int(k.split("_l")[1])
+            rp = ev._dev_block(lev)["rp"]
+            ops = m2l_i8_ops(lev, rp, m, S)
+            fp64 = m2l[lev] / (v * 1e-3) / 1e12
+            m2l_roof["levels"][k] = {
+                "ms": round(v, 4), "kernel": "plane" if lev >= 5 else "gather",
+                "int8_tops": ops / (v * 1e-3) / 1e12,
+                "frac_int8_peak": ops / (v * 1e-3) / 1e12 / i8_peak.value,
+                "fp64_equiv_tflops": fp64, "frac_of_dmma_peak": fp64 / dmma_tf}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -382,6 +451,7 @@ def run_ours(args, rank, world, local_rank):
         "stages_ms": {k: round(1e3 * v / args.steps, 4) for k, v in stage_sum.items()},
         "kernels_ms": kernels,
         "m2l_frac_of_dmma_peak": {k: round(v, 3) for k, v in m2l_frac.items()},
+        "m2l_roofline": m2l_roof,
         "fp64_peaks_tflops": {"dfma": dfma_tf, "dmma": dmma_tf},
     }
     print(json.dumps(line), flush=True)

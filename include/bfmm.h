@@ -349,6 +349,11 @@ int bfmm_device_dmma_probe(double *gflops, bfmm_stream_t stream);
 int bfmm_tc_i8_selftest(const int8_t *A, const int8_t *B, int K, int32_t *D,
                         bfmm_stream_t stream);
 
+/* Dense int8 tensor-core throughput (tcgen05.mma kind::i8, 128 x 256 x 32
+ * MMAs back to back from shared memory, one CTA per SM) in TOPS: the peak
+ * the int8 M2L (bfmm_m2l_i8) is measured against. */
+int bfmm_device_i8_probe(double *tops, bfmm_stream_t stream);
+
 /* DMMA throughput with warps_per_sm resident warps x `chains` independent
  * accumulator chains (microarchitecture sweep behind the M2L tiling). */
 int bfmm_device_dmma_sweep(int warps_per_sm, int chains, double *gflops,

@@ -273,3 +273,70 @@ extern "C" int bfmm_tc_i8_selftest(const int8_t *A, const int8_t *B, int K, int3
   bfmm::tc_i8_selftest_kernel<<<1, 128, 0, as_stream(stream)>>>(A, B, K, D);
   return check_launch("tc_i8_selftest_kernel");
 }
+
+// ---- tcgen05 kind::i8 throughput probe: back-to-back 128 x N x 32 MMAs ----
+namespace bfmm {
+namespace {
+template <int N>
+__global__ void __launch_bounds__(128, 1) tc_i8_probe_kernel(int iters, int32_t *sink) {
+  __shared__ __align__(1024) int8_t sA[128 * 32];
+  __shared__ __align__(1024) int8_t sB[N * 32];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t mbar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < 128 * 32; e += 128) sA[e] = (int8_t)(e & 7);
+  for (int e = tid; e < N * 32; e += 128) sB[e] = (int8_t)(e & 3);
+  if (warp == 0) tc::alloc(&tmem_base, 512);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint64_t da = tc::desc_kmajor(tc::smem_u32(sA), 128, 256);
+    const uint64_t db = tc::desc_kmajor(tc::smem_u32(sB), 128, 256);
+    const uint32_t idesc = tc::idesc_i8(128, N);
+    for (int i = 0; i < iters; ++i) tc::mma_i8(tmem + (uint32_t)((i & 1) * N), da, db, idesc, 1u);
+    tc::commit(&mbar);
+  }
+  if (warp == 0) {  // tcgen05.ld is warp-collective
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n" ::"r"(
+            tc::smem_u32(&mbar))
+        : "memory");
+    tc::fence_after();
+    uint32_t v[16];
+    tc::ld16(tmem, v);
+    tc::wait_ld();
+    if (v[0] == 0x7fffffffu) sink[blockIdx.x] = (int32_t)v[1];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 512);
+}
+}  // namespace
+}  // namespace bfmm
+
+extern "C" int bfmm_device_i8_probe(double *tops, bfmm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  int32_t *sink = nullptr;
+  if (cudaMalloc(&sink, 4096 * sizeof(int32_t)) != cudaSuccess) {
+    set_error("bfmm_device_i8_probe: cudaMalloc failed");
+    return 1;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int iters = 1 << 14;
+  float ms = best_ms([&] { bfmm::tc_i8_probe_kernel<256><<<sms, 128, 0, st>>>(iters, sink); }, st);
+  cudaFree(sink);
+  if (check_launch("tc_i8_probe_kernel")) return 1;
+  const double ops = 2.0 * 128 * 256 * 32 * double(iters) * sms;
+  *tops = ops / (ms * 1e-3) / 1e12;
+  return 0;
+}
