@@ -86,30 +86,31 @@ __device__ __forceinline__ double i8_zscale(unsigned long long bits) {
 // One TMEM lane (tile row) of the S int32 accumulators -> FP64 lt row:
 // x = sum_d 2^(-7d) acc_d (Horner, fixed order), times the z scale and the
 // rank row's core scale.  zero: no MMA ran (write zeros).
-template <int S>
+template <int S, int W>
 __device__ __forceinline__ void i8_drain(uint32_t tl, double *dst, double zsc, int nt, int rp,
                                          const double *__restrict__ cpow, bool zero) {
 #pragma unroll 1
-  for (int c0 = 0; c0 < kI8TN; c0 += 16) {
-    uint32_t acc[S][16];
+  for (int c0 = 0; c0 < kI8TN; c0 += W) {  // W columns at a time: S x W registers
+    uint32_t acc[S][W];
 #pragma unroll
-    for (int d = 0; d < S; ++d) bfmm::tc::ld16(tl + d * kI8TN + c0, acc[d]);
+    for (int d = 0; d < S; ++d) {
+      if constexpr (W == 16) bfmm::tc::ld16(tl + d * kI8TN + c0, acc[d]);
+      else bfmm::tc::ld8(tl + d * kI8TN + c0, acc[d]);
+    }
     bfmm::tc::wait_ld();
     const int colb = nt * kI8TN + c0;
-    if (dst && colb < rp) {
 #pragma unroll
-      for (int jj = 0; jj < 16; jj += 2) {
-        double x2[2];
+    for (int jj = 0; jj < W; jj += 2) {
+      if (!dst || colb + jj >= rp) continue;  // rp is a multiple of 8
+      double x2[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          double x = (double)(int32_t)acc[S - 1][jj + u];
+      for (int u = 0; u < 2; ++u) {
+        double x = (double)(int32_t)acc[S - 1][jj + u];
 #pragma unroll
-          for (int d = S - 2; d >= 0; --d) x = fma(x, 0.0078125, (double)(int32_t)acc[d][jj + u]);
-          x2[u] = zero ? 0.0 : x * zsc * cpow[colb + jj + u];
-        }
-        if (colb + jj < rp)
-          *reinterpret_cast<double2 *>(dst + colb + jj) = make_double2(x2[0], x2[1]);
+        for (int d = S - 2; d >= 0; --d) x = fma(x, 0.0078125, (double)(int32_t)acc[d][jj + u]);
+        x2[u] = zero ? 0.0 : x * zsc * cpow[colb + jj + u];
       }
+      *reinterpret_cast<double2 *>(dst + colb + jj) = make_double2(x2[0], x2[1]);
     }
   }
 }
@@ -318,7 +319,7 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
       dst = lt + ((orow * m + c) * nsplit + split) * rp;
       zsc = i8_zscale(zmax[c]);
     }
-    i8_drain<S>(tmem + ((uint32_t)(32 * quarter) << 16), dst, zsc, nt, rp, cpow, false);
+    i8_drain<S, 16>(tmem + ((uint32_t)(32 * quarter) << 16), dst, zsc, nt, rp, cpow, false);
   }
   bfmm::tc::fence_before();
   __syncthreads();
@@ -349,6 +350,9 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
 // copies (B ring), 2-5 = plane loads (cp.async) then the TMEM drain.
 
 constexpr int kI8PThreads = 192;
+#ifndef BFMM_I8P_SMEM_KB
+#define BFMM_I8P_SMEM_KB 227
+#endif
 constexpr int kPlaneRows = 240;  // 20 (Y') x 12 (Z')
 
 template <int S>
@@ -359,14 +363,16 @@ struct I8PShape {
   static constexpr int NP = 3;  // plane buffers
   // core-block ring: as deep as the remaining shared memory allows
   // (measured: three plane buffers matter more than a deeper ring)
-  static constexpr int NB_FIT = (227 * 1024 - NP * PLANE - 512) / B_STAGE;
+  static constexpr int NB_FIT = (BFMM_I8P_SMEM_KB * 1024 - NP * PLANE - 512) / B_STAGE;
   static constexpr int NB = NB_FIT > 12 ? 12 : NB_FIT;
   static constexpr size_t smem = (size_t)NP * PLANE + (size_t)NB * B_STAGE +
                                  (2 * NP + 2 * NB + 1) * 8 + 16;
 };
 
+// register cap: leaves room on the SM for near-field (P2P) CTAs running
+// concurrently on another stream
 template <int S>
-__global__ void __launch_bounds__(kI8PThreads, 1)
+__global__ void __maxnreg__(128)
 m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
                const int8_t *__restrict__ cs, const double *__restrict__ cpow,
                double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
@@ -562,7 +568,7 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
     const int yl = er >> 3, zl = er & 7;
     const int64_t cell = (int64_t)morton3(xs, 2 * (16 * yb + yl) + oy, 2 * (8 * zb + zl) + oz);
     double *dst = lt + ((cell * m + col) * nsplit + split) * rp;
-    i8_drain<S>(tmem + ((uint32_t)(32 * quarter) << 16), dst, i8_zscale(zmax[col]), nt, rp, cpow,
+    i8_drain<S, 8>(tmem + ((uint32_t)(32 * quarter) << 16), dst, i8_zscale(zmax[col]), nt, rp, cpow,
                 !any);
   }
   bfmm::tc::fence_before();

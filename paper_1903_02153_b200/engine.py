@@ -652,12 +652,14 @@ class FmmEvaluator:
         near = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
         side = None
         main = torch.cuda.current_stream()
+        near_ready = torch.cuda.Event()
+        near_ready.record(main)  # trees and weights: all the near field needs
 
         def near_on_side():
             # near field on a side stream, concurrent with the far field (for
             # a shard: computes while the level all-gathers are in flight)
             side = self._side_stream(1)
-            side.wait_stream(main)
+            side.wait_event(near_ready)
             with torch.cuda.stream(side):
                 self._near_field(ttree, stree, ws, m, near, shard)
             return side

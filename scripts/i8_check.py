@@ -24,6 +24,7 @@ for spec in cfgs:
     for mode, S in [("dmma", 0), ("i8", 5), ("i8", 6), ("i8", 7), ("i8", 8)]:
         ev.m2l_mode, ev.i8_slices = mode, (S or 7)
         ev.profile_kernels = True
+        ev.overlap_near = False  # kernel spans without the near field sharing the SMs
         for _ in range(3):
             phi = ev.evaluate(X, weights=W)
         torch.cuda.synchronize()

@@ -19,7 +19,7 @@ python scripts/launches.py $OUT/launches.csv > $OUT/launch_shares.txt
 # one full capture of the dominant kernels of a steady-state C2 step
 python scripts/quick_c2.py C2 > $OUT/plain_quick.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"p2p_kernel|m2l_ws_kernel|proj_gemm|l2p_warp|p2m_leaf" -s 40 -c 8 \
+    -k regex:"p2p_kernel|m2l_i8p_kernel|m2l_i8_kernel|l2p_warp|p2m_leaf" -s 14 -c 7 \
     -o $OUT/top python scripts/quick_c2.py C2 > $OUT/ncu_full.log 2>&1
 echo "ncu full rc=$?"
 python scripts/ncu_summary.py $OUT/top.ncu-rep > $OUT/top_summary.txt 2>&1
