@@ -428,7 +428,8 @@ def run_ours(args, rank, world, local_rank):
                 "ms": round(v, 4), "kernel": "plane" if lev >= 5 else "gather",
                 "int8_tops": ops / (v * 1e-3) / 1e12,
                 "frac_int8_peak": ops / (v * 1e-3) / 1e12 / i8_peak.value,
-                "fp64_equiv_tflops": fp64, "frac_of_dmma_peak": fp64 / dmma_tf}
+                "fp64_equiv_tflops": fp64, "frac_of_dmma_peak": fp64 / dmma_tf,
+                "traffic": committed_traffic(args.config, k)}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
