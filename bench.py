@@ -236,25 +236,28 @@ def _valid_offsets(o):
 def m2l_i8_ops(lev, rp, m, S):
     """int8 operations the tcgen05 M2L executes at one level: per (tile,
     offset, 32-wide k chunk, 64-wide rank tile) stage, S(S+1)/2 digit
-    products of 128 x 64 x 32 (csrc/m2l_i8.cuh).  Dense levels >= 5 use the
-    plane kernel, which skips offsets whose source plane leaves the grid;
-    the gather kernel runs all 189 (zero rows)."""
+    products of 128 x 64 x 32 (csrc/m2l_i8.cuh).  Dense levels >= 4 use the
+    plane kernel, which skips offset groups whose source planes leave the
+    grid; the gather kernel runs all 189 (zero rows)."""
     n = 1 << lev
     kc, ntn = -(-rp // 32), -(-rp // 64)
     per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
-    if lev >= 5:
+    if lev >= 4:
         h = n // 2
+        xt = 1 if lev >= 5 else 2
+        yt = 16 // xt
         stages = 0
         for o in range(8):
             ox = (o >> 2) & 1
             offs = _valid_offsets(o)
-            for xi in range(h):
-                xs = 2 * xi + ox
-                live = sum(1 for t in offs if 0 <= xs + t[0] < n)
-                stages += live * (h // 16) * (h // 8)
+            for xb in range(h // xt):
+                xs = 2 * xb * xt + ox
+                # a group (offsets sharing t_x) runs when any x slot's plane is inside
+                live = sum(1 for t in offs if xs + t[0] + 2 * (xt - 1) >= 0 and xs + t[0] < n)
+                stages += live * (h // yt) * (h // 8)
     else:
         stages = -(-(n ** 3 // 8 * m) // 128) * 8 * 189
-    return stages * kc * ntn * m * per_stage if lev >= 5 else stages * kc * ntn * per_stage
+    return stages * kc * ntn * m * per_stage if lev >= 4 else stages * kc * ntn * per_stage
 
 
 def run_ours(args, rank, world, local_rank):
@@ -425,7 +428,7 @@ def run_ours(args, rank, world, local_rank):
             ops = m2l_i8_ops(lev, rp, m, S)
             fp64 = m2l[lev] / (v * 1e-3) / 1e12
             m2l_roof["levels"][k] = {
-                "ms": round(v, 4), "kernel": "plane" if lev >= 5 else "gather",
+                "ms": round(v, 4), "kernel": "plane" if lev >= 4 else "gather",
                 "int8_tops": ops / (v * 1e-3) / 1e12,
                 "frac_int8_peak": ops / (v * 1e-3) / 1e12 / i8_peak.value,
                 "fp64_equiv_tflops": fp64, "frac_of_dmma_peak": fp64 / dmma_tf,

@@ -327,12 +327,13 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
 }
 
 // ---------------------------------------------------------------------------
-// Plane-buffered variant for dense levels >= 5 (m2l_i8p_kernel).
+// Plane-buffered variant for dense levels >= 4 (m2l_i8p_kernel).
 //
 // The gather kernel above reads, per tile, 189 shifted copies of 128 source
 // rows -- 5.6x more than the distinct sources the tile touches -- and is
 // L2-bandwidth bound.  Here a tile is a 1 x 16 x 8 block (x, y, z) of
-// same-octant targets (stride 2 cells), tile row r = 8 y + z.  The 189
+// same-octant targets (stride 2 cells), tile row r = 8 y + z (2 x 8 x 8 at
+// level 4, see I8PShape).  The 189
 // offsets split into 28 groups by (t_x, parity of o_y + t_y, parity of
 // o_z + t_z); all sources of a group lie in ONE parity plane x = x_t + t_x,
 // y = 2Y' + py, z = 2Z' + pz with Y' in [16 yb - 2, 16 yb + 18) and
@@ -353,17 +354,23 @@ constexpr int kI8PThreads = 192;
 #ifndef BFMM_I8P_SMEM_KB
 #define BFMM_I8P_SMEM_KB 227
 #endif
-constexpr int kPlaneRows = 240;  // 20 (Y') x 12 (Z')
-
-template <int S>
+// Tile XT x YT x 8 (x, y, z) same-octant targets, XT * YT = 16: 1 x 16 x 8
+// for levels >= 5, 2 x 8 x 8 at level 4.  A plane buffer holds, per Y' row,
+// the XT source x-planes of the group side by side: row (Y', x, Z'), Z'
+// fastest, so the 16 row groups g = y XT + x of the A operand sit at the
+// uniform stride SBO = 12 * 16 B for any XT.
+template <int S, int XT>
 struct I8PShape {
-  static constexpr int HALF = kPlaneRows * 16;  // one K half of one digit plane
-  static constexpr int PLANE = S * 2 * HALF;    // one plane buffer
+  static constexpr int YT = 16 / XT;
+  static constexpr int ROWS = (YT + 4) * XT * 12;  // plane rows (Y' x x x Z')
+  static constexpr int HALF = ROWS * 16;           // one K half of one digit plane
+  static constexpr int PLANE = S * 2 * HALF;       // one plane buffer
   static constexpr int B_STAGE = S * kI8TN * 32;
-  static constexpr int NP = 3;  // plane buffers
-  // core-block ring: as deep as the remaining shared memory allows
-  // (measured: three plane buffers matter more than a deeper ring)
-  static constexpr int NB_FIT = (BFMM_I8P_SMEM_KB * 1024 - NP * PLANE - 512) / B_STAGE;
+  static constexpr int BUDGET = BFMM_I8P_SMEM_KB * 1024 - 512;
+  // three plane buffers when a 4-deep core ring still fits (measured: three
+  // plane buffers matter more than a deeper ring), else two
+  static constexpr int NP = (3 * PLANE + 4 * B_STAGE <= BUDGET) ? 3 : 2;
+  static constexpr int NB_FIT = (BUDGET - NP * PLANE) / B_STAGE;
   static constexpr int NB = NB_FIT > 12 ? 12 : NB_FIT;
   static constexpr size_t smem = (size_t)NP * PLANE + (size_t)NB * B_STAGE +
                                  (2 * NP + 2 * NB + 1) * 8 + 16;
@@ -371,14 +378,14 @@ struct I8PShape {
 
 // register cap: leaves room on the SM for near-field (P2P) CTAs running
 // concurrently on another stream
-template <int S>
+template <int S, int XT>
 __global__ void __maxnreg__(128)
 m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
                const int8_t *__restrict__ cs, const double *__restrict__ cpow,
                double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
                int nsplit) {
-  using Sh = I8PShape<S>;
-  constexpr int NP = Sh::NP, NB = Sh::NB;
+  using Sh = I8PShape<S, XT>;
+  constexpr int NP = Sh::NP, NB = Sh::NB, YT = Sh::YT;
   extern __shared__ __align__(1024) uint8_t smp[];
   uint8_t *const planes = smp;
   uint8_t *const bring = smp + NP * Sh::PLANE;
@@ -392,14 +399,14 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
   const int n = 1 << level, h = n >> 1;  // cells per axis; same-octant targets per axis
   const int o = blockIdx.z & 7, split = blockIdx.z >> 3;
   const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-  const int ybn = h >> 4, zbn = h >> 3;
+  const int ybn = h / YT, zbn = h >> 3;
   int tile = blockIdx.x;
   const int zb = tile % zbn;
   tile /= zbn;
   const int yb = tile % ybn;
-  const int xi = tile / ybn;
+  const int xb = tile / ybn;
   const int col = blockIdx.y / ntn, nt = blockIdx.y - col * ntn;
-  const int xs = 2 * xi + ox;  // target x
+  const int xs = 2 * xb * XT + ox;  // target x of the tile's first x slot (slots 2 apart)
   const int units = 28 * kc_n;
   const int per = (units + nsplit - 1) / nsplit;
   const int u_lo = split * per, u_hi = min(units, u_lo + per);
@@ -410,8 +417,8 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
     kc = u / 28;
     g = u - kc * 28;
     tx = g / 4 - 3;
-    const int x = xs + tx;
-    return x >= 0 && x < n && c_grp_off[o][g + 1] > c_grp_off[o][g];
+    // some x slot's source plane inside the grid
+    return xs + tx + 2 * (XT - 1) >= 0 && xs + tx < n && c_grp_off[o][g + 1] > c_grp_off[o][g];
   };
   bool any = false;
   for (int u = u_lo; u < u_hi; ++u) {
@@ -439,7 +446,7 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
 
   if (warp == 0) {
     // ---------------- MMA issue ----------------
-    const uint64_t dP = bfmm::tc::desc_kmajor(bfmm::tc::smem_u32(planes), Sh::HALF, 192);
+    const uint64_t dP = bfmm::tc::desc_kmajor(bfmm::tc::smem_u32(planes), Sh::HALF, 192);  // SBO: 12 rows
     const uint64_t dB = bfmm::tc::desc_kmajor(bfmm::tc::smem_u32(bring), 128, 256);
     int ps = 0, bs = 0;
     uint32_t pph = 0, bph = 0;
@@ -456,7 +463,8 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
         if (lane == 0) mbar_wait(&bfull[bs], bph);
         __syncwarp();
         bfmm::tc::fence_after();
-        const uint64_t dA = dP + (uint64_t)((ps * Sh::PLANE + ((dy + 2) * 12 + dz + 2) * 16) >> 4);
+        const uint64_t dA =
+            dP + (uint64_t)((ps * Sh::PLANE + ((dy + 2) * XT * 12 + dz + 2) * 16) >> 4);
         const uint64_t dBs = dB + (uint64_t)((bs * Sh::B_STAGE) >> 4);
         if (elect_one()) {
 #pragma unroll
@@ -527,11 +535,11 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
         __syncwarp();
       }
       uint8_t *buf = planes + ps * Sh::PLANE;
-      const int x = xs + tx;
-      for (int row = p; row < kPlaneRows; row += 128) {
-        const int Yp = 16 * yb - 2 + row / 12, Zp = 8 * zb - 2 + row % 12;
+      for (int row = p; row < Sh::ROWS; row += 128) {
+        const int yx = row / 12, Zp = 8 * zb - 2 + row % 12;
+        const int Yp = YT * yb - 2 + yx / XT, x = xs + 2 * (yx % XT) + tx;
         const int y = 2 * Yp + py, z = 2 * Zp + pz;
-        const bool v = y >= 0 && y < n && z >= 0 && z < n;
+        const bool v = x >= 0 && x < n && y >= 0 && y < n && z >= 0 && z < n;
         const int8_t *src =
             v ? zs + ((int64_t)morton3(x, y, z) * m + col) * rowbytes + kc * (S * 32) : zs;
         uint8_t *dst = buf + row * 16;
@@ -565,8 +573,9 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
     }
     const int quarter = warp & 3;
     const int er = 32 * quarter + lane;
-    const int yl = er >> 3, zl = er & 7;
-    const int64_t cell = (int64_t)morton3(xs, 2 * (16 * yb + yl) + oy, 2 * (8 * zb + zl) + oz);
+    const int g = er >> 3, zl = er & 7;  // row group g = y XT + x
+    const int64_t cell = (int64_t)morton3(xs + 2 * (g % XT), 2 * (YT * yb + g / XT) + oy,
+                                          2 * (8 * zb + zl) + oz);
     double *dst = lt + ((cell * m + col) * nsplit + split) * rp;
     i8_drain<S, 8>(tmem + ((uint32_t)(32 * quarter) << 16), dst, i8_zscale(zmax[col]), nt, rp, cpow,
                 !any);
@@ -678,38 +687,43 @@ int launch_i8(const I8Call &a) {
   return check_launch("m2l_i8_kernel");
 }
 
-template <int S>
+template <int S, int XT>
 int launch_i8p(const I8Call &a) {
-  using Sh = I8PShape<S>;
+  using Sh = I8PShape<S, XT>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(m2l_i8p_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(m2l_i8p_kernel<S, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
     attr_set = true;
   }
   const int h = 1 << (a.level - 1);
-  dim3 grid((unsigned)(h * (h / 16) * (h / 8)), (unsigned)(a.ntn * a.m), 8 * a.nsplit);
-  m2l_i8p_kernel<S><<<grid, kI8PThreads, Sh::smem, a.st>>>(
+  dim3 grid((unsigned)((h / XT) * (h / Sh::YT) * (h / 8)), (unsigned)(a.ntn * a.m),
+            8 * a.nsplit);
+  m2l_i8p_kernel<S, XT><<<grid, kI8PThreads, Sh::smem, a.st>>>(
       a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit);
   return check_launch("m2l_i8p_kernel");
 }
 
-// the plane kernel covers whole dense levels >= 5; shards and listed cells
-// use the gather kernel
+// the plane kernel covers whole dense levels >= 4 (1 x 16 x 8 tiles from
+// level 5, 2 x 8 x 8 at level 4); shards and listed cells use the gather
+// kernel.  BFMM_I8_GATHER (diagnostic) forces the gather kernel.
 inline bool i8_plane_ok(const I8Call &a) {
-  return !a.act.cells && a.level >= 5 && a.q_lo == 0 &&
+  return !a.act.cells && a.level >= 4 && a.q_lo == 0 &&
          a.nq == (int64_t(1) << (3 * a.level - 3)) && !getenv("BFMM_I8_GATHER");
 }
 
-inline int dispatch_i8(int S, const I8Call &a) {
-  if (i8_plane_ok(a)) {
-    switch (S) {
-      case 5: return launch_i8p<5>(a);
-      case 6: return launch_i8p<6>(a);
-      case 7: return launch_i8p<7>(a);
-      default: return launch_i8p<8>(a);
-    }
+template <int XT>
+int dispatch_i8p(int S, const I8Call &a) {
+  switch (S) {
+    case 5: return launch_i8p<5, XT>(a);
+    case 6: return launch_i8p<6, XT>(a);
+    case 7: return launch_i8p<7, XT>(a);
+    default: return launch_i8p<8, XT>(a);
   }
+}
+
+inline int dispatch_i8(int S, const I8Call &a) {
+  if (i8_plane_ok(a)) return a.level >= 5 ? dispatch_i8p<1>(S, a) : dispatch_i8p<2>(S, a);
   switch (S) {
     case 5: return launch_i8<5>(a);
     case 6: return launch_i8<6>(a);

@@ -13,7 +13,7 @@ lib = _native.load()
 st = _native.C.c_void_p(0)
 g = np.random.default_rng(0)
 import os
-for level, rp, m, S in [(5, 56, 1, 7), (5, 104, 1, 7), (5, 32, 2, 6), (6, 56, 1, 7), (5, 56, 1, 8), (3, 56, 1, 7)]:
+for level, rp, m, S in [(4, 104, 1, 7), (4, 56, 2, 7), (5, 56, 1, 7), (4, 128, 1, 8), (3, 56, 1, 7)]:
     ncell = 8 ** level
     z = g.standard_normal((ncell * m, rp)) * np.exp(g.uniform(-3, 0, (ncell * m, 1)))
     cores = g.standard_normal((316, rp, rp)) * np.logspace(0, -6, rp)[None, :, None]

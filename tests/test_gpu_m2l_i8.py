@@ -67,6 +67,7 @@ def _run_both(level, rp, m, S, ns, seed=0, gather=False):
                                              (3, 64, 3, 6, 2), (2, 168, 1, 8, 1),
                                              (4, 56, 1, 5, 4), (2, 8, 2, 7, 189),
                                              (5, 56, 1, 7, 1), (5, 104, 2, 7, 3),
+                                             (4, 104, 1, 7, 1), (4, 48, 3, 6, 2),
                                              (5, 64, 1, 8, 2), (6, 24, 1, 6, 1)])
 def test_i8_translation_matches_dmma(level, rp, m, S, ns):
     got, ref, _ = _run_both(level, rp, m, S, ns)
@@ -89,12 +90,14 @@ def test_i8_split_blocks_past_the_last_offset_are_zero():
     assert np.abs(got - ref).max() < 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("rp,m,S", [(56, 1, 7), (40, 2, 6)])
-def test_i8_plane_and_gather_kernels_agree_bitwise(rp, m, S):
-    """Dense levels >= 5 use the plane-buffered kernel; its int32 sums are
-    the gather kernel's integers, so the lt blocks are bitwise equal."""
-    _, _, a = _run_both(5, rp, m, S, 1)
-    _, _, b = _run_both(5, rp, m, S, 1, gather=True)
+@pytest.mark.parametrize("level,rp,m,S", [(5, 56, 1, 7), (5, 40, 2, 6), (4, 104, 1, 7),
+                                          (4, 64, 2, 8)])
+def test_i8_plane_and_gather_kernels_agree_bitwise(level, rp, m, S):
+    """Dense levels >= 4 use the plane-buffered kernel (1 x 16 x 8 tiles, or
+    2 x 8 x 8 at level 4); its int32 sums are the gather kernel's integers,
+    so the lt blocks are bitwise equal."""
+    _, _, a = _run_both(level, rp, m, S, 1)
+    _, _, b = _run_both(level, rp, m, S, 1, gather=True)
     assert torch.equal(a, b)
 
 
