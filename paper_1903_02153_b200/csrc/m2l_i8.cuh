@@ -30,6 +30,7 @@
 constexpr int kI8TM = 128, kI8TN = 64;
 #ifdef BFMM_I8_TRACE
 __device__ long long g_i8_trace[8192];
+__device__ int g_trace_n;
 #endif
 constexpr int kI8Threads = 160;  // warp 0: TMEM + MMA issue; warps 1-4: producers/epilogue
 
@@ -454,13 +455,26 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
     for (int u = u_lo; u < u_hi; ++u) {
       int kc, g, tx;
       if (!live(u, kc, g, tx)) continue;
+#ifdef BFMM_I8_TRACE
+      const bool trc = lane == 0 && blockIdx.x == 3 && blockIdx.y == 0 && blockIdx.z == 0;
+      long long tw0 = clock64();
+#endif
       if (lane == 0) mbar_wait(&pfull[ps], pph);
+#ifdef BFMM_I8_TRACE
+      if (trc && g_trace_n < 4000) { g_i8_trace[2 * g_trace_n] = tw0; g_i8_trace[2 * g_trace_n + 1] = -clock64(); ++g_trace_n; }
+#endif
       __syncwarp();
       bfmm::tc::fence_after();
       for (int e = c_grp_off[o][g]; e < c_grp_off[o][g + 1]; ++e) {
         const int t = c_grp[o][e];
         const int dy = (oy + c_offsets[t][1]) >> 1, dz = (oz + c_offsets[t][2]) >> 1;
+#ifdef BFMM_I8_TRACE
+        long long tb0 = clock64();
+#endif
         if (lane == 0) mbar_wait(&bfull[bs], bph);
+#ifdef BFMM_I8_TRACE
+        if (trc && g_trace_n < 4000) { g_i8_trace[2 * g_trace_n] = tb0; g_i8_trace[2 * g_trace_n + 1] = clock64(); ++g_trace_n; }
+#endif
         __syncwarp();
         bfmm::tc::fence_after();
         const uint64_t dA =
