@@ -2,7 +2,7 @@
 """FMM matvec throughput (points/s, fp64) on B200 — the BASELINE.json metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2] [--no-cpu-baseline]
+                    [--config C2] [--no-cpu-baseline] [--no-graph]
 
 Workload (N=1): BASELINE.json configs[1] = C2 (Gaussian exp(-(r/0.2)^2),
 N = 1,000,000 uniform in [-1,1]^3, L=5, Chebyshev p=5, eps 1e-7, 1 RHS),
@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--balance", default="auto", choices=["auto", "cells", "work"],
                     help="N>1 shard ranges: equal cell ranges, work-weighted, or auto "
                          "(work-weighted for the clustered C4)")
@@ -169,7 +170,8 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded SURVEY.md §8(d) recipe)",
         "config": dict(config_dict(wl), m2l_engine=(
             f"int8 tcgen05, {ev.i8_slices} digits" if ev.m2l_mode == "i8" else "fp64 dmma"),
-            near_field_stream="own stream, overlaps kernel tails" if ev.overlap_near else "serial"),
+            near_field_stream="own stream, overlaps kernel tails" if ev.overlap_near else "serial",
+        cuda_graph=bool(ev.use_graph)),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
                          "sample": f"full {args.config} matvec per step (oracle/fmm_oracle.py)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
@@ -282,6 +284,9 @@ def run_ours(args, rank, world, local_rank):
                       n_cols=wl["ncols"])
     kernel = workload_kernel(wl["kernel"])
     ev = bf.FmmEvaluator(kernel, plan, cache_dir=os.path.join("/tmp", "bfmm_bench_cache"))
+    # whole device step replayed from a CUDA graph (FmmEvaluator.use_graph;
+    # captured during warm-up, eager path for the per-kernel timing pass)
+    ev.use_graph = not args.no_graph
     lib = _native.load()
     stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     n = wl["points"].shape[0]
@@ -307,7 +312,7 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = lib.bfmm_launch_count()
+    launches0 = lib.bfmm_launch_count() + ev.graph_launches
     spans, kms, stage_sum = [], [], {}
     for _ in range(args.steps):
         flush.zero_()
@@ -322,7 +327,7 @@ def run_ours(args, rank, world, local_rank):
             if isinstance(v, float):
                 stage_sum[k] = stage_sum.get(k, 0.0) + v
     torch.cuda.synchronize()
-    launches = lib.bfmm_launch_count() - launches0
+    launches = lib.bfmm_launch_count() + ev.graph_launches - launches0
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
@@ -453,10 +458,12 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (seeded SURVEY.md §8(d) recipe)",
         "config": dict(config_dict(wl), m2l_engine=(
             f"int8 tcgen05, {ev.i8_slices} digits" if ev.m2l_mode == "i8" else "fp64 dmma"),
-            near_field_stream="own stream, overlaps kernel tails" if ev.overlap_near else "serial"),
+            near_field_stream="own stream, overlaps kernel tails" if ev.overlap_near else "serial",
+        cuda_graph=bool(ev.use_graph)),
         "roofline": roof, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,
+                "step_ms": [round(x, 3) for x in e2e_ms]},
         "gpu_launches": int(launches), "clocks": clk,
         "stages_ms": {k: round(1e3 * v / args.steps, 4) for k, v in stage_sum.items()},
         "kernels_ms": kernels,

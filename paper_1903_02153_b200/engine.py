@@ -158,6 +158,10 @@ class FmmEvaluator:
         self._side = None
         self.kernel_ms = {}
         self._kpending = []
+        # replay the device step from a CUDA graph when possible (_graph_ok)
+        self.use_graph = False
+        self._graphs = {}
+        self.graph_launches = 0  # kernels of ours run by graph replays (bench accounting)
 
     # -- setup --------------------------------------------------------------
     def _kernel_handle(self) -> int:
@@ -604,6 +608,8 @@ class FmmEvaluator:
                     f"weights shape {np.shape(weights)} does not match {src_np.shape[0]} sources")
             if w_np.size and not np.all(np.isfinite(w_np)):
                 raise ConfigurationError("weights contain non-finite values")
+        if self._graph_ok(sources, targets, weights, sharded, shared):
+            return self._graph_evaluate(sources, weights, as_tensor, out_device)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         t_host0 = time.perf_counter()
         ev[0].record()
@@ -626,9 +632,45 @@ class FmmEvaluator:
             w, squeeze = self._prepare_weights(weights, src.shape[0])
         m = int(w.shape[1])
         n_src, n_tgt = int(src.shape[0]), int(tgt.shape[0])
+        phi, status, ttree, stree, extras = self._device_step(
+            src, tgt, w, w_event, m, n_src, n_tgt, shared, sharded, _shard, ev)
+        if self.keep_stages:
+            self.stages = dict(extras, stree=stree, ttree=ttree)
+        phi_host = None
+        if not as_tensor or out_device.type != "cuda":
+            # async D2H into pinned memory, ordered before the status read
+            phi_host = torch.empty((n_tgt, m), dtype=torch.float64, pin_memory=True)
+            phi_host.copy_(phi, non_blocking=True)
+        stat = status.cpu().numpy()  # the one synchronising read-back
+        self.kernel_ms = {name: a.elapsed_time(b) for name, a, b in self._kpending}
+        self._kpending = []
+        self._raise_flags(stat, ttree, stree)
+        if as_tensor:
+            result = phi if out_device.type == "cuda" else phi_host
+        else:
+            result = phi_host.numpy()
+        total_host = time.perf_counter() - t_host0
+        ms = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(6)]
+        self.timings = {
+            "upload": ms[0], "distribute": ms[1], "upward": ms[2],
+            "far_field": ms[3] if not self._disable_far_field else 0.0,
+            "downward": ms[4] if not self._disable_far_field else 0.0,
+            "near_field": ms[5], "near_pairs": int(stat.view(np.int64)[4]),
+        }
+        self.timings["total"] = sum(v for k, v in self.timings.items()
+                                    if k not in ("near_pairs", "upload"))
+        self.timings["wall"] = total_host
+        return result[:, 0] if squeeze else result
+
+    def _device_step(self, src, tgt, w, w_event, m, n_src, n_tgt, shared, sharded, _shard, ev):
+        """Everything of a matvec that runs on the device, from the tree build
+        to the output scatter (no host synchronisation: capturable in a CUDA
+        graph).  ev: 7 timing events or None."""
+        torch = _torch()
         status = torch.zeros(16, dtype=torch.int32, device=self.device)
         st = self._stream()
-        ev[1].record()
+        if ev:
+            ev[1].record()
         stree = self._build_tree(src, status, _ST_DOMAIN_SRC)
         ttree = stree if shared else self._build_tree(tgt, status, _ST_DOMAIN_TGT)
         if w_event is not None:
@@ -637,7 +679,8 @@ class FmmEvaluator:
         _native.check(self.lib.bfmm_gather_weights(w.data_ptr(), n_src, m, stree.perm.data_ptr(),
                                                    ws.data_ptr(), stree.pts4.data_ptr(), st),
                       "bfmm_gather_weights")
-        ev[2].record()
+        if ev:
+            ev[2].record()
         shard = _shard if sharded else None
         if sharded and _shard[0].balance == "work":
             # work-balanced Morton ranges from this target tree (same on every rank)
@@ -668,7 +711,8 @@ class FmmEvaluator:
         if overlap and (sharded or self.near_after_far is False):
             side = near_on_side()
         moments, leaf_geom = self._upward(stree, ws, m, status, shard)
-        ev[3].record()
+        if ev:
+            ev[3].record()
         phi_far = None
         if not self._disable_far_field:
             locs = self._far_field(moments, m, shard, self._active_cells(ttree, shard))
@@ -676,13 +720,16 @@ class FmmEvaluator:
                 # enqueued after the far field: the persistent P2P grid fills
                 # the SMs the M2L CTAs leave free instead of holding them all
                 side = near_on_side()
-            ev[4].record()
+            if ev:
+                ev[4].record()
             phi_far = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
             self._downward(locs, ttree, m, leaf_geom, status, phi_far, shard)
         else:
             locs = None
-            ev[4].record()
-        ev[5].record()
+            if ev:
+                ev[4].record()
+        if ev:
+            ev[5].record()
         if side is None:
             self._near_field(ttree, stree, ws, m, near, shard)
         else:
@@ -699,34 +746,124 @@ class FmmEvaluator:
             pairs_dev.data_ptr(), st), "bfmm_near_pair_count")
         if sharded:
             _shard[1].allreduce_sum(phi)  # every rank wrote only its own targets
-        ev[6].record()
-        if self.keep_stages:
-            self.stages = {"stree": stree, "ttree": ttree, "moments": moments, "locals": locs,
-                           "near": near, "far": phi_far, "ws": ws}
-        phi_host = None
-        if not as_tensor or out_device.type != "cuda":
-            # async D2H into pinned memory, ordered before the status read
-            phi_host = torch.empty((n_tgt, m), dtype=torch.float64, pin_memory=True)
-            phi_host.copy_(phi, non_blocking=True)
-        stat = status.cpu().numpy()  # the one synchronising read-back
-        self.kernel_ms = {name: a.elapsed_time(b) for name, a, b in self._kpending}
-        self._kpending = []
-        self._raise_flags(stat, ttree, stree)
-        if as_tensor:
-            result = phi if out_device.type == "cuda" else phi_host
+        if ev:
+            ev[6].record()
+        extras = {"moments": moments, "locals": locs, "near": near, "far": phi_far, "ws": ws}
+        return phi, status, ttree, stree, extras
+
+    # -- CUDA graph replay (use_graph) ----------------------------------------
+    def _graph_ok(self, sources, targets, weights, sharded, shared):
+        """The whole device step replays from a CUDA graph when nothing in it
+        needs the host: one point set (targets = sources), Chebyshev tables,
+        the dense far field, no sharding, no per-kernel/stage inspection."""
+        if not self.use_graph or sharded or not shared or self.keep_stages:
+            return False
+        if self.profile_kernels or self._disable_far_field or weights is None:
+            return False
+        if self.plan.scheme is not SchemeKind.CHEBYSHEV:
+            return False
+        n = int(sources.shape[0])
+        L = self.plan.levels
+        # the sparse-cloud active lists read counts back on the host
+        return self.far_mode == "dense" or (self.far_mode == "auto" and n >= 8 * (1 << (3 * L)))
+
+    def _graph_evaluate(self, sources, weights, as_tensor, out_device):
+        """evaluate() through a captured CUDA graph of _device_step (identical
+        kernels and buffers, so identical results: tests/test_gpu_graph.py).
+        Device float64 inputs are read in place and pinned host tensors are
+        copied inside the graph (the weights on a side stream, under the tree
+        build, as in the eager path) -- graphs are keyed by the input
+        buffers; other host inputs go through static device buffers.  Stage
+        timings are not split in this mode (only total / wall / near_pairs)."""
+        torch = _torch()
+        t_host0 = time.perf_counter()
+        src_t = sources if as_tensor else torch.from_numpy(
+            np.ascontiguousarray(sources, dtype=np.float64))
+        if src_t.ndim != 2 or src_t.shape[1] != 3:
+            raise ConfigurationError(
+                f"sources must be an (N, 3) array, got shape {tuple(src_t.shape)}")
+        w_t = weights if isinstance(weights, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(weights, dtype=np.float64))
+        squeeze = w_t.ndim == 1
+        if squeeze:
+            w_t = w_t[:, None]
+        n = int(src_t.shape[0])
+        if w_t.ndim != 2 or w_t.shape[0] != n:
+            raise ConfigurationError(
+                f"weights shape {tuple(weights.shape)} does not match {n} sources")
+        m = int(w_t.shape[1])
+
+        def plain(t, dev):
+            return (t.dtype == torch.float64 and t.is_contiguous() and
+                    (t.is_cuda if dev else (not t.is_cuda and t.is_pinned())))
+        if plain(src_t, True) and plain(w_t, True) and src_t.device == self.device:
+            kind, key = "device", ("device", n, m, src_t.data_ptr(), w_t.data_ptr())
+        elif plain(src_t, False) and plain(w_t, False):
+            kind, key = "pinned", ("pinned", n, m, src_t.data_ptr(), w_t.data_ptr())
         else:
-            result = phi_host.numpy()
-        total_host = time.perf_counter() - t_host0
-        ms = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(6)]
-        self.timings = {
-            "upload": ms[0], "distribute": ms[1], "upward": ms[2],
-            "far_field": ms[3] if not self._disable_far_field else 0.0,
-            "downward": ms[4] if not self._disable_far_field else 0.0,
-            "near_field": ms[5], "near_pairs": int(stat.view(np.int64)[4]),
-        }
-        self.timings["total"] = sum(v for k, v in self.timings.items()
-                                    if k not in ("near_pairs", "upload"))
-        self.timings["wall"] = total_host
+            kind, key = "static", ("static", n, m)
+        ent = self._graphs.get(key)
+        if ent is None:
+            if len(self._graphs) >= 4:  # each graph keeps its memory pool
+                self._graphs.pop(next(iter(self._graphs)))
+            stat_in = None
+            if kind == "static":
+                stat_in = (torch.empty((n, 3), dtype=torch.float64, device=self.device),
+                           torch.empty((n, m), dtype=torch.float64, device=self.device))
+                stat_in[0].copy_(src_t)
+                stat_in[1].copy_(w_t)
+
+            def body():
+                if kind == "device":
+                    xs, ws_, w_ev = src_t, w_t, None
+                elif kind == "static":
+                    (xs, ws_), w_ev = stat_in, None
+                else:
+                    main = torch.cuda.current_stream()
+                    xs = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+                    xs.copy_(src_t, non_blocking=True)
+                    side = self._side_stream()
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        ws_ = torch.empty((n, m), dtype=torch.float64, device=self.device)
+                        ws_.copy_(w_t, non_blocking=True)
+                        w_ev = torch.cuda.Event()
+                        w_ev.record()
+                    ws_.record_stream(main)
+                return self._device_step(xs, xs, ws_, w_ev, m, n, n, True, False, None, None)
+
+            body()  # eager warm-up: lazy tables, kernel attributes
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            l0 = self.lib.bfmm_launch_count()
+            with torch.cuda.graph(g):
+                outs = body()
+            ent = self._graphs[key] = (g, stat_in, outs, int(self.lib.bfmm_launch_count() - l0))
+        g, stat_in, outs, nlaunch = ent
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if stat_in is not None:
+            stat_in[0].copy_(src_t, non_blocking=True)
+            stat_in[1].copy_(w_t, non_blocking=True)
+        g.replay()
+        self.graph_launches += nlaunch  # our kernels inside the replayed graph
+        phi, status, ttree, stree, _ = outs
+        if as_tensor and out_device.type == "cuda":
+            result = phi.clone()
+        else:
+            result = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+            result.copy_(phi, non_blocking=True)
+        e1.record()
+        stat = status.cpu().numpy()  # the one synchronising read-back
+        self.kernel_ms = {}
+        self._raise_flags(stat, ttree, stree)
+        if not as_tensor:
+            result = result.numpy()
+        total = e0.elapsed_time(e1) * 1e-3
+        self.timings = {"upload": 0.0, "distribute": 0.0, "upward": 0.0, "far_field": 0.0,
+                        "downward": 0.0, "near_field": 0.0,
+                        "near_pairs": int(stat.view(np.int64)[4]), "total": total,
+                        "wall": time.perf_counter() - t_host0}
         return result[:, 0] if squeeze else result
 
     def _raise_flags(self, stat, ttree, stree):
