@@ -261,14 +261,24 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
         for (int e = lane; e < P3; e += 32) sL[wid][e] = src[e];
         __syncwarp();
         const double *L = sL[wid];
-        double s = 0.0;
-#pragma unroll 1
-        for (int ab = 0; ab < P2; ++ab) {
-          double sb = 0.0;
+        // one partial sum per x node a (P independent chains), added in a
+        // fixed order -- the same arithmetic as l2p_point_kernel
+        double sa[P];
 #pragma unroll
-          for (int k = 0; k < P; ++k) sb = fma(wz[k], L[ab * P + k], sb);
-          s = fma(sWxy[wid][ab][lane], sb, s);
+        for (int a = 0; a < P; ++a) {
+          sa[a] = 0.0;
+#pragma unroll
+          for (int b = 0; b < P; ++b) {
+            const int ab = a * P + b;
+            double sb = 0.0;
+#pragma unroll
+            for (int k = 0; k < P; ++k) sb = fma(wz[k], L[ab * P + k], sb);
+            sa[a] = fma(sWxy[wid][ab][lane], sb, sa[a]);
+          }
         }
+        double s = sa[0];
+#pragma unroll
+        for (int a = 1; a < P; ++a) s += sa[a];
         if (have) phi[i * m + c] = s;
       }
     }
@@ -309,18 +319,22 @@ l2p_point_kernel(const double *__restrict__ pts4, int m,
     weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
     for (int c = 0; c < m; ++c) {
       const double *L = locals + (cell * m + c) * (int64_t)P3;
-      double s = 0.0;
+      double sa[P];
 #pragma unroll
       for (int a = 0; a < P; ++a) {
+        sa[a] = 0.0;
 #pragma unroll
         for (int b = 0; b < P; ++b) {
           const double *Lab = L + (a * P + b) * P;
           double sb = 0.0;
 #pragma unroll
           for (int k = 0; k < P; ++k) sb = fma(wz[k], Lab[k], sb);
-          s = fma(wx[a] * wy[b], sb, s);  // same products as the warp kernel
+          sa[a] = fma(wx[a] * wy[b], sb, sa[a]);  // same products as the warp kernel
         }
       }
+      double s = sa[0];
+#pragma unroll
+      for (int a = 1; a < P; ++a) s += sa[a];
       phi[i * m + c] = s;
     }
   }
