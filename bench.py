@@ -168,10 +168,7 @@ def run_reference(args, rank, world):
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SURVEY.md §8(d) recipe)",
-        "config": dict(config_dict(wl), m2l_engine=(
-            f"int8 tcgen05, {ev.i8_slices} digits" if ev.m2l_mode == "i8" else "fp64 dmma"),
-            near_field_stream="own stream, overlaps kernel tails" if ev.overlap_near else "serial",
-        cuda_graph=bool(ev.use_graph)),
+        "config": config_dict(wl),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
                          "sample": f"full {args.config} matvec per step (oracle/fmm_oracle.py)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
@@ -456,10 +453,12 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SURVEY.md §8(d) recipe)",
-        "config": dict(config_dict(wl), m2l_engine=(
-            f"int8 tcgen05, {ev.i8_slices} digits" if ev.m2l_mode == "i8" else "fp64 dmma"),
-            near_field_stream="own stream, overlaps kernel tails" if ev.overlap_near else "serial",
-        cuda_graph=bool(ev.use_graph)),
+        "config": config_dict(wl),
+        "engine": {"m2l": (f"int8 tcgen05, {ev.i8_slices} digits" if ev.m2l_mode == "i8"
+                           else "fp64 dmma"),
+                   "near_field": ("own stream, overlaps kernel tails" if ev.overlap_near
+                                  else "serial"),
+                   "cuda_graph": bool(ev.use_graph)},
         "roofline": roof, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,

@@ -200,3 +200,21 @@ def test_i8_core_slices_reconstruct_the_cores():
         assert np.all(err <= 2.0 ** (1 - 7 * S) * scale)
         assert np.all(rec[:, rp:, :] == 0) and np.all(rec[:, :, rp:] == 0)
         assert cpow[5] == 1.0 and np.all(Dr[:, :, 5] == 0)
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """The driver's reference arm (bench.py --impl reference) must print one
+    JSON line with the contract's keys; C1 keeps it to about a second."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "C1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
