@@ -49,6 +49,25 @@ def _rank_interleave(rp: int) -> np.ndarray:
     return (k // 8) * 8 + 2 * (k % 4) + (k // 4) % 2
 
 
+_PIN_WARM = None
+
+
+def _warm_pinned_dma(device):
+    """Once per process: one H2D copy from a small sacrificial pinned buffer.
+    Measured on the B200 pool: the first pinned buffer a process copies from
+    keeps running at ~25 GB/s while every later one gets the full ~55 GB/s
+    (scripts/numa_probe.py), so without this the caller's first pinned input
+    (e.g. the points of every end-to-end matvec) pays double H2D time."""
+    global _PIN_WARM
+    if _PIN_WARM is None:
+        torch = _torch()
+        h = torch.zeros(1 << 19, dtype=torch.float64).pin_memory()  # 4 MiB
+        d = torch.empty_like(h, device=device)
+        d.copy_(h)
+        torch.cuda.synchronize(device)
+        _PIN_WARM = h  # kept alive: the warmed buffer must not be reused
+
+
 def _i8_core_slices(CP: np.ndarray, S: int):
     """Cores (316, rp, rp) [t][i][k] -> the digit planes bfmm_m2l_i8 reads
     (csrc/m2l_i8.cuh): row i is scaled by 2^-e_i (e_i the exponent of
@@ -104,6 +123,7 @@ class FmmEvaluator:
         if not torch.cuda.is_available():
             raise NativeLibraryError("no CUDA device is visible; the FMM matvec runs on the GPU only")
         self.lib = _native.load()
+        _warm_pinned_dma(torch.device(device if device is not None else "cuda"))
         self.kernel = kernel
         self.plan = plan
         self.threads = max(1, int(threads))
