@@ -353,6 +353,8 @@ int bfmm_tc_i8_selftest(const int8_t *A, const int8_t *B, int K, int32_t *D,
  * MMAs back to back from shared memory, one CTA per SM) in TOPS: the peak
  * the int8 M2L (bfmm_m2l_i8) is measured against. */
 int bfmm_device_i8_probe(double *tops, bfmm_stream_t stream);
+/* The same with 128 x N x 32 MMAs, N in {64, 128, 192, 256} (shape sweep). */
+int bfmm_device_i8_probe_n(int N, double *tops, bfmm_stream_t stream);
 
 /* DMMA throughput with warps_per_sm resident warps x `chains` independent
  * accumulator chains (microarchitecture sweep behind the M2L tiling). */

@@ -49,6 +49,7 @@ SIGNATURES = {
     "bfmm_m2l_i8_cells": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "bfmm_device_dmma_probe": (_I, [_DP, _P]),
     "bfmm_device_i8_probe": (_I, [_DP, _P]),
+    "bfmm_device_i8_probe_n": (_I, [_I, _DP, _P]),
     "bfmm_tc_i8_selftest": (_I, [_P, _P, _I, _P, _P]),
     "bfmm_device_dmma_sweep": (_I, [_I, _I, _DP, _P]),
     "bfmm_launch_count": (C.c_longlong, []),

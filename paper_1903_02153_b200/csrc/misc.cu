@@ -322,6 +322,27 @@ __global__ void __launch_bounds__(128, 1) tc_i8_probe_kernel(int iters, int32_t 
 }  // namespace
 }  // namespace bfmm
 
+extern "C" int bfmm_device_i8_probe_n(int N, double *tops, bfmm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  int32_t *sink = nullptr;
+  if (cudaMalloc(&sink, 4096 * sizeof(int32_t)) != cudaSuccess) return 1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int iters = 1 << 14;
+  float ms = 0;
+  switch (N) {
+    case 64: ms = best_ms([&] { bfmm::tc_i8_probe_kernel<64><<<sms, 128, 0, st>>>(iters, sink); }, st); break;
+    case 128: ms = best_ms([&] { bfmm::tc_i8_probe_kernel<128><<<sms, 128, 0, st>>>(iters, sink); }, st); break;
+    case 192: ms = best_ms([&] { bfmm::tc_i8_probe_kernel<192><<<sms, 128, 0, st>>>(iters, sink); }, st); break;
+    default: ms = best_ms([&] { bfmm::tc_i8_probe_kernel<256><<<sms, 128, 0, st>>>(iters, sink); }, st); N = 256; break;
+  }
+  cudaFree(sink);
+  if (check_launch("tc_i8_probe_kernel")) return 1;
+  *tops = 2.0 * 128 * N * 32 * double(iters) * sms / (ms * 1e-3) / 1e12;
+  return 0;
+}
+
 extern "C" int bfmm_device_i8_probe(double *tops, bfmm_stream_t stream) {
   cudaStream_t st = as_stream(stream);
   int32_t *sink = nullptr;
