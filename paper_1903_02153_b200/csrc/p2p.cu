@@ -27,11 +27,12 @@ struct KLaplace {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : rsqrt(r2);
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+  template <class F>
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, F &bad) {
     const double r2 = dx * dx + dy * dy + dz * dz;
     bool b = false;
     const double v = bfmm_nf::bfmm_rsqrt_fast(r2, b);
-    bad |= b && r2 != 0.0;
+    bfmm_nf::flag_set(bad, b && r2 != 0.0);
     return r2 == 0.0 ? 0.0 : v;
   }
 };
@@ -41,11 +42,12 @@ struct KLaplaceForce {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : 1.0 / (r2 * r2);
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+  template <class F>
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, F &bad) {
     const double r2 = dx * dx + dy * dy + dz * dz;
     bool b = false;
     const double v = bfmm_nf::bfmm_rcp_fast(r2 * r2, b);
-    bad |= b && r2 != 0.0;
+    bfmm_nf::flag_set(bad, b && r2 != 0.0);
     return r2 == 0.0 ? 0.0 : v;
   }
 };
@@ -54,7 +56,8 @@ struct KGaussian {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     return bfmm_nf::bfmm_exp(-(dx * dx + dy * dy + dz * dz));
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+  template <class F>
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, F &bad) {
     return bfmm_nf::bfmm_exp_fast(-(dx * dx + dy * dy + dz * dz), bad);
   }
 };
@@ -63,7 +66,8 @@ struct KExponential {
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     return bfmm_nf::bfmm_exp(-sqrt(dx * dx + dy * dy + dz * dz));
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &bad) {
+  template <class F>
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, F &bad) {
     return bfmm_nf::bfmm_exp_fast(-sqrt(dx * dx + dy * dy + dz * dz), bad);
   }
 };
@@ -73,7 +77,8 @@ struct KLogarithm {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : 0.5 * log(r2);
   }
-  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, bool &) {
+  template <class F>
+  __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, F &) {
     return eval(dx, dy, dz);
   }
 };
@@ -139,8 +144,8 @@ std::string functor_source(int kind, const char *expr) {
   return "#define exp(x) bfmm_exp(x)\nstruct KUser {\n __device__ __forceinline__ "
          "static double eval(double dx, double dy, double dz) {\n " +
          body + "\n }\n#undef exp\n#define exp(x) bfmm_exp_fast(x, bfmm_bad_)\n"
-         " __device__ __forceinline__ static double eval_fast(double dx, double dy, "
-         "double dz, bool &bfmm_bad_) {\n " + body + "\n }\n#undef exp\n};\n";
+         " template <class F> __device__ __forceinline__ static double eval_fast(double dx, "
+         "double dy, double dz, F &bfmm_bad_) {\n " + body + "\n }\n#undef exp\n};\n";
 }
 
 int jit_compile(int kind, const char *expr, int *handle) {
