@@ -244,6 +244,18 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
       const int64_t i = s0 + c0 + (have ? lane : 0);
       double wz[P];
       const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+      // column 0's locals are loaded into registers before the weights are
+      // evaluated, so the global-memory latency overlaps that arithmetic
+      constexpr int NL = (P3 + 31) / 32;
+      double lpre[NL];
+      {
+        const double *src0 = locals + (cell * m) * (int64_t)P3;
+#pragma unroll
+        for (int u = 0; u < NL; ++u) {
+          const int e = lane + 32 * u;
+          lpre[u] = e < P3 ? src0[e] : 0.0;
+        }
+      }
       {
         double wx[P], wy[P];
         weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, inv_hw, cx, flag), wx);
@@ -257,8 +269,16 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
       weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
       for (int c = 0; c < m; ++c) {
         __syncwarp();
-        const double *src = locals + (cell * m + c) * (int64_t)P3;
-        for (int e = lane; e < P3; e += 32) sL[wid][e] = src[e];
+        if (c == 0) {
+#pragma unroll
+          for (int u = 0; u < NL; ++u) {
+            const int e = lane + 32 * u;
+            if (e < P3) sL[wid][e] = lpre[u];
+          }
+        } else {
+          const double *src = locals + (cell * m + c) * (int64_t)P3;
+          for (int e = lane; e < P3; e += 32) sL[wid][e] = src[e];
+        }
         __syncwarp();
         const double *L = sL[wid];
         // one partial sum per x node a (P independent chains), added in a
