@@ -392,8 +392,9 @@ static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int 
     if (check_launch("reduce_splits_kernel")) return 1;
   }
   const int64_t lda = (int64_t)a_splits * K;
-  // one CTA spans all N <= 128 columns, so A is read once
-  const int wn = N > 64 ? 2 : 1;
+  // one CTA spans all N <= 128 columns, so A is read once -- unless that
+  // leaves most SMs idle (small levels): then 64-column tiles, twice the CTAs
+  const int wn = (N > 64 && ceil_div(rows, kPjTM) >= kNumSMs) ? 2 : 1;
   dim3 grid((unsigned)ceil_div(rows, kPjTM), (unsigned)ceil_div(N, 64 * wn));
   static bool attr = false;
   if (!attr) {
