@@ -544,7 +544,10 @@ extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp,
 }
 
 extern "C" int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq) {
-  (void)level;
+  if (level <= 3) {  // mixed-octant rows, 316 offsets (m2l_i8_kernel)
+    const int64_t ctas = ceil_div(8 * nq * m, kI8TM) * ceil_div(rp, kI8TN);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(79, ceil_div(kNumSMs, ctas)));
+  }
   const int64_t ctas = ceil_div(nq * m, kI8TM) * ceil_div(rp, kI8TN) * 8;
   const double slots = kNumSMs;  // one CTA per SM (TMEM 512 columns, ~215 KB smem)
   if (ctas * 4 < slots) return (int)std::min<int64_t>(189, ceil_div(4 * (int64_t)slots, ctas));
@@ -570,8 +573,8 @@ static int i8_check(const char *fn, int level, int m, int rp, int S, int nsplit)
     set_error("%s: rp=%d (multiple of 8, <= 256), level=%d, S=%d (5..8)", fn, rp, level, S);
     return 2;
   }
-  if (nsplit < 1 || nsplit > 189) {
-    set_error("%s: nsplit=%d outside [1, 189]", fn, nsplit);
+  if (nsplit < 1 || nsplit > 316) {
+    set_error("%s: nsplit=%d outside [1, 316]", fn, nsplit);
     return 2;
   }
   return 0;

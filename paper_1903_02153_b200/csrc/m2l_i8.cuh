@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
               const int8_t *__restrict__ cs, const double *__restrict__ cpow,
               double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
-              int nsplit, int64_t q_lo, int64_t nq, OctList act) {
+              int nsplit, int64_t q_lo, int64_t nq, OctList act, int mixed) {
   using Sh = I8Shape<S>;
   constexpr int NS = Sh::NS;
   extern __shared__ __align__(1024) uint8_t smi[];
@@ -130,14 +130,24 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
   uint64_t *done = empty + NS;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
-  const int o = blockIdx.z & 7;
-  const int split = blockIdx.z >> 3;
-  const int per = (189 + nsplit - 1) / nsplit;
-  const int v_lo = split * per, v_hi = min(189, v_lo + per);
+  // mixed (coarse levels): one row per cell of all eight octants, all 316
+  // offsets, the parity rule applied per row (zero rows) -- a level with a few
+  // cells per octant then fills one tile instead of eight nearly empty ones
+  const int o = mixed ? 0 : (blockIdx.z & 7);
+  const int split = mixed ? blockIdx.z : (blockIdx.z >> 3);
+  const int ntap = mixed ? 316 : 189;
+  const int per = (ntap + nsplit - 1) / nsplit;
+  const int v_lo = split * per, v_hi = min(ntap, v_lo + per);
   const int nt = blockIdx.y;
   const int n = 1 << level;
   const int64_t *ocells = act.cells ? act.cells + act.off[o] : nullptr;
-  const int64_t rows = (act.cells ? act.off[o + 1] - act.off[o] : nq) * m;
+  const int64_t rows = mixed ? 8 * nq * m : (act.cells ? act.off[o + 1] - act.off[o] : nq) * m;
+  auto cell_of = [&](int64_t q) -> int64_t {  // q-th cell of this CTA's row set
+    return mixed ? 8 * q_lo + q : (ocells ? ocells[q] : 8 * (q_lo + q) + o);
+  };
+  auto orow_of = [&](int64_t q) -> int64_t {  // its lt row
+    return mixed ? 8 * q_lo + q : (ocells ? act.off[o] + q : 8 * (q_lo + q) + o);
+  };
   const int64_t row0 = int64_t(blockIdx.x) * kI8TM;
   if (row0 >= rows) return;  // whole CTA
   // (cell indices are 30-bit Morton codes: levels <= 10, checked by the caller)
@@ -150,7 +160,7 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
       if (r >= rows || col >= rp) continue;
       const int64_t q = r / m;
       const int c = (int)(r - q * m);
-      const int64_t orow = ocells ? act.off[o] + q : 8 * (q_lo + q) + o;
+      const int64_t orow = orow_of(q);
       lt[((orow * m + c) * nsplit + split) * rp + col] = 0.0;
     }
     return;
@@ -235,7 +245,7 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
     if (rok) {
       const int64_t q = r / m;
       colm = (int)(r - q * m);
-      const int64_t cell = ocells ? ocells[q] : 8 * (q_lo + q) + o;
+      const int64_t cell = cell_of(q);
       cd = (uint32_t)cell;
       unmorton3((uint64_t)cell, cx, cy, cz);
     }
@@ -247,11 +257,16 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
     int s = 0, sl = 0, step = 0;
     uint32_t ph = 0;
     for (int vi = v_lo; vi < v_hi; ++vi) {
-      const int t = c_valid[o][vi];
-      // the octant's parity already admits t; only the grid bounds remain
+      const int t = mixed ? vi : c_valid[o][vi];
+      // the octant's parity already admits t (octant mode); only the grid
+      // bounds remain -- mixed rows check the full rule
       const int sx = cx + c_offsets[t][0], sy = cy + c_offsets[t][1], sz = cz + c_offsets[t][2];
       int srow = -1;
-      if (rok && (unsigned)sx < (unsigned)n && (unsigned)sy < (unsigned)n && (unsigned)sz < (unsigned)n) {
+      const bool ok = mixed ? far_pair(n, cx, cy, cz, c_offsets[t][0], c_offsets[t][1],
+                                       c_offsets[t][2])
+                            : ((unsigned)sx < (unsigned)n && (unsigned)sy < (unsigned)n &&
+                               (unsigned)sz < (unsigned)n);
+      if (rok && ok) {
         const uint32_t sc = (((cd | ~MX) + c_dil[t][0]) & MX) | (((cd | ~MY) + c_dil[t][1]) & MY) |
                             (((cd | ~MZ) + c_dil[t][2]) & MZ);
         srow = (int)sc * m + colm;
@@ -316,7 +331,7 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
     if (orr < rows) {
       const int64_t q = orr / m;
       const int c = (int)(orr - q * m);
-      const int64_t orow = ocells ? act.off[o] + q : 8 * (q_lo + q) + o;
+      const int64_t orow = orow_of(q);
       dst = lt + ((orow * m + c) * nsplit + split) * rp;
       zsc = i8_zscale(zmax[c]);
     }
@@ -679,6 +694,12 @@ struct I8Call {
   cudaStream_t st;
 };
 
+// coarse dense levels (<= 512 cells): one mixed-octant row set, all 316
+// offsets (see m2l_i8_kernel); BFMM_I8_OCTANT (diagnostic) forces octant mode
+inline bool i8_mixed_ok(const I8Call &a) {
+  return !a.act.cells && a.level <= 3 && !getenv("BFMM_I8_OCTANT");
+}
+
 template <int S>
 int launch_i8(const I8Call &a) {
   using Sh = I8Shape<S>;
@@ -688,16 +709,17 @@ int launch_i8(const I8Call &a) {
                          (int)Sh::smem);
     attr_set = true;
   }
-  int64_t rows = a.nq * a.m;
+  const int mixed = i8_mixed_ok(a) ? 1 : 0;
+  int64_t rows = mixed ? 8 * a.nq * a.m : a.nq * a.m;
   if (a.act.cells) {
     rows = 0;
     for (int o = 0; o < 8; ++o) rows = std::max(rows, (a.act.off[o + 1] - a.act.off[o]) * a.m);
   }
   if (rows <= 0) return 0;
-  dim3 grid((unsigned)ceil_div(rows, kI8TM), (unsigned)a.ntn, 8 * a.nsplit);
+  dim3 grid((unsigned)ceil_div(rows, kI8TM), (unsigned)a.ntn, (mixed ? 1 : 8) * a.nsplit);
   m2l_i8_kernel<S><<<grid, kI8Threads, Sh::smem, a.st>>>(
       a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, a.q_lo,
-      a.nq, a.act);
+      a.nq, a.act, mixed);
   return check_launch("m2l_i8_kernel");
 }
 
