@@ -623,13 +623,23 @@ __global__ void absmax_bits_kernel(const double *__restrict__ z, int64_t rows, i
   const int64_t nr = (rows - c + m - 1) / m;
   const int64_t n = nr * rp;
   unsigned long long mx = 0;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / rp;
-    const int k = (int)(e - i * rp);
-    const unsigned long long b =
-        (unsigned long long)__double_as_longlong(z[(c + i * m) * rp + k]) & 0x7fffffffffffffffull;
-    mx = b > mx ? b : mx;
+  if (m == 1) {  // one column: the whole array, no index arithmetic
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+      const unsigned long long b =
+          (unsigned long long)__double_as_longlong(z[e]) & 0x7fffffffffffffffull;
+      mx = b > mx ? b : mx;
+    }
+  } else {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+      const int64_t i = e / rp;
+      const int k = (int)(e - i * rp);
+      const unsigned long long b =
+          (unsigned long long)__double_as_longlong(z[(c + i * m) * rp + k]) &
+          0x7fffffffffffffffull;
+      mx = b > mx ? b : mx;
+    }
   }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) {
@@ -650,13 +660,15 @@ __global__ void z_slice_kernel(const double *__restrict__ z, int64_t rows, int r
                                int m, const unsigned long long *__restrict__ zmax,
                                int8_t *__restrict__ zs) {
   const int64_t total = rows * kc_n * 2;
+  const unsigned per_row = (unsigned)(kc_n * 2);
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t row = e / (kc_n * 2);
-    const int rem = (int)(e - row * (kc_n * 2));
+    // 32-bit division when the index fits (every level up to 2^31 chunks)
+    const int64_t row = total <= 0xffffffffll ? (int64_t)((unsigned)e / per_row) : e / per_row;
+    const int rem = (int)(e - row * per_row);
     const int kc = rem >> 1, h = rem & 1;
     const int k0 = kc * 32 + h * 16;
-    const double amax = __longlong_as_double((long long)zmax[row % m]);
+    const double amax = __longlong_as_double((long long)zmax[m == 1 ? 0 : row % m]);
     int ez = 0;
     if (amax > 0 && amax <= 1.7976931348623157e308) frexp(amax, &ez);
     const double inv = ldexp(1.0, 6 - ez);  // first digit: x * 2^(6 - ez) in [-64, 64]
