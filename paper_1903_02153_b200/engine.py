@@ -728,13 +728,26 @@ class FmmEvaluator:
         near_ready = torch.cuda.Event()
         near_ready.record(main)  # trees and weights: all the near field needs
 
+        pairs_counted = False
+
+        def count_pairs():
+            # timings["near_pairs"] (reference engine.py:532): status int64 slot 4
+            _native.check(self.lib.bfmm_near_pair_count(
+                ttree.leaves.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
+                ttree.max_leaves, stree.cell_count.data_ptr(), self.plan.levels,
+                status.view(torch.int64)[4:5].data_ptr(), self._stream()),
+                "bfmm_near_pair_count")
+
         def near_on_side():
             # near field on a side stream, concurrent with the far field (for
             # a shard: computes while the level all-gathers are in flight)
+            nonlocal pairs_counted
             side = self._side_stream(1)
             side.wait_event(near_ready)
             with torch.cuda.stream(side):
                 self._near_field(ttree, stree, ws, m, near, shard)
+                count_pairs()  # off the far field's critical path
+            pairs_counted = True
             return side
 
         overlap = self.overlap_near or (sharded and self.overlap_near_sharded)
@@ -778,11 +791,8 @@ class FmmEvaluator:
             phi_far.data_ptr() if phi_far is not None else None, near.data_ptr(),
             ttree.perm.data_ptr(), n_tgt, m, phi.data_ptr(), status[_ST_NONFINITE:].data_ptr(), st),
             "bfmm_scatter_output")
-        pairs_dev = status.view(torch.int64)[4:5]
-        _native.check(self.lib.bfmm_near_pair_count(
-            ttree.leaves.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
-            ttree.max_leaves, stree.cell_count.data_ptr(), self.plan.levels,
-            pairs_dev.data_ptr(), st), "bfmm_near_pair_count")
+        if not pairs_counted:
+            count_pairs()
         if sharded:
             _shard[1].allreduce_sum(phi)  # every rank wrote only its own targets
         if ev:
