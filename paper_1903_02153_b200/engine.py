@@ -177,8 +177,10 @@ class FmmEvaluator:
         # P2M / L2P: warp per leaf ("warp"), thread per (leaf, node) / point
         # ("point"), or "auto" (thread-per-point L2P for sparse clouds)
         self.l2p_mode = "auto"
-        # coarse far-field levels on a side stream (see _far_field)
+        # coarse far-field levels on a side stream (see _far_field); the
+        # finest main_levels levels stay on the calling stream
         self.stream_levels = True
+        self.main_levels = 2
         self._side = None
         self.kernel_ms = {}
         self._kpending = []
@@ -452,7 +454,7 @@ class FmmEvaluator:
         L = self.plan.levels
         active = active or {}
         locs = {}
-        coarse = list(range(2, L - 1)) if (self.stream_levels and shard is None) else []
+        coarse = list(range(2, L - self.main_levels + 1)) if (self.stream_levels and shard is None) else []
         if coarse:
             main = torch.cuda.current_stream()
             side = self._side_stream()
