@@ -240,7 +240,8 @@ def m2l_i8_ops(lev, rp, m, S):
     offset, 32-wide k chunk, 64-wide rank tile) stage, S(S+1)/2 digit
     products of 128 x 64 x 32 (csrc/m2l_i8.cuh).  Dense levels >= 4 use the
     plane kernel, which skips offset groups whose source planes leave the
-    grid; the gather kernel runs all 189 (zero rows)."""
+    grid; coarser levels run all 316 offsets over mixed-octant row tiles
+    (zero rows where the parity rule or the grid excludes a pair)."""
     n = 1 << lev
     kc, ntn = -(-rp // 32), -(-rp // 64)
     per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
@@ -257,9 +258,9 @@ def m2l_i8_ops(lev, rp, m, S):
                 # a group (offsets sharing t_x) runs when any x slot's plane is inside
                 live = sum(1 for t in offs if xs + t[0] + 2 * (xt - 1) >= 0 and xs + t[0] < n)
                 stages += live * (h // yt) * (h // 8)
-    else:
-        stages = -(-(n ** 3 // 8 * m) // 128) * 8 * 189
-    return stages * kc * ntn * m * per_stage if lev >= 4 else stages * kc * ntn * per_stage
+    else:  # levels <= 3: one mixed-octant row set over all 316 offsets
+        stages = -(-(n ** 3 * m) // 128) * 316
+    return stages * kc * ntn * (m if lev >= 4 else 1) * per_stage
 
 
 def run_ours(args, rank, world, local_rank):
