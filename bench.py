@@ -2,35 +2,50 @@
 """FMM matvec throughput (points/s, fp64) on B200 — the BASELINE.json metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2] [--no-cpu-baseline] [--no-graph]
+                    [--config C5] [--secondary C2|none] [--no-cpu-baseline]
 
-Workload (N=1): BASELINE.json configs[1] = C2 (Gaussian exp(-(r/0.2)^2),
-N = 1,000,000 uniform in [-1,1]^3, L=5, Chebyshev p=5, eps 1e-7, 1 RHS),
-seeded synthetic inputs; the other configs are parity
-cases (tests/).  A step is one full matvec phi = K sigma: tree build, P2M,
-M2M, M2L, L2L, L2P, P2P, output scatter.
+Workload (N=1): C5 of BASELINE.json — Laplace 1/r, N = 64,000,000 i.i.d.
+uniform in [-1,1]^3, octree L=8, Chebyshev p=5, 1 RHS — the configuration
+the metric ("points/s at 1/2/4/8 B200") is quoted on: the only config
+defined as a 1/2/4/8-GPU run, and the largest that fits one B200 (71 GB
+peak).  Inputs are the seeded synthetic recipe of SURVEY.md §8(d) (no public
+dataset is involved; the paper itself uses uniform random clouds).  A step
+is one full matvec phi = K sigma: tree build, P2M, M2M, M2L, L2L, L2P, P2P,
+output scatter.  ``--config C1..C5`` runs any other config the same way;
+``--secondary C2`` (default) adds a short C2 measurement (the P2P-dominated
+config) to the same JSON line under "secondary".
 
-* value     device-resident inputs, CUDA-event time of K steps, L2 flushed
-            (256 MiB write) between steps outside the timed spans.
-* e2e       the public API on pinned host tensors: H2D of points + weights,
-            the matvec, D2H of phi, every step.
-* roofline  the dominant kernel (largest share of the step), timed live
-            with CUDA events on its launching stream; FP64 peak measured live
-            (DMMA/DFMA microbenchmarks in libbfmm.so: MEASURED_PEAKS.json has
-            no FP64 entry).
-* cpu_baseline  the CPU oracle (oracle/fmm_oracle.py, a NumPy restatement of
-            the reference's engine with its thread pool) on the same C2
-            inputs, timed on this host's cores, rank 0 at N=1 only.
-* --impl reference  the same oracle as the reference arm (the reference is
-            pure Python and not present on the GPU box; the oracle is pinned
-            to its outputs by tests/test_oracle_golden.py).
-* N > 1: target leaves are split by Morton range across ranks (one process
-  per GPU, NCCL); each rank evaluates its share, phi is all-gathered.
+* value     device-resident inputs, CUDA-event time of K steps (barrier +
+            synchronize on both sides, max over ranks); inputs are larger
+            than L2 (C5: 2 GB) and L2 is flushed anyway (256 MiB write)
+            between steps, outside the timed spans.
+* e2e       the public API (FmmEvaluator.evaluate) on pinned host tensors:
+            H2D of points + weights, the matvec, D2H of phi, every step.
+  e2e_numpy the same through NumPy arrays (the reference's calling
+            convention): pageable inputs staged through the evaluator's
+            reusable pinned buffer.
+* roofline  the dominant kernel (largest share of the step in a separate
+            pass with CUDA events around every launch on its stream, the
+            far-field levels and the near field serialised).  C5: the level-8
+            int8 tcgen05 M2L against the measured kind::i8 peak (useful ops,
+            executed ops beside); P2P against the measured DFMA peak;
+            FFT M2L (C3) in Hadamard flops against the DFMA peak.
+* cpu_baseline  the unmodified reference (boxfmm, installed under
+            baseline/_ref by scripts/install_reference.sh) with every host
+            core, on a bounded sample of the same workload: the
+            density-preserving C5/512 (N = 125,000, L = 5, same kernel,
+            order and points per leaf), rank 0 at N=1 only.
+* --impl reference  the same reference run as the reference arm: per step
+            one evaluate of that sample, all host threads, rank 0 only.
+* N > 1: torchrun ranks (or ``--gpus N`` spawns them itself), NCCL; target
+  cells split by Morton range (strong scaling: N = 64M in total), z of
+  each level exchanged, each rank's phi range all-gathered.
 """
 
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
@@ -46,25 +61,62 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FMM matvec points/sec (fp64) at 1/2/4/8 B200; P2P & M2L % of roofline"
 
-# FP64 flops per near-field pair interaction, frozen from ncu instruction
-# counts of the P2P kernel (2*DFMA + DMUL + DADD thread instructions / pair,
-# profiles/r01_p2p_flops.txt); kernel-specific.
+# FP64 flops per near-field pair interaction, per kernel functor: the FP64
+# thread instructions the P2P kernel executes per pair (2*DFMA + DMUL + DADD,
+# ncu smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum over
+# the pair count), frozen once (profiles/r01_p2p_flops.txt for gauss02,
+# profiles/r02_p2p_flops.txt for the others); plus 2m for the weight FMAs
+# beyond the first column (the figure is per single-column pair).
 P2P_FLOPS_PER_PAIR = {"gauss02": 40.0}
+NOMINAL_FP64_TF = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: DFMA/clk/SM x SMs x clock
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--secondary", default="C2", help="second config measured into the same "
+                    "line ('none' to skip); N=1 only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--balance", default="auto", choices=["auto", "cells", "work"],
                     help="N>1 shard ranges: equal cell ranges, work-weighted, or auto "
                          "(work-weighted for the clustered C4)")
-    return ap.parse_args()
+    ap.add_argument("--ref-scale", type=int, default=None,
+                    help="reference sample: the config scaled by 8^-k (default C5: 3, C4: 2, "
+                         "C3: 2, C2: 1, C1: 0)")
+    return ap.parse_args(argv)
+
+
+# ---------------------------------------------------------------------------
+def _workloads():
+    """paper_1903_02153_b200/workloads.py loaded on its own (NumPy only): the
+    reference arm must not import the package (its library, its engine)."""
+    spec = importlib.util.spec_from_file_location(
+        "_bfmm_workloads", os.path.join(ROOT, "paper_1903_02153_b200", "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+REF_SCALE = {"C1": 0, "C2": 1, "C3": 2, "C4": 2, "C5": 3}
+
+
+def config_of(name):
+    W = _workloads()
+    N, L, p, scheme, eps, kern, m = W.CONFIGS[name]
+    return {"workload": f"{name}: {W.DESCRIPTION[name]}", "n_points": N, "levels": L,
+            "order": p, "scheme": scheme, "eps": eps, "kernel": kern, "ncols": m,
+            "l2": "inputs larger than L2 where the config has them; L2 flushed between "
+                  "steps anyway (256 MiB write, outside the timed spans)"}
+
+
+def config_dict(wl):
+    return config_of(wl["name"])
 
 
 class ClockSampler:
@@ -117,30 +169,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(name):
-    from paper_1903_02153_b200 import workloads
-    return workloads.make(name)
-
-
-def config_dict(wl):
-    from paper_1903_02153_b200 import workloads
-    return {"workload": f"{wl['name']}: {workloads.DESCRIPTION[wl['name']]}",
-            "n_points": int(wl["points"].shape[0]), "levels": wl["levels"],
-            "order": wl["order"], "scheme": wl["scheme"], "eps": wl["eps"],
-            "kernel": wl["kernel"], "ncols": wl["ncols"],
-            "l2": "flushed between steps (256 MiB write, outside the timed spans)"}
-
-
-def oracle_step(wl, threads):
-    from oracle import fmm_oracle as O
-    from paper_1903_02153_b200.kernel import workload_kernel
-    fmm = O.OracleFMM(workload_kernel(wl["kernel"]), wl["levels"], wl["order"],
-                      wl["scheme"], wl["eps"], wl["center"], wl["length"], threads=threads)
-    t0 = time.perf_counter()
-    fmm.matvec(wl["points"], weights=wl["weights"])
-    return time.perf_counter() - t0
-
-
 def cpu_threads():
     try:
         import psutil
@@ -149,82 +177,124 @@ def cpu_threads():
         return max(1, os.cpu_count() or 1)
 
 
+# ---------------------------------------------------------------------------
+# the reference (unmodified boxfmm from baseline/_ref)
+def _import_reference():
+    path = os.environ.get("BOXFMM_SRC", os.path.join(ROOT, "baseline", "_ref"))
+    if not os.path.isdir(os.path.join(path, "boxfmm")):
+        return None, f"reference not installed at {path} (scripts/install_reference.sh)"
+    sys.path.insert(0, path)
+    import boxfmm
+    return boxfmm, None
+
+
+def _ref_kernel(boxfmm, key):
+    if key == "gauss02":
+        return boxfmm.KernelSpec("gauss02", homogen=0.0, symmetry=1,
+                                 profile=lambda r: np.exp(-(r / 0.2) ** 2))
+    if key == "exp03":
+        return boxfmm.KernelSpec("exp03", homogen=0.0, symmetry=1,
+                                 profile=lambda r: np.exp(-r / 0.3))
+    return boxfmm.kernel_by_name(key)
+
+
+class ReferenceSample:
+    """One reference evaluate of the density-preserving scaled config (the
+    bounded CPU sample), warm operator cache, `threads` host threads."""
+
+    def __init__(self, config, scale, threads):
+        boxfmm, err = _import_reference()
+        if boxfmm is None:
+            raise RuntimeError(err)
+        self.wl = _workloads().make(config, scale)
+        wl = self.wl
+        plan = boxfmm.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"],
+                              eps=wl["eps"], domain_center=wl["center"],
+                              domain_length=wl["length"], n_cols=wl["ncols"])
+        self.ev = boxfmm.FmmEvaluator(_ref_kernel(boxfmm, wl["kernel"]), plan,
+                                      cache_dir="/tmp/bfmm_ref_cache", threads=threads)
+        self.threads = threads
+        self.n = int(wl["points"].shape[0])
+        self.desc = (f"{config}/{8 ** scale} (N={self.n:,}, L={wl['levels']}, same kernel, "
+                     f"order, scheme and points per leaf): one boxfmm.FmmEvaluator("
+                     f"threads={threads}).evaluate per step, warm operator cache")
+
+    def step(self):
+        t0 = time.perf_counter()
+        self.ev.evaluate(self.wl["points"], weights=self.wl["weights"])
+        return time.perf_counter() - t0
+
+
 def run_reference(args, rank, world):
-    """Reference arm: the CPU oracle (reference algorithm, NumPy, thread pool)
-    on the host cores; rank 0 only."""
+    """Reference arm: the unmodified reference's CPU path, rank 0 only."""
     if rank != 0:
         return
-    wl = make_workload(args.config)
+    cfg = args.config
+    scale = REF_SCALE.get(cfg, 0) if args.ref_scale is None else args.ref_scale
     threads = cpu_threads()
+    try:
+        ref = ReferenceSample(cfg, scale, threads)
+    except RuntimeError as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}), flush=True)
+        return
     for _ in range(args.warmup):
-        oracle_step(wl, threads)
-    times = [oracle_step(wl, threads) for _ in range(args.steps)]
+        ref.step()
+    times = [ref.step() for _ in range(args.steps)]
     total = sum(times)
-    n = wl["points"].shape[0]
-    value = n * args.steps / total
+    value = ref.n * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SURVEY.md §8(d) recipe)",
-        "config": config_dict(wl),
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
-                         "sample": f"full {args.config} matvec per step (oracle/fmm_oracle.py)"},
+        "config": config_of(cfg),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads,
+                         "kind": "reference", "sample": ref.desc},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_timings_s": {k: round(float(v), 4) for k, v in ref.ev.timings.items()},
     }
     print(json.dumps(line), flush=True)
 
 
-def fp64_peaks(lib, stream):
-    import ctypes as C
-    g1, g2 = C.c_double(0), C.c_double(0)
-    lib.bfmm_device_fp64_probe(C.byref(g1), stream)
-    lib.bfmm_device_dmma_probe(C.byref(g2), stream)
-    return g1.value / 1e3, g2.value / 1e3  # TFLOP/s
-
-
-def committed_traffic(config, kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/r01_traffic.json), or None when that kernel was not captured."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
-    try:
-        with open(path) as f:
-            rec = json.load(f).get(config, {}).get(kernel)
-    except (OSError, ValueError):
-        return None
-    return None if rec is None else rec["bytes"]
+# ---------------------------------------------------------------------------
+# algorithmic work (SURVEY.md §8(d))
+def level_pairs(lev):
+    """P_l: (target, source) M2L cell pairs over the full level (oct:128-145)."""
+    from paper_1903_02153_b200.tables import OFFSETS
+    n = 1 << lev
+    cnt = 0
+    for t in OFFSETS:
+        c = 1
+        for a in range(3):
+            tt = int(t[a])
+            lo, hi = max(0, -tt), min(n - 1, n - 1 - tt)
+            if abs(tt) == 3:
+                k = len([x for x in range(lo, hi + 1) if (x % 2 == 0) == (tt > 0)])
+            else:
+                k = max(0, hi - lo + 1)
+            c *= k
+        cnt += c
+    return cnt
 
 
 def m2l_flops(ev, wl):
-    """Algorithmic M2L flops per level: pairs P_l * 2 r_l^2 * m."""
-    from paper_1903_02153_b200.tables import OFFSETS
-    out = {}
+    """Algorithmic Chebyshev M2L flops per level: P_l * 2 r_l^2 * m."""
     m = wl["ncols"]
-    for lev in range(2, wl["levels"] + 1):
-        n = 1 << lev
-        pairs = 1
-        cnt = 0
-        for t in OFFSETS:
-            c = 1
-            for a in range(3):
-                tt = int(t[a])
-                lo, hi = max(0, -tt), min(n - 1, n - 1 - tt)
-                k = max(0, hi - lo + 1)
-                if abs(tt) == 3:
-                    k = len([x for x in range(lo, hi + 1) if (x % 2 == 0) == (tt > 0)])
-                c *= k
-            cnt += c
-        blk = ev.table.block_for_level(lev)
-        r = blk.rank
-        out[lev] = cnt * 2.0 * r * r * m
-        del pairs
-    return out
+    return {lev: level_pairs(lev) * 2.0 * ev.table.block_for_level(lev).rank ** 2 * m
+            for lev in range(2, wl["levels"] + 1)}
+
+
+def fft_flops(wl):
+    """Uniform M2L Hadamard flops per level: P_l * F * m * 8 (F = q^2 (q/2+1)
+    complex bins, 8 flops per complex MAC)."""
+    q = 2 * wl["order"] - 1
+    F = q * q * (q // 2 + 1)
+    return {lev: level_pairs(lev) * F * wl["ncols"] * 8.0 for lev in range(2, wl["levels"] + 1)}
 
 
 def _valid_offsets(o):
-    """The 189 offsets a child octant admits (octree.py:128-145 parity rule)."""
     from paper_1903_02153_b200.tables import OFFSETS
     bits = ((o >> 2) & 1, (o >> 1) & 1, o & 1)
     out = []
@@ -240,8 +310,7 @@ def m2l_i8_ops(lev, rp, m, S):
     offset, 32-wide k chunk, 64-wide rank tile) stage, S(S+1)/2 digit
     products of 128 x 64 x 32 (csrc/m2l_i8.cuh).  Dense levels >= 4 use the
     plane kernel, which skips offset groups whose source planes leave the
-    grid; coarser levels run all 316 offsets over mixed-octant row tiles
-    (zero rows where the parity rule or the grid excludes a pair)."""
+    grid; coarser levels run all 316 offsets over mixed-octant row tiles."""
     n = 1 << lev
     kc, ntn = -(-rp // 32), -(-rp // 64)
     per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
@@ -255,242 +324,380 @@ def m2l_i8_ops(lev, rp, m, S):
             offs = _valid_offsets(o)
             for xb in range(h // xt):
                 xs = 2 * xb * xt + ox
-                # a group (offsets sharing t_x) runs when any x slot's plane is inside
                 live = sum(1 for t in offs if xs + t[0] + 2 * (xt - 1) >= 0 and xs + t[0] < n)
                 stages += live * (h // yt) * (h // 8)
-    else:  # levels <= 3: one mixed-octant row set over all 316 offsets
-        stages = -(-(n ** 3 * m) // 128) * 316
-    return stages * kc * ntn * (m if lev >= 4 else 1) * per_stage
+        return stages * kc * ntn * m * per_stage
+    stages = -(-(n ** 3 * m) // 128) * 316
+    return stages * kc * ntn * per_stage
 
 
-def run_ours(args, rank, world, local_rank):
+def committed_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu captures
+    (profiles/r02_traffic.json, else r01), or None when not captured."""
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(path) as f:
+                rec = json.load(f).get(config, {}).get(kernel)
+        except (OSError, ValueError):
+            rec = None
+        if rec is not None:
+            return rec["bytes"]
+    return None
+
+
+def device_peaks(lib, stream):
     import ctypes as C
-    import torch
+    g1, g2, g3 = C.c_double(0), C.c_double(0), C.c_double(0)
+    lib.bfmm_device_fp64_probe(C.byref(g1), stream)
+    lib.bfmm_device_dmma_probe(C.byref(g2), stream)
+    lib.bfmm_device_i8_probe(C.byref(g3), stream)
+    return {"dfma_tflops": g1.value / 1e3, "dmma_tflops": g2.value / 1e3,
+            "i8_tops": g3.value}
 
+
+# ---------------------------------------------------------------------------
+def _evaluator(wl, device):
     import paper_1903_02153_b200 as bf
-    from paper_1903_02153_b200 import _native
     from paper_1903_02153_b200.kernel import workload_kernel
-
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    wl = make_workload(args.config)
     plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"],
                       eps=wl["eps"], domain_center=wl["center"], domain_length=wl["length"],
                       n_cols=wl["ncols"])
-    kernel = workload_kernel(wl["kernel"])
-    ev = bf.FmmEvaluator(kernel, plan, cache_dir=os.path.join("/tmp", "bfmm_bench_cache"))
-    # whole device step replayed from a CUDA graph (FmmEvaluator.use_graph;
-    # captured during warm-up, eager path for the per-kernel timing pass)
+    return bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan,
+                           cache_dir=os.path.join("/tmp", "bfmm_bench_cache"), device=device)
+
+
+def _max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measure(cfg, args, rank, world, local_rank, dist, lib, peaks, steps, warmup,
+            with_e2e=True):
+    """Everything of one config's bench line except the CPU baseline."""
+    import torch
+    W = _workloads()
+    wl = W.make(cfg)
+    ev = _evaluator(wl, torch.device("cuda", local_rank))
     ev.use_graph = not args.no_graph
-    lib = _native.load()
-    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    n = wl["points"].shape[0]
-    m = wl["ncols"]
+    n, m = wl["points"].shape[0], wl["ncols"]
     X = torch.from_numpy(wl["points"]).cuda()
-    W = torch.from_numpy(np.ascontiguousarray(wl["weights"])).cuda()
+    Wt = torch.from_numpy(np.ascontiguousarray(wl["weights"])).cuda()
     if world > 1:
         from paper_1903_02153_b200.parallel import ShardedEvaluator
-        balance = args.balance if args.balance != "auto" else (
-            "work" if args.config == "C4" else "cells")
+        balance = args.balance if args.balance != "auto" else ("work" if cfg == "C4" else "cells")
         runner = ShardedEvaluator(ev, dist, balance=balance)
-        step = lambda x, w: runner.evaluate(x, weights=w)  # noqa: E731
     else:
         runner = ev
-        step = lambda x, w: ev.evaluate(x, weights=w)  # noqa: E731
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    def measure_e2e():
-        # ---- e2e through the public API with pinned host tensors ----
-        Xh = torch.from_numpy(wl["points"]).pin_memory()
-        Wh = torch.from_numpy(np.ascontiguousarray(wl["weights"])).pin_memory()
-        phi = None
-        for _ in range(max(3, args.warmup)):
-            # keep the previous result alive, as in the timed loop, so both pinned
-            # output blocks of the host caching allocator exist before timing
-            phi = runner.evaluate(Xh, weights=Wh)
+    def barrier():
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
-        e2e_ms = []
-        for _ in range(args.steps):
+        torch.cuda.synchronize()
+
+    def host_timed(make_inputs, tag):
+        xs, ws = make_inputs()
+        for _ in range(max(3, warmup)):
+            phi = runner.evaluate(xs, weights=ws)
+        barrier()
+        ms = []
+        for _ in range(steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            phi = runner.evaluate(Xh, weights=Wh)
-            assert phi.device.type == "cpu"
-            e2e_ms.append(1e3 * (time.perf_counter() - t0))
-        e2e_total = float(sum(e2e_ms))
-        if dist is not None:
-            t = torch.tensor([e2e_total], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_total = float(t.item())
-        e2e_value = n * args.steps / (e2e_total * 1e-3)
-        return Xh, Wh, e2e_ms, e2e_total, e2e_value
+            phi = runner.evaluate(xs, weights=ws)
+            assert not (hasattr(phi, "is_cuda") and phi.is_cuda), tag
+            ms.append(1e3 * (time.perf_counter() - t0))
+        barrier()
+        total = _max_over_ranks(dist, float(sum(ms)))
+        del phi
+        return {"value": n * steps / (total * 1e-3), "unit": "points/s",
+                "ms_per_step": total / steps, "step_ms": [round(x, 3) for x in ms]}
 
-    # measured first: after the device-resident loop below the same calls took
-    # 3.7-4.4 ms instead of 3.5 on some boxes (a process-state effect we could
-    # not pin down: not the pinned-copy bandwidth, which stays at ~54 GB/s)
-    Xh, Wh, e2e_ms, e2e_total, e2e_value = measure_e2e()
-    for _ in range(args.warmup):
-        step(X, W)
-    torch.cuda.synchronize()
+    e2e = e2e_np = None
+    if with_e2e:
+        # measured before the device-resident loop (round-1 note: after it the
+        # same calls ran slower on some boxes, a process-state effect)
+        def pinned():
+            return (torch.from_numpy(wl["points"]).pin_memory(),
+                    torch.from_numpy(np.ascontiguousarray(wl["weights"])).pin_memory())
+        e2e = host_timed(pinned, "e2e")
+        e2e.update({"h2d_bytes_per_step": int(n * 3 * 8 + n * m * 8),
+                    "d2h_bytes_per_step": int(n * m * 8),
+                    "inputs": "pinned host torch tensors (points, weights) -> phi in "
+                              "pinned host memory"})
+        e2e_np = host_timed(lambda: (wl["points"], wl["weights"]), "e2e_numpy")
+        e2e_np.update({"h2d_bytes_per_step": int(n * 3 * 8 + n * m * 8),
+                       "d2h_bytes_per_step": int(n * m * 8),
+                       "inputs": "NumPy arrays (pageable), as the reference's callers pass "
+                                 "them; phi returned as a NumPy array"})
+
+    # ---- device-resident timed loop ----
+    for _ in range(warmup):
+        runner.evaluate(X, weights=Wt)
+    barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
+    barrier()
     launches0 = lib.bfmm_launch_count() + ev.graph_launches
-    spans, kms, stage_sum = [], [], {}
-    for _ in range(args.steps):
+    spans, stage_sum = [], {}
+    for _ in range(steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        step(X, W)
+        runner.evaluate(X, weights=Wt)
         e1.record()
         e1.synchronize()
         spans.append(e0.elapsed_time(e1))
         for k, v in ev.timings.items():
             if isinstance(v, float):
                 stage_sum[k] = stage_sum.get(k, 0.0) + v
-    torch.cuda.synchronize()
+    barrier()
     launches = lib.bfmm_launch_count() + ev.graph_launches - launches0
-    if dist is not None:
-        dist.barrier()
     clk = clocks.stop()
-    total_ms = float(sum(spans))
-    # per-kernel times for the roofline: a separate pass with CUDA events
-    # around each launch on its own stream, near field NOT overlapped (the
-    # timed steps above overlap it with the far field, which would charge
-    # the SM sharing to both kernels)
-    ov = ev.overlap_near
-    ev.overlap_near, ev.profile_kernels = False, True
-    for _ in range(args.steps):
+    total_ms = _max_over_ranks(dist, float(sum(spans)))
+    value = n * steps / (total_ms * 1e-3)
+
+    # ---- per-kernel pass: CUDA events around every launch on its own
+    # stream, far-field levels and near field serialised on one stream ----
+    saved = (ev.overlap_near, ev.stream_levels, ev.profile_kernels)
+    ev.overlap_near, ev.stream_levels, ev.profile_kernels = False, False, True
+    kms = []
+    for _ in range(max(2, min(steps, 5))):
         flush.zero_()
-        step(X, W)
+        runner.evaluate(X, weights=Wt)
         torch.cuda.synchronize()
         kms.append(dict(ev.kernel_ms))
-    ev.overlap_near, ev.profile_kernels = ov, False
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = n * args.steps / (total_ms * 1e-3)
-
-
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline of the dominant kernel ----
-    dfma_tf, dmma_tf = fp64_peaks(lib, stream)
+        stages_serial = dict(ev.timings)
+    ev.overlap_near, ev.stream_levels, ev.profile_kernels = saved
     avg = {}
     for d in kms:
         for k, v in d.items():
             avg[k] = avg.get(k, 0.0) + v / len(kms)
-    dom = max(avg, key=avg.get) if avg else None
-    roof = None
-    if dom is not None:
-        ms = avg[dom]
-        if dom == "p2p":
-            fpp = P2P_FLOPS_PER_PAIR.get(wl["kernel"])
-            pairs = ev.timings["near_pairs"] * m
-            flops = pairs * fpp
-            peak = dfma_tf
-            roof = {"kernel": "p2p (near field, FP64 pipe)", "bound": "fp64",
-                    "flops_per_pair": fpp, "pair_interactions": pairs,
-                    "pairs_per_s": pairs / (ms * 1e-3),
-                    "flops_note": "frozen algorithmic figure (profiles/r01_p2p_flops.txt); "
-                                  "the current kernel executes ~32 FP64 flops per pair"}
-        else:
-            lev = int(dom.split("_l")[1])
-            flops = m2l_flops(ev, wl)[lev]
-            peak = dmma_tf
-            roof = {"kernel": f"m2l level {lev} ({ev.m2l_mode} implicit GEMM)",
-                    "bound": "fp64-tensor"}
-        achieved = flops / (ms * 1e-3) / 1e12
-        roof.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": committed_traffic(args.config, dom),
-                     "peak_source": "measured live: DFMA / DMMA microbenchmarks (libbfmm.so); "
-                                    "MEASURED_PEAKS.json has no FP64 entry",
-                     "kernel_ms": ms, "share_of_step": ms / (total_ms / args.steps)})
-    m2l = m2l_flops(ev, wl)
-    kernels = {k: round(v, 4) for k, v in sorted(avg.items())}
-    m2l_frac = {k: (m2l[int(k.split("_l")[1])] / (v * 1e-3) / 1e12) / dmma_tf
-                for k, v in avg.items() if k.startswith("m2l_l")}
-    # the int8 tensor-core M2L against its own roofline: executed int8 ops
-    # per launch / launch time vs the measured tcgen05 kind::i8 peak
-    m2l_roof = None
-    if ev.m2l_mode == "i8" and wl["scheme"] == "chebyshev":
-        i8_peak = C.c_double(0)
-        lib.bfmm_device_i8_probe(C.byref(i8_peak), stream)
+    step_ms = total_ms / steps
+    near_pairs = int(ev.timings.get("near_pairs", 0))
+
+    out = {"wl": wl, "ev": ev, "value": value, "total_ms": total_ms, "step_ms": step_ms,
+           "launches": launches, "clocks": clk, "e2e": e2e, "e2e_numpy": e2e_np,
+           "stages_ms": {k: round(1e3 * v / steps, 4) for k, v in stage_sum.items()},
+           "stages_serial_ms": {k: (round(1e3 * v, 4) if isinstance(v, float) else v)
+                                for k, v in stages_serial.items()},
+           "kernels_ms": {k: round(v, 4) for k, v in sorted(avg.items())}}
+    if rank == 0:
+        out["roofline"], out["m2l"] = rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms)
+    return out
+
+
+def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
+    """roofline of the dominant kernel + per-level M2L figures."""
+    m = wl["ncols"]
+    levels = {}
+    if wl["scheme"] == "chebyshev":
+        flops = m2l_flops(ev, wl)
         S = int(ev.i8_slices)
-        m2l_roof = {"engine": f"int8 tcgen05, {S} digits per operand",
-                    "peak_int8_tops": i8_peak.value,
-                    "peak_source": "measured live: bfmm_device_i8_probe (128x256x32 MMAs "
-                                   "back to back)", "levels": {}}
         for k, v in avg.items():
             if not k.startswith("m2l_l"):
                 continue
             lev = int(k.split("_l")[1])
-            rp = ev._dev_block(lev)["rp"]
-            ops = m2l_i8_ops(lev, rp, m, S)
-            fp64 = m2l[lev] / (v * 1e-3) / 1e12
-            m2l_roof["levels"][k] = {
-                "ms": round(v, 4), "kernel": "plane" if lev >= 4 else "gather",
-                "int8_tops": ops / (v * 1e-3) / 1e12,
-                "frac_int8_peak": ops / (v * 1e-3) / 1e12 / i8_peak.value,
-                "fp64_equiv_tflops": fp64, "frac_of_dmma_peak": fp64 / dmma_tf,
-                "traffic": committed_traffic(args.config, k)}
+            blk = ev._dev_block(lev)
+            r, rp = ev.table.block_for_level(lev).rank, blk["rp"]
+            fp64 = flops[lev] / (v * 1e-3) / 1e12
+            rec = {"ms": round(v, 4), "engine": ev._level_engine(lev, m, rp),
+                   "rank": r, "fp64_equiv_tflops": fp64,
+                   "frac_of_dmma_peak": fp64 / peaks["dmma_tflops"],
+                   "traffic": committed_traffic(cfg, k)}
+            if rec["engine"] == "i8":
+                useful = flops[lev] * S * (S + 1) / 2  # digit products of the unpadded rank
+                executed = m2l_i8_ops(lev, rp, m, S)
+                rec.update({"kernel": "plane" if lev >= 4 else "gather",
+                            "useful_int8_tops": useful / (v * 1e-3) / 1e12,
+                            "executed_int8_tops": executed / (v * 1e-3) / 1e12,
+                            "frac_useful": useful / (v * 1e-3) / 1e12 / peaks["i8_tops"],
+                            "frac_executed": executed / (v * 1e-3) / 1e12 / peaks["i8_tops"]})
+            levels[k] = rec
+    else:
+        flops = fft_flops(wl)
+        for k, v in avg.items():
+            if not k.startswith("m2lfft_l"):
+                continue
+            lev = int(k.split("_l")[1])
+            tf = flops[lev] / (v * 1e-3) / 1e12
+            levels[k] = {"ms": round(v, 4), "hadamard_tflops": tf,
+                         "frac_dfma_peak": tf / peaks["dfma_tflops"],
+                         "traffic": committed_traffic(cfg, k)}
+    dom = max(avg, key=avg.get) if avg else None
+    if dom is None:
+        return None, levels
+    ms = avg[dom]
+    share = ms / step_ms
+    if dom == "p2p":
+        fpp = P2P_FLOPS_PER_PAIR.get(wl["kernel"])
+        pairs = near_pairs * m
+        roof = {"kernel": "p2p_kernel (near field, FP64 pipe)", "bound": "fp64",
+                "pair_interactions": pairs, "pairs_per_s": pairs / (ms * 1e-3),
+                "flops_per_pair": fpp}
+        if fpp is not None:
+            ach = pairs * fpp / (ms * 1e-3) / 1e12
+            roof.update({"achieved": ach, "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
+                         "frac": ach / peaks["dfma_tflops"],
+                         "frac_of_nominal_37.2": ach / NOMINAL_FP64_TF,
+                         "peak_source": "measured live: DFMA microbenchmark "
+                                        "(bfmm_device_fp64_probe); MEASURED_PEAKS.json has no "
+                                        "FP64 entry"})
+    elif dom.startswith("m2lfft_l"):
+        rec = levels[dom]
+        roof = {"kernel": f"uniform FFT M2L level {dom.split('_l')[1]} (fft_fwd + stencil + "
+                          "fft_inv)", "bound": "fp64", "achieved": rec["hadamard_tflops"],
+                "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
+                "frac": rec["hadamard_tflops"] / peaks["dfma_tflops"],
+                "frac_of_nominal_37.2": rec["hadamard_tflops"] / NOMINAL_FP64_TF,
+                "algorithmic": "Hadamard flops P_l * q^2(q/2+1) * m * 8",
+                "peak_source": "measured live: DFMA microbenchmark"}
+    else:
+        rec = levels[dom]
+        lev = dom.split("_l")[1]
+        if rec["engine"] == "i8":
+            roof = {"kernel": f"m2l_i8{'p' if rec['kernel'] == 'plane' else ''}_kernel "
+                              f"(M2L level {lev}, int8 tcgen05, {ev.i8_slices} digits/operand)",
+                    "bound": "tensor", "achieved": rec["useful_int8_tops"],
+                    "peak": peaks["i8_tops"], "unit": "TFLOP/s",
+                    "op_kind": "int8 tensor-core ops (1 MAC = 2), tcgen05 kind::i8",
+                    "frac": rec["frac_useful"],
+                    "algorithmic": "useful = P_l * 2 r^2 * m * S(S+1)/2 digit products of the "
+                                   "unpadded rank",
+                    "executed_int8_tops": rec["executed_int8_tops"],
+                    "frac_executed": rec["frac_executed"],
+                    "fp64_equiv_tflops": rec["fp64_equiv_tflops"],
+                    "fp64_equiv_frac_of_dmma_peak": rec["frac_of_dmma_peak"],
+                    "peak_source": "measured live: bfmm_device_i8_probe (128x256x32 kind::i8 "
+                                   "MMAs back to back); MEASURED_PEAKS.json has no int8 entry"}
+        else:
+            roof = {"kernel": f"m2l_ws_kernel (M2L level {lev}, FP64 DMMA)", "bound": "tensor",
+                    "achieved": rec["fp64_equiv_tflops"], "peak": peaks["dmma_tflops"],
+                    "unit": "TFLOP/s", "frac": rec["frac_of_dmma_peak"],
+                    "peak_source": "measured live: DMMA microbenchmark"}
+    roof.update({"kernel_key": dom, "kernel_ms": ms, "share_of_step": share,
+                 "traffic": committed_traffic(cfg, dom)})
+    return roof, levels
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+    import torch
+
+    from paper_1903_02153_b200 import _native
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        assert dist.get_world_size() == world == args.gpus, (dist.get_world_size(), args.gpus)
+    lib = _native.load()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    peaks = device_peaks(lib, stream) if rank == 0 else None
+    res = measure(args.config, args, rank, world, local_rank, dist, lib, peaks,
+                  args.steps, args.warmup, with_e2e=not args.no_e2e)
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    wl = res["wl"]
+    res.pop("ev")  # free the primary config's device memory before the secondary
+    torch.cuda.empty_cache()
+
+    secondary = None
+    if world == 1 and args.secondary and args.secondary.lower() != "none" \
+            and args.secondary != args.config:
+        s = measure(args.secondary, args, 0, 1, local_rank, None, lib, peaks,
+                    min(args.steps, 10), args.warmup, with_e2e=False)
+        secondary = {"config": config_dict(s["wl"]), "value": s["value"], "unit": "points/s",
+                     "ms_per_step": s["step_ms"], "steps": min(args.steps, 10),
+                     "roofline": s["roofline"], "kernels_ms": s["kernels_ms"],
+                     "m2l_levels": s["m2l"], "clocks": s["clocks"],
+                     "gpu_launches": s["launches"]}
+        s.pop("ev")
+        del s
+        torch.cuda.empty_cache()
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        threads = cpu_threads()
-        secs = oracle_step(wl, threads)
-        cpu = {"value": n / secs, "unit": "points/s", "cores": threads, "kind": "port",
-               "sample": f"one full {args.config} matvec (oracle/fmm_oracle.py, {secs:.1f} s)"}
+        scale = REF_SCALE.get(args.config, 0) if args.ref_scale is None else args.ref_scale
+        try:
+            ref = ReferenceSample(args.config, scale, cpu_threads())
+            ref.step()  # warm: tables and first-touch
+            secs = [ref.step() for _ in range(2)]
+            cpu = {"value": ref.n * len(secs) / sum(secs), "unit": "points/s",
+                   "cores": ref.threads, "kind": "reference",
+                   "sample": ref.desc + f"; {len(secs)} timed evaluates, "
+                                        f"{sum(secs):.1f} s"}
+        except RuntimeError as e:
+            cpu = {"value": None, "unit": "points/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
 
-    h2d = int(Xh.numel() * 8 + Wh.numel() * 8)
-    d2h = int(n * m * 8)
+    ev_m2l = res["m2l"]
     line = {
-        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "metric": METRIC, "value": res["value"], "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["step_ms"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SURVEY.md §8(d) recipe)",
         "config": config_dict(wl),
-        "engine": {"m2l": (f"int8 tcgen05, {ev.i8_slices} digits" if ev.m2l_mode == "i8"
-                           else "fp64 dmma"),
-                   "near_field": ("own stream, overlaps kernel tails" if ev.overlap_near
-                                  else "serial"),
-                   "cuda_graph": bool(ev.use_graph)},
-        "roofline": roof, "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,
-                "step_ms": [round(x, 3) for x in e2e_ms]},
-        "gpu_launches": int(launches), "clocks": clk,
-        "stages_ms": {k: round(1e3 * v / args.steps, 4) for k, v in stage_sum.items()},
-        "kernels_ms": kernels,
-        "m2l_frac_of_dmma_peak": {k: round(v, 3) for k, v in m2l_frac.items()},
-        "m2l_roofline": m2l_roof,
-        "fp64_peaks_tflops": {"dfma": dfma_tf, "dmma": dmma_tf},
+        "engine": {"m2l": "int8 tcgen05 (error-free digit splitting) where rank <= 256, "
+                          "else FP64 DMMA" if wl["scheme"] == "chebyshev" else "FFT Hadamard",
+                   "near_field": "own stream, overlaps kernel tails",
+                   "parallelism": f"dp{world}: Morton-range target shards" if world > 1
+                   else "single GPU"},
+        "roofline": res["roofline"], "cpu_baseline": cpu,
+        "e2e": res["e2e"], "e2e_numpy": res["e2e_numpy"],
+        "gpu_launches": int(res["launches"]), "clocks": res["clocks"],
+        "stages_ms": res["stages_ms"], "stages_serial_ms": res["stages_serial_ms"],
+        "kernels_ms": res["kernels_ms"], "m2l_levels": ev_m2l,
+        "peaks": dict(peaks, source="measured live in this process (libbfmm.so probes)"),
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.barrier()
         dist.destroy_process_group()
+
+
+def spawn(args):
+    """--gpus N without a torchrun environment: launch N ranks ourselves."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:
+        if world != args.gpus:
+            raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
         run_ours(args, rank, world, local_rank)
 
 

@@ -60,10 +60,12 @@ int bfmm_tree_build(const double *points, int64_t n, const double *geom,
                     int32_t *domain_flag, bfmm_stream_t stream);
 
 /* w (N, m) original order -> wsorted (N, m) and pts4[:, 3] = w[perm, 0]
- * (the weights[part.perm] of engine.py:168,528). */
+ * (the weights[part.perm] of engine.py:168,528).  A non-finite weight sets
+ * *weights_flag |= 1 (device; may be NULL) -- the reference's
+ * ConfigurationError("weights contain non-finite values", engine.py:496-497). */
 int bfmm_gather_weights(const double *w, int64_t n, int m,
                         const int64_t *perm, double *wsorted, double *pts4,
-                        bfmm_stream_t stream);
+                        int32_t *weights_flag, bfmm_stream_t stream);
 
 /* Active cells for sparse clouds: the sorted distinct ancestors
  * leaves[i] >> shift (shift = 3 * (levels - level)) of the n_leaves

@@ -580,6 +580,7 @@ class OracleFMM:
                 locs = {lev: self.m2l(lev, M[lev]) for lev in range(2, self.L + 1)}
                 self.stage["m2l"] = {k: v.copy() for k, v in locs.items()}
                 self.l2p(tgt, self.l2l(locs), phi)
+                self.stage["locals"] = locs  # after L2L (eng:296-311)
             near, npairs = self.p2p(tgt, src, w[src.perm])
             phi[tgt.perm] += near
             self.stage["near_pairs"] = npairs

@@ -28,7 +28,7 @@ SIGNATURES = {
     "bfmm_version": (_I, []),
     "bfmm_tree_scratch_bytes": (_SZ, [_I64, _I]),
     "bfmm_tree_build": (_I, [_P, _I64, _DP, _I, _P, _SZ, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "bfmm_gather_weights": (_I, [_P, _I64, _I, _P, _P, _P, _P]),
+    "bfmm_gather_weights": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P]),
     "bfmm_p2m": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_p2m_sparse": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_m2m": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),

@@ -32,6 +32,16 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int kNumSMs = 148;  // B200
 
+// Per-device one-time setup (function attributes, __constant__ tables live
+// in each device's context): true the first time it is called for the
+// current device with this mask word.
+inline bool first_on_device(unsigned long long *mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  return (__atomic_fetch_or(mask, bit, __ATOMIC_ACQ_REL) & bit) == 0;
+}
+
 // 21-bit Morton spread: bit b of v moves to bit 3b (octree.py:75-83 layout).
 __host__ __device__ inline uint64_t spread3(uint64_t v) {
   v &= 0x1FFFFFull;

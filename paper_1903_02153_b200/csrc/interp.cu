@@ -5,6 +5,8 @@
 //   L2L  descend          (engine.py:296-311)
 // Coefficient layout per cell is (m, p^3) with the node index
 // a = (i*p + j)*p + k, z fastest (interpolation.py:93-102).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bfmm {
@@ -75,7 +77,7 @@ constexpr int kLeafThreads = 128;
 
 __global__ void __launch_bounds__(kLeafThreads)
 p2m_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
-           int m, const int64_t *__restrict__ leaves,
+           int m, int ncmax, const int64_t *__restrict__ leaves,
            const int64_t *__restrict__ starts,
            const int64_t *__restrict__ counts,
            const int64_t *__restrict__ n_leaves, int levels, Interp ip,
@@ -85,7 +87,7 @@ p2m_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
   double *wx = sm;                          // [kLeafThreads][p]
   double *wy = wx + kLeafThreads * p;
   double *wz = wy + kLeafThreads * p;
-  double *wv = wz + kLeafThreads * p;       // [kLeafThreads][m]
+  double *wv = wz + kLeafThreads * p;       // [kLeafThreads][ncmax]: the pass's columns
   const int64_t nl = *n_leaves;
   for (int64_t leaf = blockIdx.x; leaf < nl; leaf += gridDim.x) {
     const int64_t cell = leaves[leaf];
@@ -94,42 +96,47 @@ p2m_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
     const int nout = m * p3;
-    // up to ceil(nout / threads) accumulators per thread
-    double acc[27];
-    const int per = (nout + kLeafThreads - 1) / kLeafThreads;
-    for (int u = 0; u < per && u < 27; ++u) acc[u] = 0.0;
-    for (int64_t c0 = 0; c0 < cnt; c0 += kLeafThreads) {
-      const int nb = (int)(cnt - c0 < kLeafThreads ? cnt - c0 : kLeafThreads);
-      __syncthreads();
-      if (threadIdx.x < nb) {
-        const int64_t i = s0 + c0 + threadIdx.x;
-        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
-        double w1[kMaxP];
-        weights_1d(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), w1);
-        for (int j = 0; j < p; ++j) wx[threadIdx.x * p + j] = w1[j];
-        weights_1d(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), w1);
-        for (int j = 0; j < p; ++j) wy[threadIdx.x * p + j] = w1[j];
-        weights_1d(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), w1);
-        for (int j = 0; j < p; ++j) wz[threadIdx.x * p + j] = w1[j];
-        for (int c = 0; c < m; ++c) wv[threadIdx.x * m + c] = ws[i * m + c];
+    // outputs in passes of up to 27 accumulators per thread (any m * p^3;
+    // the leaf's points are re-staged for every pass)
+    for (int o0 = 0; o0 < nout; o0 += 27 * kLeafThreads) {
+      const int nrem = nout - o0 < 27 * kLeafThreads ? nout - o0 : 27 * kLeafThreads;
+      double acc[27];
+      const int per = (nrem + kLeafThreads - 1) / kLeafThreads;
+      const int cl = o0 / p3, nc = (o0 + nrem - 1) / p3 - cl + 1;  // columns of this pass
+      for (int u = 0; u < per; ++u) acc[u] = 0.0;
+      for (int64_t c0 = 0; c0 < cnt; c0 += kLeafThreads) {
+        const int nb = (int)(cnt - c0 < kLeafThreads ? cnt - c0 : kLeafThreads);
+        __syncthreads();
+        if (threadIdx.x < nb) {
+          const int64_t i = s0 + c0 + threadIdx.x;
+          const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+          double w1[kMaxP];
+          weights_1d(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), w1);
+          for (int j = 0; j < p; ++j) wx[threadIdx.x * p + j] = w1[j];
+          weights_1d(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), w1);
+          for (int j = 0; j < p; ++j) wy[threadIdx.x * p + j] = w1[j];
+          weights_1d(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), w1);
+          for (int j = 0; j < p; ++j) wz[threadIdx.x * p + j] = w1[j];
+          for (int c = 0; c < nc; ++c) wv[threadIdx.x * ncmax + c] = ws[i * m + cl + c];
+        }
+        __syncthreads();
+        for (int u = 0; u < per; ++u) {
+          const int o = o0 + threadIdx.x + u * kLeafThreads;
+          if (o >= nout) break;
+          const int c = o / p3, a = o - c * p3;
+          const int i = a / (p * p), j = (a / p) % p, k = a % p;
+          double s = acc[u];
+          for (int t = 0; t < nb; ++t)
+            s += ((wx[t * p + i] * wy[t * p + j]) * wz[t * p + k]) * wv[t * ncmax + c - cl];
+          acc[u] = s;
+        }
       }
-      __syncthreads();
+      double *dst = moments + cell * (int64_t)nout;
       for (int u = 0; u < per; ++u) {
-        const int o = threadIdx.x + u * kLeafThreads;
+        const int o = o0 + threadIdx.x + u * kLeafThreads;
         if (o >= nout) break;
-        const int c = o / p3, a = o - c * p3;
-        const int i = a / (p * p), j = (a / p) % p, k = a % p;
-        double s = acc[u];
-        for (int t = 0; t < nb; ++t)
-          s += ((wx[t * p + i] * wy[t * p + j]) * wz[t * p + k]) * wv[t * m + c];
-        acc[u] = s;
+        dst[o] = acc[u];
       }
-    }
-    double *dst = moments + cell * (int64_t)nout;
-    for (int u = 0; u < per; ++u) {
-      const int o = threadIdx.x + u * kLeafThreads;
-      if (o >= nout) break;
-      dst[o] = acc[u];
     }
   }
 }
@@ -138,13 +145,14 @@ p2m_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
 // L2P: one CTA per nonempty leaf, leaf locals in shared memory, one thread
 // per target point.
 __global__ void __launch_bounds__(kLeafThreads)
-l2p_kernel(const double *__restrict__ pts4, int m,
+l2p_kernel(const double *__restrict__ pts4, int m, int mc,
            const int64_t *__restrict__ leaves,
            const int64_t *__restrict__ starts,
            const int64_t *__restrict__ counts,
            const int64_t *__restrict__ n_leaves, Interp ip, LeafGeom g,
            const double *__restrict__ locals, double *__restrict__ phi,
            int32_t *flag) {
+  // mc columns of the leaf's locals staged per pass (any m * p^3)
   extern __shared__ double sm[];
   const int p = ip.p, p3 = p * p * p;
   const int nout = m * p3;
@@ -155,27 +163,30 @@ l2p_kernel(const double *__restrict__ pts4, int m,
     const int64_t s0 = starts[leaf], cnt = counts[leaf];
     int cx, cy, cz;
     unmorton3((uint64_t)cell, cx, cy, cz);
-    __syncthreads();
-    for (int o = threadIdx.x; o < nout; o += kLeafThreads)
-      sm[o] = locals[cell * (int64_t)nout + o];
-    __syncthreads();
-    for (int64_t t = threadIdx.x; t < cnt; t += kLeafThreads) {
-      const int64_t i = s0 + t;
-      const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
-      double wx[kMaxP], wy[kMaxP], wz[kMaxP];
-      weights_1d(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), wx);
-      weights_1d(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), wy);
-      weights_1d(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), wz);
-      for (int c = 0; c < m; ++c) {
-        const double *L = sm + c * p3;
-        double s = 0.0;
-        int a = 0;
-        for (int ii = 0; ii < p; ++ii)
-          for (int jj = 0; jj < p; ++jj) {
-            const double wxy = wx[ii] * wy[jj];
-            for (int kk = 0; kk < p; ++kk, ++a) s = fma(wxy * wz[kk], L[a], s);
-          }
-        phi[i * m + c] = s;
+    for (int c0 = 0; c0 < m; c0 += mc) {
+      const int nc = m - c0 < mc ? m - c0 : mc;
+      __syncthreads();
+      for (int o = threadIdx.x; o < nc * p3; o += kLeafThreads)
+        sm[o] = locals[cell * (int64_t)nout + (int64_t)c0 * p3 + o];
+      __syncthreads();
+      for (int64_t t = threadIdx.x; t < cnt; t += kLeafThreads) {
+        const int64_t i = s0 + t;
+        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+        double wx[kMaxP], wy[kMaxP], wz[kMaxP];
+        weights_1d(ip, ref_coord(q.x, g.lo[0], g.h, g.hw, cx, flag), wx);
+        weights_1d(ip, ref_coord(q.y, g.lo[1], g.h, g.hw, cy, flag), wy);
+        weights_1d(ip, ref_coord(q.z, g.lo[2], g.h, g.hw, cz, flag), wz);
+        for (int c = 0; c < nc; ++c) {
+          const double *L = sm + c * p3;
+          double s = 0.0;
+          int a = 0;
+          for (int ii = 0; ii < p; ++ii)
+            for (int jj = 0; jj < p; ++jj) {
+              const double wxy = wx[ii] * wy[jj];
+              for (int kk = 0; kk < p; ++kk, ++a) s = fma(wxy * wz[kk], L[a], s);
+            }
+          phi[i * m + c0 + c] = s;
+        }
       }
     }
   }
@@ -320,16 +331,14 @@ static int p2m_impl(const double *pts4, const double *wsorted, int m,
                nullptr, moments, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, true, a);
   }
-  if (m * p * p * p > 27 * kLeafThreads) {
-    set_error("bfmm_p2m: unsupported p=%d m=%d", p, m);
-    return 2;
-  }
-  size_t smem = sizeof(double) * kLeafThreads * (3 * p + m);
+  const int p3 = p * p * p;
+  const int ncmax = std::min(m, 27 * kLeafThreads / p3 + 2);  // columns one output pass spans
+  size_t smem = sizeof(double) * kLeafThreads * (3 * p + ncmax);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   p2m_kernel<<<grid_cap(max_leaves, 16), kLeafThreads, smem,
-               as_stream(stream)>>>(pts4, wsorted, m, leaves, starts, counts,
+               as_stream(stream)>>>(pts4, wsorted, m, ncmax, leaves, starts, counts,
                                     n_leaves, levels, ip, g, moments, ref_flag);
   return check_launch("p2m_kernel");
 }
@@ -353,16 +362,14 @@ static int l2p_impl(const double *pts4, int m, const int64_t *leaves,
                per_point, ip, g, locals, phi_sorted, ref_flag, as_stream(stream)};
     return dispatch_leaf(p, false, a);
   }
-  size_t smem = sizeof(double) * m * p * p * p;
-  if (smem > 200 * 1024) {
-    set_error("bfmm_l2p: m*p^3 too large for one leaf tile");
-    return 2;
-  }
+  const int p3 = p * p * p;
+  const int mc = std::min(m, (int)((200 * 1024) / (sizeof(double) * p3)));
+  size_t smem = sizeof(double) * mc * p3;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(l2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   l2p_kernel<<<grid_cap(max_leaves, 16), kLeafThreads, smem,
-               as_stream(stream)>>>(pts4, m, leaves, starts, counts, n_leaves,
+               as_stream(stream)>>>(pts4, m, mc, leaves, starts, counts, n_leaves,
                                     ip, g, locals, phi_sorted, ref_flag);
   return check_launch("l2p_kernel");
 }

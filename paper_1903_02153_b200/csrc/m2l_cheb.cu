@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "tcgen05.cuh"
 
@@ -64,10 +66,15 @@ __constant__ uint32_t c_dil[316][3];
 // c_grp[o][c_grp_off[o][g] .. c_grp_off[o][g + 1]) (m2l_i8p_kernel)
 __constant__ short c_grp[8][189];
 __constant__ unsigned char c_grp_off[8][29];
-bool g_offsets_ready = false;
+std::mutex g_offsets_mu;
+unsigned long long g_offsets_ready = 0;  // one bit per device (its own __constant__ bank)
 
 void ensure_offsets() {
-  if (g_offsets_ready) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lock(g_offsets_mu);
+  if (g_offsets_ready & bit) return;
   signed char h[316][3];
   short v[8][189];
   int n = 0;
@@ -119,7 +126,7 @@ void ensure_offsets() {
   }
   cudaMemcpyToSymbol(c_grp, gr, sizeof(gr));
   cudaMemcpyToSymbol(c_grp_off, go, sizeof(go));
-  g_offsets_ready = true;
+  g_offsets_ready |= bit;
 }
 
 // ---- DMMA helpers -------------------------------------------------------------
@@ -396,13 +403,12 @@ static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int 
   // leaves most SMs idle (small levels): then 64-column tiles, twice the CTAs
   const int wn = (N > 64 && ceil_div(rows, kPjTM) >= kNumSMs) ? 2 : 1;
   dim3 grid((unsigned)ceil_div(rows, kPjTM), (unsigned)ceil_div(N, 64 * wn));
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) {
     cudaFuncSetAttribute(proj_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)pj_smem<1>());
     cudaFuncSetAttribute(proj_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)pj_smem<2>());
-    attr = true;
   }
   if (wn == 2)
     proj_gemm_kernel<2><<<grid, 256, pj_smem<2>(), st>>>(A, rows, lda, K, B, N, C, alpha,

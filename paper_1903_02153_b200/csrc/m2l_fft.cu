@@ -19,6 +19,8 @@
 // twiddles: zero padding makes them cheaper than a generic FFT.
 #include <algorithm>
 
+#include <mutex>
+
 #include "common.cuh"
 
 
@@ -358,7 +360,13 @@ FftGeom make_geom(int p) {
 // 7^3 table: offset (a, b, c) -> index among the 316 far offsets
 // (lexicographic, octree.py:110-119), -1 for the 27 near offsets.
 short *tap_table() {
-  static short *dev = nullptr;
+  // one copy per device (the table is read by that device's kernels)
+  static std::mutex mu;
+  static short *per_dev[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  std::lock_guard<std::mutex> lock(mu);
+  short *&dev = per_dev[d & 63];
   if (dev) return dev;
   short h[343];
   int t = 0;
@@ -413,11 +421,10 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const int n = 1 << level;
   const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
   const size_t smem_s = sizeof(double2) * (kHX * kHYP * kHZP + 343);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) {
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_s);
-    attr = true;
   }
   int rc = 0;
   switch (p) {

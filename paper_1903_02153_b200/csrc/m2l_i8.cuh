@@ -715,11 +715,10 @@ inline bool i8_mixed_ok(const I8Call &a) {
 template <int S>
 int launch_i8(const I8Call &a) {
   using Sh = I8Shape<S>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(&attr_set)) {
     cudaFuncSetAttribute(m2l_i8_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
-    attr_set = true;
   }
   const int mixed = i8_mixed_ok(a) ? 1 : 0;
   int64_t rows = mixed ? 8 * a.nq * a.m : a.nq * a.m;
@@ -738,11 +737,10 @@ int launch_i8(const I8Call &a) {
 template <int S, int XT>
 int launch_i8p(const I8Call &a) {
   using Sh = I8PShape<S, XT>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(&attr_set)) {
     cudaFuncSetAttribute(m2l_i8p_kernel<S, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
-    attr_set = true;
   }
   const int h = 1 << (a.level - 1);
   dim3 grid((unsigned)((h / XT) * (h / Sh::YT) * (h / 8)), (unsigned)(a.ntn * a.m),

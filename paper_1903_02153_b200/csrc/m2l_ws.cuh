@@ -221,11 +221,10 @@ struct M2LCall {
 template <int NT8, int MW>
 int launch_ws(const M2LCall &a) {
   using S = WsShape<NT8, MW>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(&attr_set)) {
     cudaFuncSetAttribute(m2l_ws_kernel<NT8, MW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
-    attr_set = true;
   }
   int64_t rows = a.nq * a.m;
   if (a.act.cells) {  // the longest octant list sizes the grid

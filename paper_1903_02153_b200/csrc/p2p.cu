@@ -150,7 +150,10 @@ std::string functor_source(int kind, const char *expr) {
 
 int jit_compile(int kind, const char *expr, int *handle) {
   std::lock_guard<std::mutex> lock(g_jit_mu);
-  std::string key = std::to_string(kind) + ":" + expr;
+  // modules are loaded into the current device's context: one per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::string key = std::to_string(dev) + ":" + std::to_string(kind) + ":" + expr;
   auto it = g_jit_cache.find(key);
   if (it != g_jit_cache.end()) {
     *handle = it->second;

@@ -123,13 +123,12 @@ template <int P>
 int launch_xfer(bool up, const double *src, double *dst, int64_t n_parent, int m,
                 const Halves &hv, cudaStream_t st) {
   constexpr size_t smem = xfer_smem<P>();
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) {
     cudaFuncSetAttribute(m2m_stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaFuncSetAttribute(l2l_stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    attr = true;
   }
   const unsigned grid = (unsigned)std::min<int64_t>(n_parent * m, (int64_t)kNumSMs * 16);
   if (up) {

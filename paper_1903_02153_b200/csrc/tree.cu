@@ -103,16 +103,23 @@ __global__ void gather_points_kernel(const double *__restrict__ pts,
 __global__ void gather_weights_kernel(const double *__restrict__ w, int64_t n,
                                       int m, const int64_t *__restrict__ perm,
                                       double *__restrict__ ws,
-                                      double *__restrict__ pts4) {
+                                      double *__restrict__ pts4,
+                                      int32_t *__restrict__ weights_flag) {
   const int64_t total = n * m;
+  bool bad = false;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     int64_t i = e / m;
     int c = (int)(e - i * m);
     double v = w[perm[i] * m + c];
+    bad |= !isfinite(v);
     ws[e] = v;
     if (c == 0) pts4[4 * i + 3] = v;
   }
+  // "weights contain non-finite values" (engine.py:496-497), checked on the
+  // device in the same pass instead of an O(N) host scan
+  if (weights_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(weights_flag, 1);
 }
 
 inline int grid_for(int64_t n, int threads) {
@@ -303,10 +310,11 @@ extern "C" int bfmm_tree_build(const double *points, int64_t n,
 
 extern "C" int bfmm_gather_weights(const double *w, int64_t n, int m,
                                    const int64_t *perm, double *wsorted,
-                                   double *pts4, bfmm_stream_t stream) {
+                                   double *pts4, int32_t *weights_flag,
+                                   bfmm_stream_t stream) {
   if (n == 0) return 0;
   gather_weights_kernel<<<grid_for(n * m, 256), 256, 0, as_stream(stream)>>>(
-      w, n, m, perm, wsorted, pts4);
+      w, n, m, perm, wsorted, pts4, weights_flag);
   return check_launch("gather_weights_kernel");
 }
 

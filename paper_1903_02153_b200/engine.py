@@ -123,11 +123,21 @@ class FmmEvaluator:
         if not torch.cuda.is_available():
             raise NativeLibraryError("no CUDA device is visible; the FMM matvec runs on the GPU only")
         self.lib = _native.load()
-        _warm_pinned_dma(torch.device(device if device is not None else "cuda"))
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.type != "cuda":
+            raise ConfigurationError(f"device must be a CUDA device, got {dev}")
+        # an explicit index: every launch, stream and module load of this
+        # evaluator happens with it current (evaluate() enters it too)
+        self.device = dev if dev.index is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        with torch.cuda.device(self.device):
+            self._init_on_device(kernel, plan, cache_dir, threads, table, use_cache)
+
+    def _init_on_device(self, kernel, plan, cache_dir, threads, table, use_cache):
+        _warm_pinned_dma(self.device)
         self.kernel = kernel
         self.plan = plan
         self.threads = max(1, int(threads))
-        self.device = torch.device(device if device is not None else "cuda")
         t0 = time.perf_counter()
         p, sch = plan.order, plan.scheme
         self._H = np.ascontiguousarray(half_interval_matrices(p, sch))
@@ -144,6 +154,7 @@ class FmmEvaluator:
         self.table_seconds = time.perf_counter() - t0
         self.precompute_seconds = self.tree_seconds + self.table_seconds
         self._handle = self._kernel_handle()
+        self._check_device_kernel()
         self.timings = {}
         self._disable_far_field = False
         self.keep_stages = False
@@ -200,6 +211,40 @@ class FmmEvaluator:
                       f"NVRTC compile of kernel {k.name!r}")
         return int(h.value)
 
+    def _check_device_kernel(self):
+        """The device functor must be the kernel the tables were built from.
+        A custom kernel is given twice -- the NumPy hook (operator tables,
+        reference ops:244-341) and cuda_expr (near field) -- so the two are
+        compared on fixed sample pairs in the domain (no r = 0 pair) before
+        the evaluator is usable; a mismatch would silently give a wrong phi."""
+        if self.kernel.builtin_id:
+            return
+        torch = _torch()
+        d = self.plan.domain
+        g = np.random.default_rng(12345)
+        X = np.asarray(d.low) + d.length * g.random((64, 3))
+        Y = np.asarray(d.low) + d.length * g.random((2, 3))
+        host = np.asarray(self.kernel.block(X, Y), dtype=np.float64)
+        xt = torch.from_numpy(X).to(self.device)
+        dev = np.empty_like(host)
+        for j in range(Y.shape[0]):
+            yt = torch.from_numpy(Y[j:j + 1].copy()).to(self.device)
+            wt = torch.ones((1, 1), dtype=torch.float64, device=self.device)
+            out = torch.empty((X.shape[0], 1), dtype=torch.float64, device=self.device)
+            _native.check(self.lib.bfmm_direct(self._handle, xt.data_ptr(), X.shape[0],
+                                               yt.data_ptr(), wt.data_ptr(), 1, 1,
+                                               out.data_ptr(), self._stream()), "bfmm_direct")
+            dev[:, j] = out[:, 0].cpu().numpy()
+        ok = np.isfinite(host)
+        scale = np.maximum(np.abs(host), 1e-300)
+        bad = ok & ~(np.abs(dev - host) <= 1e-11 * scale)
+        if bad.any() or not np.array_equal(ok, np.isfinite(dev)):
+            i, j = np.argwhere(bad | (ok != np.isfinite(dev)))[0]
+            raise ConfigurationError(
+                f"kernel {self.kernel.name!r}: cuda_expr {self.kernel.cuda_expr!r} gives "
+                f"{dev[i, j]!r} where the host hook gives {host[i, j]!r} "
+                f"(x={tuple(X[i])}, y={tuple(Y[j])}); the two forms must agree")
+
     def _upload_tables(self):
         torch = _torch()
         dev = self.device
@@ -237,11 +282,20 @@ class FmmEvaluator:
                         torch.from_numpy(cpow).to(self.device))
         return blk[key]
 
+    def _level_engine(self, lev, m, rp):
+        """The Chebyshev M2L engine of one level: self.m2l_mode, except that
+        the int8 kernels take rank tiles up to rp = 256 and 32-bit row
+        indices (8^lev * m < 2^31); larger plans (e.g. order 8 at eps 1e-10,
+        rank 288) run that level on the FP64 DMMA engine."""
+        if self.m2l_mode == "i8" and rp <= 256 and (1 << (3 * lev)) * m < (1 << 31):
+            return "i8"
+        return "dmma"
+
     def _m2l_translate(self, z, lt, lev, m, rp, ns, blk, st, q_lo=0, nq=0, cells=None, off=None):
         """lt = the 189-offset translation of z (engine.py:228-256), on the
-        engine self.m2l_mode selects; cells/off: listed active targets."""
+        level's engine (_level_engine); cells/off: listed active targets."""
         torch = _torch()
-        if self.m2l_mode == "i8":
+        if self._level_engine(lev, m, rp) == "i8":
             S = int(self.i8_slices)
             cs, cpow = self._i8_tables(blk, S)
             rows = z.numel() // rp
@@ -275,7 +329,7 @@ class FmmEvaluator:
         self._kspan(f"m2l_l{lev}", e0)
 
     def _m2l_splits(self, lev, m, rp, nq):
-        if self.m2l_mode == "i8":
+        if self._level_engine(lev, m, rp) == "i8":
             return int(self.lib.bfmm_m2l_i8_splits(lev, m, rp, nq))
         return int(self.lib.bfmm_m2l_cheb_splits(lev, m, rp, nq))
 
@@ -303,16 +357,48 @@ class FmmEvaluator:
             self._side[k] = torch.cuda.Stream(device=self.device)
         return self._side[k]
 
+    _STAGE_ELEMS = 1 << 23  # 64 MiB per half of the pinned staging buffer
+
+    def _h2d_into(self, dst, a):
+        """Copy a NumPy array (pageable host memory, the reference's calling
+        convention) into the device tensor dst: 64 MiB chunks go through the
+        evaluator's reusable two-half pinned buffer, so the host copy of one
+        chunk overlaps the DMA of the previous one and no O(N) pinned buffer
+        is allocated per call."""
+        torch = _torch()
+        src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).reshape(-1)
+        flat = dst.view(-1)
+        n = src.numel()
+        if n <= (1 << 16):
+            flat.copy_(src)
+            return dst
+        CH = self._STAGE_ELEMS
+        if getattr(self, "_stage", None) is None:
+            self._stage = torch.empty(2 * CH, dtype=torch.float64).pin_memory()
+            self._stage_ev = [torch.cuda.Event(), torch.cuda.Event()]
+            for e in self._stage_ev:
+                e.record()
+        st = torch.cuda.current_stream()
+        for i, off in enumerate(range(0, n, CH)):
+            k, b = min(CH, n - off), i % 2
+            self._stage_ev[b].synchronize()  # the DMA that last read this half is done
+            half = self._stage[b * CH:b * CH + k]
+            half.copy_(src[off:off + k])
+            flat[off:off + k].copy_(half, non_blocking=True)
+            self._stage_ev[b].record(st)
+        return dst
+
     def _prepare_points(self, arr, name):
         torch = _torch()
         if isinstance(arr, torch.Tensor):
             if arr.ndim != 2 or arr.shape[1] != 3:
                 raise ConfigurationError(f"{name} must be an (N, 3) array, got shape {tuple(arr.shape)}")
             return arr.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous()
-        pts = np.ascontiguousarray(arr, dtype=np.float64)
+        pts = np.asarray(arr)
         if pts.ndim != 2 or pts.shape[1] != 3:
             raise ConfigurationError(f"{name} must be an (N, 3) array, got shape {np.shape(arr)}")
-        return torch.from_numpy(pts).to(self.device, non_blocking=True)
+        out = torch.empty(pts.shape, dtype=torch.float64, device=self.device)
+        return self._h2d_into(out, pts)
 
     def _prepare_weights(self, w, n_src):
         torch = _torch()
@@ -325,14 +411,15 @@ class FmmEvaluator:
                 raise ConfigurationError(
                     f"weights shape {tuple(w.shape)} does not match {n_src} sources")
             return wt.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous(), squeeze
-        wa = np.ascontiguousarray(w, dtype=np.float64)
+        wa = np.asarray(w)
         squeeze = wa.ndim == 1
         if squeeze:
             wa = wa[:, None]
         if wa.ndim != 2 or wa.shape[0] != n_src:
             raise ConfigurationError(
                 f"weights shape {np.shape(w)} does not match {n_src} sources")
-        return torch.from_numpy(wa).to(self.device, non_blocking=True), squeeze
+        out = torch.empty(wa.shape, dtype=torch.float64, device=self.device)
+        return self._h2d_into(out, wa), squeeze
 
     def _geom(self):
         d = self.plan.domain
@@ -622,24 +709,30 @@ class FmmEvaluator:
         ``_shard`` = (MortonShards, ShardComm) runs this call as one rank of a
         multi-GPU matvec (paper_1903_02153_b200.parallel.ShardedEvaluator)."""
         torch = _torch()
+        with torch.cuda.device(self.device):
+            return self._evaluate(sources, targets, weights, _shard)
+
+    def _evaluate(self, sources, targets, weights, _shard):
+        torch = _torch()
         sharded = _shard is not None and not _shard[0].full
         shared = targets is None or targets is sources
         as_tensor = isinstance(sources, torch.Tensor)
         out_device = sources.device if as_tensor else None
         if not as_tensor:
-            # host-side validation mirrors the reference (eng:51-57, 484-497)
+            # shape validation mirrors the reference (eng:51-57, 484-497); the
+            # O(N) finiteness checks of points and weights run on the device
+            # (tree build / weight gather status flags, _raise_flags) in the
+            # reference's order: sources, targets, weights
             src_np = np.asarray(sources)
-            _check_host_points(src_np, "sources")
+            _check_host_shape(src_np, "sources")
             if not shared:
-                _check_host_points(np.asarray(targets), "targets")
+                _check_host_shape(np.asarray(targets), "targets")
             if weights is None:
                 raise ConfigurationError("weights are required")
-            w_np = np.asarray(weights, dtype=np.float64)
-            if w_np.ndim not in (1, 2) or w_np.shape[0] != src_np.shape[0]:
+            w_shape = np.shape(weights)
+            if len(w_shape) not in (1, 2) or w_shape[0] != src_np.shape[0]:
                 raise ConfigurationError(
-                    f"weights shape {np.shape(weights)} does not match {src_np.shape[0]} sources")
-            if w_np.size and not np.all(np.isfinite(w_np)):
-                raise ConfigurationError("weights contain non-finite values")
+                    f"weights shape {w_shape} does not match {src_np.shape[0]} sources")
         if self._graph_ok(sources, targets, weights, sharded, shared):
             return self._graph_evaluate(sources, weights, as_tensor, out_device)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
@@ -709,7 +802,8 @@ class FmmEvaluator:
             torch.cuda.current_stream().wait_event(w_event)
         ws = torch.empty((max(n_src, 1), m), dtype=torch.float64, device=self.device)
         _native.check(self.lib.bfmm_gather_weights(w.data_ptr(), n_src, m, stree.perm.data_ptr(),
-                                                   ws.data_ptr(), stree.pts4.data_ptr(), st),
+                                                   ws.data_ptr(), stree.pts4.data_ptr(),
+                                                   status[_ST_WEIGHTS:].data_ptr(), st),
                       "bfmm_gather_weights")
         if ev:
             ev[2].record()
@@ -818,6 +912,15 @@ class FmmEvaluator:
         # the sparse-cloud active lists read counts back on the host
         return self.far_mode == "dense" or (self.far_mode == "auto" and n >= 8 * (1 << (3 * L)))
 
+    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "far_mode", "near_mode", "overlap_near",
+                    "near_after_far", "far_priority", "l2p_mode", "stream_levels",
+                    "main_levels")
+
+    def _graph_knobs(self):
+        """Every evaluator knob that changes the captured kernels: part of
+        the graph key, so changing one after a capture re-captures."""
+        return tuple(getattr(self, k) for k in self._GRAPH_KNOBS)
+
     def _graph_evaluate(self, sources, weights, as_tensor, out_device):
         """evaluate() through a captured CUDA graph of _device_step (identical
         kernels and buffers, so identical results: tests/test_gpu_graph.py).
@@ -847,12 +950,13 @@ class FmmEvaluator:
         def plain(t, dev):
             return (t.dtype == torch.float64 and t.is_contiguous() and
                     (t.is_cuda if dev else (not t.is_cuda and t.is_pinned())))
+        knobs = self._graph_knobs()
         if plain(src_t, True) and plain(w_t, True) and src_t.device == self.device:
-            kind, key = "device", ("device", n, m, src_t.data_ptr(), w_t.data_ptr())
+            kind, key = "device", ("device", n, m, src_t.data_ptr(), w_t.data_ptr(), knobs)
         elif plain(src_t, False) and plain(w_t, False):
-            kind, key = "pinned", ("pinned", n, m, src_t.data_ptr(), w_t.data_ptr())
+            kind, key = "pinned", ("pinned", n, m, src_t.data_ptr(), w_t.data_ptr(), knobs)
         else:
-            kind, key = "static", ("static", n, m)
+            kind, key = "static", ("static", n, m, knobs)
         ent = self._graphs.get(key)
         if ent is None:
             if len(self._graphs) >= 4:  # each graph keeps its memory pool
@@ -894,8 +998,11 @@ class FmmEvaluator:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if stat_in is not None:
-            stat_in[0].copy_(src_t, non_blocking=True)
-            stat_in[1].copy_(w_t, non_blocking=True)
+            for dst, a in ((stat_in[0], src_t), (stat_in[1], w_t)):
+                if a.is_cuda or a.is_pinned():
+                    dst.copy_(a, non_blocking=True)
+                else:
+                    self._h2d_into(dst, a.numpy())
         g.replay()
         self.graph_launches += nlaunch  # our kernels inside the replayed graph
         phi, status, ttree, stree, _ = outs
@@ -918,8 +1025,15 @@ class FmmEvaluator:
         return result[:, 0] if squeeze else result
 
     def _raise_flags(self, stat, ttree, stree):
-        if stat[_ST_DOMAIN_SRC] & 2 or stat[_ST_DOMAIN_TGT] & 2:
-            raise DomainError("points contain non-finite coordinates")
+        # the reference's order: non-finite sources, then targets (eng:51-57,
+        # 485-486), non-finite weights (eng:496-497), then the domain check
+        # of the tree (oct:190-196)
+        if stat[_ST_DOMAIN_SRC] & 2:
+            raise DomainError("sources contain non-finite coordinates")
+        if stat[_ST_DOMAIN_TGT] & 2:
+            raise DomainError("targets contain non-finite coordinates")
+        if stat[_ST_WEIGHTS]:
+            raise ConfigurationError("weights contain non-finite values")
         if stat[_ST_DOMAIN_SRC] or stat[_ST_DOMAIN_TGT]:
             d = self.plan.domain
             raise DomainError(f"a point lies outside the box centered at {d.center} "
@@ -993,11 +1107,9 @@ class FmmEvaluator:
         return tseg, o[tseg]
 
 
-def _check_host_points(pts, name):
+def _check_host_shape(pts, name):
     if pts.ndim != 2 or pts.shape[1] != 3:
         raise ConfigurationError(f"{name} must be an (N, 3) array, got shape {np.shape(pts)}")
-    if pts.size and not np.all(np.isfinite(pts)):
-        raise DomainError(f"{name} contain non-finite coordinates")
 
 
 def direct_evaluate(kernel: KernelSpec, sources, targets=None, weights=None,

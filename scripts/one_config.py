@@ -1,4 +1,6 @@
-"""One warm matvec of a config (for ncu launch lists): python scripts/one_config.py C5 [scale]"""
+"""One warm matvec of a config (for ncu launch lists / metric captures):
+python scripts/one_config.py C5 [scale]  -- prints the stage timings and the
+near-field pair count.  Near field and far-field levels serialised."""
 import sys
 
 import numpy as np
@@ -16,6 +18,7 @@ plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"], e
                   domain_center=wl["center"], domain_length=wl["length"], n_cols=wl["ncols"])
 ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir="/tmp/bfmm_cfg_cache")
 ev.stream_levels = False  # serial levels: clean per-kernel times
+ev.overlap_near = False
 X = torch.from_numpy(wl["points"]).cuda()
 W = torch.from_numpy(np.ascontiguousarray(wl["weights"])).cuda()
 for _ in range(2):

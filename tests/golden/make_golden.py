@@ -22,7 +22,14 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
-sys.path.insert(0, "/root/reference/pkg/src")
+# the reference: /root/reference in the builder container, or the unmodified
+# install under baseline/_ref (scripts/install_reference.sh) on the GPU box
+_REF_SRC = os.environ.get("BOXFMM_SRC") or next(
+    (p for p in ("/root/reference/pkg/src", os.path.join(HERE, "..", "..", "baseline", "_ref"))
+     if os.path.isdir(os.path.join(p, "boxfmm"))), None)
+if _REF_SRC is None:
+    raise SystemExit("reference boxfmm not found (set BOXFMM_SRC)")
+sys.path.insert(0, _REF_SRC)
 
 import boxfmm  # noqa: E402
 from boxfmm import engine as reng  # noqa: E402
@@ -33,7 +40,7 @@ from boxfmm.plan import FmmPlan  # noqa: E402
 
 from paper_1903_02153_b200 import workloads  # noqa: E402
 
-CACHE = "/tmp/golden_cache"
+CACHE = os.environ.get("BOXFMM_CACHE", "/tmp/golden_cache")
 
 
 def ref_kernel(key):
@@ -274,6 +281,89 @@ def case_config(name, scale, direct=True, threads=1):
     save(f"{name.lower()}_s{scale}", **out)
 
 
+def case_full(name, threads, direct=True):
+    """One full-size reference run of a BASELINE config:
+    the partition digests, phi at the 1,000 check targets and on a fixed
+    stride of the sorted-index range, and the direct sum at the check
+    targets.  C3/C5 need more RAM than the builder container has: run this on
+    the GPU host with the unmodified reference installed under baseline/_ref
+    (scripts/gen_full_fixtures.sh)."""
+    wl = workloads.make(name, 0)
+    kernel = ref_kernel(wl["kernel"])
+    plan = plan_of(wl)
+    X, w = wl["points"], wl["weights"]
+    n = X.shape[0]
+    t0 = time.perf_counter()
+    ev = reng.FmmEvaluator(kernel, plan, cache_dir=CACHE, threads=threads)
+    part = reng._Partition.build(ev.tree, X)
+    out = {"perm_sha": np.array(sha(part.perm.astype(np.int64))),
+           "leaves_sha": np.array(sha(part.leaves.astype(np.int64))),
+           "starts_sha": np.array(sha(part.starts.astype(np.int64))),
+           "counts_sha": np.array(sha(part.counts.astype(np.int64))),
+           "n_leaves": np.array(len(part.leaves)),
+           "max_count": np.array(int(part.counts.max())),
+           "perm_head": part.perm[:4096].astype(np.int64),
+           "center": np.array(wl["center"]), "length": np.array(wl["length"])}
+    del part
+    print(name, "partition", time.perf_counter() - t0, "s", flush=True)
+    t0 = time.perf_counter()
+    phi = ev.evaluate(X, weights=w)
+    secs = time.perf_counter() - t0
+    idx = wl["check_idx"]
+    stride = max(1, n // 65536)
+    out.update({"phi_idx": phi[idx], "phi_norm": np.array(np.linalg.norm(phi, axis=0)),
+                "phi_sum": np.array(phi.sum(axis=0)), "stride": np.array(stride),
+                "phi_stride": phi[::stride][:65536], "seconds": np.array(secs),
+                "threads": np.array(threads),
+                "timings": np.array([ev.timings[k] for k in
+                                     ("distribute", "upward", "far_field", "downward",
+                                      "near_field", "near_pairs", "total")])})
+    print(name, "evaluate", secs, "s", ev.timings, flush=True)
+    del phi, ev
+    if not direct:
+        # C5: the reference's long-double direct sum over 64M sources takes
+        # ~30 min; the GPU test computes the direct sum (bfmm_direct, pinned
+        # to the reference's direct_evaluate on C1, C2 and the scaled
+        # configs) and compares both phi_idx against it
+        save(f"{name.lower()}_full", **out)
+        return
+    t0 = time.perf_counter()
+    d = reng.direct_evaluate(kernel, X, targets=X[idx], weights=w)
+    out["direct_idx"] = d
+    out["direct_seconds"] = np.array(time.perf_counter() - t0)
+    out["rel_l2_vs_direct"] = np.array(np.linalg.norm(out["phi_idx"] - d) / np.linalg.norm(d))
+    print(name, "rel l2 vs direct", float(out["rel_l2_vs_direct"]), flush=True)
+    save(f"{name.lower()}_full", **out)
+
+
+def case_highorder():
+    """The reference's plan range beyond the BASELINE configs (plan.py:37-38,
+    ops:296-329): ranks above 256 (order 8 at eps 1e-10: r = 288), orders 1,
+    7, 9-12, and 16 / 120 weight columns."""
+    out = {}
+    cases = {
+        "p8r288": ("laplacian", 3, 8, "chebyshev", 1e-10, 2500, 1),
+        "p12": ("laplacian", 2, 12, "chebyshev", 1e-7, 1500, 1),
+        "p9m16": ("exponential", 2, 9, "chebyshev", 1e-9, 1500, 16),
+        "p1m120": ("gaussian", 3, 1, "chebyshev", 1e-5, 2000, 120),
+        "p7u": ("laplacianforce", 3, 7, "uniform", 1e-5, 2000, 3),
+        "p5m120": ("exponential", 3, 5, "chebyshev", 1e-7, 1500, 120),
+    }
+    for tag, (kname, L, p, scheme, eps, n, m) in cases.items():
+        pts, w = unit_cloud(n, seed=100 + p, ncols=m)
+        plan = FmmPlan(levels=L, order=p, scheme=scheme, eps=eps,
+                       domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+        t0 = time.perf_counter()
+        phi, secs, ev = _run(kernel_by_name(kname), plan, pts, w)
+        blk = ev.table.blocks[min(ev.table.blocks)]
+        out[f"{tag}_phi"] = phi
+        out[f"{tag}_rank"] = np.array(getattr(blk, "rank", -1))
+        out[f"{tag}_cfg"] = np.array([L, p, n, m, eps, 0 if scheme == "chebyshev" else 1])
+        out[f"{tag}_kernel"] = np.array(kname)
+        print(tag, "rank", out[f"{tag}_rank"], f"{time.perf_counter() - t0:.1f}s", flush=True)
+    save("highorder", **out)
+
+
 def case_eig():
     """randomized_eig on the FMM matvec, k + q = 120 columns (lin:39-104)."""
     from boxfmm.linops import evaluator_matvec, randomized_eig
@@ -360,6 +450,10 @@ CASES = {
     "c5s2": lambda: case_config("C5", 2, threads=8),
     "c3s1": lambda: case_config("C3", 1, threads=8),
     "c4s1": lambda: case_config("C4", 1, threads=8),
+    "highorder": case_highorder,
+    "c3full": lambda: case_full("C3", int(os.environ.get("BOXFMM_THREADS", "8"))),
+    "c4full": lambda: case_full("C4", int(os.environ.get("BOXFMM_THREADS", "6"))),
+    "c5full": lambda: case_full("C5", int(os.environ.get("BOXFMM_THREADS", "2")), direct=False),
 }
 
 if __name__ == "__main__":

@@ -230,6 +230,11 @@ def test_stage_moments_and_locals_match_oracle(cache_dir):
     for lev, mom in orc.stage["M"].items():
         got = ev.stages["moments"][lev].view(-1, 1, p3).cpu().numpy().transpose(0, 2, 1)
         assert rel_l2(got, mom) < 1e-12, lev
+    # per-level locals after M2L + L2L, every level 2..L
+    assert sorted(orc.stage["locals"]) == list(range(2, wl["levels"] + 1))
+    for lev, loc in orc.stage["locals"].items():
+        got = ev.stages["locals"][lev].view(-1, 1, p3).cpu().numpy().transpose(0, 2, 1)
+        assert rel_l2(got, loc) < 1e-12, lev
 
 
 # ---------------------------------------------------------------------------
