@@ -277,6 +277,16 @@ int bfmm_p2p_symmetric(int handle, const double *pts4, const int64_t *leaves,
                        double sign, double *out, void *scratch,
                        size_t scratch_bytes, bfmm_stream_t stream);
 
+/* Kernel values on point-pair grids for the M2L table build on the device
+ * (replaces the host assembly of operators.py:244-258 `_dense_family` and
+ * operators.py:88-108 `uniform_difference_grid`):
+ *   out[t][a][b] = K(xt[a] - (ys[b] + shift[t]))   t < nt, a < na, b < nb
+ * with the functor `handle` (built-in or NVRTC).  xt (na, 3), ys (nb, 3),
+ * shift (nt, 3) device arrays; a non-finite value sets *bad |= 1 (device). */
+int bfmm_kernel_block(int handle, const double *xt, int64_t na, const double *ys,
+                      int64_t nb, const double *shift, int nt, double *out,
+                      int32_t *bad, bfmm_stream_t stream);
+
 /* Direct O(nt * ns) sum, the reference's direct_evaluate (engine.py:565-624):
  * out[i][c] = sum_j K(t_i - s_j) w[j][c] with explicit differences
  * (coincident points give r = 0 exactly) and Neumaier-compensated

@@ -66,6 +66,7 @@ SIGNATURES = {
     "bfmm_p2p_symmetric": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _I64, _I64, _I64, _D,
                                 _P, _P, _SZ, _P]),
     "bfmm_direct": (_I, [_I, _P, _I64, _P, _P, _I64, _I, _P, _P]),
+    "bfmm_kernel_block": (_I, [_I, _P, _I64, _P, _I64, _P, _I, _P, _P, _P]),
     "bfmm_p2p_locate": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _P, _P]),
     "bfmm_scatter_output": (_I, [_P, _P, _P, _I64, _I, _P, _P, _P]),
     "bfmm_far_pairs": (_I, [_I, _I, _P, _P, _P, _P, _SZ, _P]),

@@ -40,105 +40,123 @@ __device__ __forceinline__ int64_t lex_of(int x, int y, int z, int n) {
 
 // The transforms work on G lexicographically consecutive cells (a z-run)
 // per CTA pass, so the frequency-major spectra are written / read as
-// G * 16-byte runs instead of isolated 16-byte values, and every
-// spectrum value is touched once.  Twiddles come from a q x q shared table
-// tw[a][b] = e^{2 pi i (a b mod q) / q} (no integer modulo in the loops).
-// G = 2 cells per run when the tiles fit in shared memory, else 1 (large
-// p); fft_group() picks it.
+// G * 16-byte runs, and every spectrum value is touched once.  Each 1-D DFT
+// line (p inputs -> q bins, or back) is computed by ONE thread in
+// registers: its inputs are loaded once, every output is an independent
+// FMA chain, and the twiddles e^{2 pi i r / q} are read from the kernel
+// parameter bank at compile-time indices (r = j k mod q, all loops
+// unrolled on P) -- so a line costs p loads + q stores for 4pq DFMAs,
+// instead of one shared-memory twiddle and one input load per MAC.
+template <int P, int G>
+struct FftShape {
+  static constexpr int p = P, q = 2 * P - 1, h = q / 2 + 1, F = q * q * h;
+  static constexpr int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
+  // forward: {in [G][p^3] real, B [G][p][q][h]} and {A [G][p][p][h], stage [F][G]}
+  // share storage (in dies before B is written, A before stage)
+  static constexpr size_t U1 = (sizeof(double) * G * P3 > sizeof(double2) * G * PQH)
+                                   ? sizeof(double) * G * P3 : sizeof(double2) * G * PQH;
+  static constexpr size_t U2 = (sizeof(double2) * G * PPH > sizeof(double2) * F * G)
+                                   ? sizeof(double2) * G * PPH : sizeof(double2) * F * G;
+  static constexpr size_t smem = U1 + U2;
+  // inverse: {stage [F][G], D [G][p][p][h]} (stage dies before D is
+  // written) and C [G][p][q][h]
+  static constexpr size_t V1 = (F > PPH ? F : PPH) * sizeof(double2) * G;
+  static constexpr size_t smem_inv = V1 + sizeof(double2) * G * PQH;
+  static constexpr size_t most = smem > smem_inv ? smem : smem_inv;
+};
 
-__device__ __forceinline__ void stage_twiddles(const FftGeom &g, double2 *tw) {
-  for (int e = threadIdx.x; e < g.q * g.q; e += blockDim.x) {
-    const int r = ((e / g.q) * (e % g.q)) % g.q;
-    tw[e] = make_double2(g.c[r], g.s[r]);
-  }
-}
-
-inline size_t fft_fwd_smem(const FftGeom &g, int G) {
-  const size_t F = size_t(g.q) * g.q * g.h;
-  return sizeof(double2) * (g.q * g.q + G * (g.p * g.p * g.h + g.p * g.q * g.h) + F * G) +
-         sizeof(double) * G * g.p * g.p * g.p;
-}
-
-// ---- 1. forward transform: X[col][f][lex] = rfftn(pad_q(M[cell, col]))[f] ---
-// P is a template parameter so the short DFT sums unroll and each thread's
-// independent outputs (2 per pass iteration) interleave their FMA chains.
+// cells per CTA pass: 4 when both kernels fit 3 CTAs per SM, else fewer
 template <int P>
+constexpr int fft_cells() {
+  return FftShape<P, 4>::most <= 72 * 1024 ? 4 : FftShape<P, 2>::most <= 100 * 1024 ? 2 : 1;
+};
+
+template <int P, int G>
 __global__ void __launch_bounds__(128)
 fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
-               int cc, FftGeom g, int G, double2 *__restrict__ X) {
-  extern __shared__ double2 sm2[];
-  constexpr int p = P, q = 2 * P - 1, h = q / 2 + 1, F = q * q * h;
-  const int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
+               int cc, FftGeom g, double2 *__restrict__ X) {
+  using Sh = FftShape<P, G>;
+  constexpr int p = Sh::p, q = Sh::q, h = Sh::h, F = Sh::F;
+  constexpr int P3 = Sh::P3, PPH = Sh::PPH, PQH = Sh::PQH;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double *in = reinterpret_cast<double *>(smraw);            // [G][p^3]
+  double2 *B = reinterpret_cast<double2 *>(smraw);           // [G][p][q][h]
+  double2 *A = reinterpret_cast<double2 *>(smraw + Sh::U1);  // [G][p][p][h]
+  double2 *stage = A;                                        // [F][G]
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
   const int64_t ngroups = ncell / G;
-  double2 *tw = sm2;                   // [q][q]
-  double2 *A = tw + q * q;             // [G][p][p][h]  z transformed
-  double2 *B = A + G * PPH;        // [G][p][q][h]  y transformed
-  double2 *stage = B + G * PQH;    // [F][G]        x transformed
-  double *in = reinterpret_cast<double *>(stage + F * G);  // [G][p^3]
-  stage_twiddles(g, tw);
   for (int64_t w = blockIdx.x; w < ngroups * cc; w += gridDim.x) {
     const int crel = (int)(w / ngroups);
     const int64_t lex0 = (w - crel * ngroups) * G;
+    const int x = (int)(lex0 / ((int64_t)n * n)), y = (int)((lex0 / n) % n), z0 = (int)(lex0 % n);
     __syncthreads();
-    #pragma unroll 2
     for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
       const int gi = e / P3, r = e - gi * P3;
-      const int64_t lex = lex0 + gi;
-      const int x = (int)(lex / ((int64_t)n * n)), y = (int)((lex / n) % n), z = (int)(lex % n);
-      in[e] = moments[((int64_t)morton3(x, y, z) * m + c0 + crel) * P3 + r];
+      in[e] = moments[((int64_t)morton3(x, y, z0 + gi) * m + c0 + crel) * P3 + r];
     }
     __syncthreads();
-    // z: real -> h complex bins, e^{-2 pi i k kz / q}
-    #pragma unroll 2
-    for (int e = threadIdx.x; e < G * PPH; e += blockDim.x) {
-      const int gi = e / PPH, r = e - gi * PPH, ij = r / h, kz = r - ij * h;
-      const double *v = in + gi * P3 + ij * p;
-      double re = 0.0, im = 0.0;
+    // z: p reals -> h bins, e^{-2 pi i k kz / q}; one line (gi, i, j) per thread
+    for (int l = threadIdx.x; l < G * p * p; l += blockDim.x) {
+      double v[p];
 #pragma unroll
-      for (int k = 0; k < p; ++k) {
-        const double2 t = tw[k * q + kz];
-        re = fma(v[k], t.x, re);
-        im = fma(-v[k], t.y, im);
+      for (int k = 0; k < p; ++k) v[k] = in[l * p + k];
+      double2 *dst = A + l * h;
+#pragma unroll
+      for (int kz = 0; kz < h; ++kz) {
+        double re = v[0], im = 0.0;
+#pragma unroll
+        for (int k = 1; k < p; ++k) {
+          const int r = (k * kz) % q;
+          re = fma(v[k], g.c[r], re);
+          im = fma(-v[k], g.s[r], im);
+        }
+        dst[kz] = make_double2(re, im);
       }
-      A[e] = make_double2(re, im);
     }
     __syncthreads();
-    // y: p inputs -> q bins
-    #pragma unroll 2
-    for (int e = threadIdx.x; e < G * PQH; e += blockDim.x) {
-      const int gi = e / PQH, r = e - gi * PQH;
-      const int i = r / (q * h), rem = r - i * q * h, ky = rem / h, kz = rem - ky * h;
+    // y: p inputs -> q bins; line (gi, i, kz)
+    for (int l = threadIdx.x; l < G * p * h; l += blockDim.x) {
+      const int gi = l / (p * h), r0 = l - gi * p * h, i = r0 / h, kz = r0 - i * h;
       const double2 *a = A + gi * PPH + i * p * h + kz;
-      double re = 0.0, im = 0.0;
+      double2 v[p];
 #pragma unroll
-      for (int j = 0; j < p; ++j) {
-        const double2 t = tw[j * q + ky], v = a[j * h];
-        re = fma(v.x, t.x, fma(v.y, t.y, re));  // (v.x + i v.y)(c - i s)
-        im = fma(v.y, t.x, fma(-v.x, t.y, im));
+      for (int j = 0; j < p; ++j) v[j] = a[j * h];
+      double2 *dst = B + gi * PQH + i * q * h + kz;
+#pragma unroll
+      for (int ky = 0; ky < q; ++ky) {
+        double re = v[0].x, im = v[0].y;
+#pragma unroll
+        for (int j = 1; j < p; ++j) {
+          const int r = (j * ky) % q;  // (v.x + i v.y)(c - i s)
+          re = fma(v[j].x, g.c[r], fma(v[j].y, g.s[r], re));
+          im = fma(v[j].y, g.c[r], fma(-v[j].x, g.s[r], im));
+        }
+        dst[ky * h] = make_double2(re, im);
       }
-      B[e] = make_double2(re, im);
     }
     __syncthreads();
-    // x: p inputs -> q bins, into the [f][cell] staging tile
-    #pragma unroll 2
-    for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
-      const int f = e / G, gi = e - f * G;
-      const int kx = f / (q * h), rem = f - kx * q * h;
+    // x: p inputs -> q bins, into the [f][cell] staging tile; line (gi, ky, kz)
+    for (int l = threadIdx.x; l < G * q * h; l += blockDim.x) {
+      const int gi = l / (q * h), rem = l - gi * q * h;
       const double2 *b = B + gi * PQH + rem;
-      double re = 0.0, im = 0.0;
+      double2 v[p];
 #pragma unroll
-      for (int i = 0; i < p; ++i) {
-        const double2 t = tw[i * q + kx], v = b[i * q * h];
-        re = fma(v.x, t.x, fma(v.y, t.y, re));
-        im = fma(v.y, t.x, fma(-v.x, t.y, im));
+      for (int i = 0; i < p; ++i) v[i] = b[i * q * h];
+#pragma unroll
+      for (int kx = 0; kx < q; ++kx) {
+        double re = v[0].x, im = v[0].y;
+#pragma unroll
+        for (int i = 1; i < p; ++i) {
+          const int r = (i * kx) % q;
+          re = fma(v[i].x, g.c[r], fma(v[i].y, g.s[r], re));
+          im = fma(v[i].y, g.c[r], fma(-v[i].x, g.s[r], im));
+        }
+        stage[(kx * q * h + rem) * G + gi] = make_double2(re, im);
       }
-      stage[e] = make_double2(re, im);
     }
     __syncthreads();
     double2 *dst = X + (int64_t)crel * F * ncell + lex0;
-    #pragma unroll 2
     for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
       const int f = e / G, gi = e - f * G;
       dst[(int64_t)f * ncell + gi] = stage[e];
@@ -214,24 +232,34 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
   double2 acc[kR];
 #pragma unroll
   for (int k = 0; k < kR; ++k) acc[k] = make_double2(0.0, 0.0);
-  // parity rule: +3 needs an even target coordinate, -3 an odd one
-  const int px = x & 1, py = y & 1, pzz = (z0 + pz) & 1;
-  for (int a = -3; a <= 3; ++a) {
-    if ((a == 3 && px) || (a == -3 && !px)) continue;
-    for (int b = -3; b <= 3; ++b) {
-      if ((b == 3 && py) || (b == -3 && !py)) continue;
-      // the z column of sources for all 8 targets and all 7 z offsets
-      double2 seg[kR * 2 + 5];
-      const double2 *col_src = &halo[ix + 3 + a][iy + 3 + b][pz];
+  // Parity rule (octree.py:128-145): +3 needs an even target coordinate,
+  // -3 an odd one, so a target of parity p along an axis takes the offsets
+  // t = t' - p, t' in [-2, 3].  x and y parities are warp-uniform; along z
+  // the tile starts even, so target z0 + pz + 2k with source offset
+  // c = c' - pz reads source z0 + 2k + c' -- the same source column for both
+  // z parities (only the tap differs per lane): no divergence, no skipped
+  // lanes, 12 source loads serve 6 x 4 complex MACs.  For the near (a, b)
+  // columns (|a|, |b| <= 1) only |c| >= 2 taps are nonzero: c' in
+  // {-2, -1, 2, 3} covers both parities (one of the four is zero per lane).
+  const int px = x & 1, py = y & 1;
+  for (int ap = -2; ap <= 3; ++ap) {
+    const int a = ap - px;
+#pragma unroll 2
+    for (int bp = -2; bp <= 3; ++bp) {
+      const int b = bp - py;
+      double2 seg[2 * kR + 4];
+      const double2 *col_src = &halo[ix + 3 + a][iy + 3 + b][1];  // source z0 - 2
 #pragma unroll
-      for (int u = 0; u < kR * 2 + 5; ++u) seg[u] = col_src[u];
+      for (int u = 0; u < 2 * kR + 4; ++u) seg[u] = col_src[u];
+      const double2 *tp = &taps[a + 3][b + 3][3 - pz];  // tap of c' = tp[c']
+      const bool near_col = a >= -1 && a <= 1 && b >= -1 && b <= 1;  // warp-uniform
 #pragma unroll
-      for (int c = -3; c <= 3; ++c) {
-        if ((c == 3 && pzz) || (c == -3 && !pzz)) continue;
-        const double2 s = taps[a + 3][b + 3][c + 3];  // zero for near offsets
+      for (int cp = -2; cp <= 3; ++cp) {
+        if (near_col && (cp == 0 || cp == 1)) continue;
+        const double2 s = tp[cp];
 #pragma unroll
         for (int k = 0; k < kR; ++k) {
-          const double2 v = seg[c + 3 + 2 * k];
+          const double2 v = seg[cp + 2 + 2 * k];
           acc[k].x = fma(s.x, v.x, fma(-s.y, v.y, acc[k].x));
           acc[k].y = fma(s.x, v.y, fma(s.y, v.x, acc[k].y));
         }
@@ -247,35 +275,22 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
 }
 
 // ---- 3. inverse transform + crop + scale ------------------------------------
-inline size_t fft_inv_smem(const FftGeom &g, int G) {
-  const size_t F = size_t(g.q) * g.q * g.h;
-  return sizeof(double2) * (g.q * g.q + F * G + G * (g.p * g.q * g.h + g.p * g.p * g.h));
-}
-
-inline int fft_group(const FftGeom &g) {
-  // measured on C3 (p = 6): G = 2 (4 CTAs/SM) 661 ms, G = 4 763 ms, G = 1 712 ms
-  for (int G = 2; G > 1; G /= 2)
-    if (std::max(fft_fwd_smem(g, G), fft_inv_smem(g, G)) <= 200 * 1024) return G;
-  return 1;
-}
-
-template <int P>
+template <int P, int G>
 __global__ void __launch_bounds__(128)
 fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_t cell_hi,
-               int m, int c0, int cc, FftGeom g, int G, double scale,
+               int m, int c0, int cc, FftGeom g, double scale,
                double *__restrict__ locals) {
-  extern __shared__ double2 sm2[];
-  constexpr int p = P, q = 2 * P - 1, h = q / 2 + 1, F = q * q * h;
-  const int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
+  using Sh = FftShape<P, G>;
+  constexpr int p = Sh::p, q = Sh::q, h = Sh::h, F = Sh::F;
+  constexpr int P3 = Sh::P3, PPH = Sh::PPH, PQH = Sh::PQH;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2 *stage = reinterpret_cast<double2 *>(smraw);           // [F][G]
+  double2 *D = stage;                                            // [G][p][p][h]  y inverted, j < p
+  double2 *C = reinterpret_cast<double2 *>(smraw + Sh::V1);      // [G][p][q][h]  x inverted, i < p
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
   const int64_t ngroups = ncell / G;
-  double2 *tw = sm2;                 // [q][q]
-  double2 *stage = tw + q * q;       // [F][G]
-  double2 *C = stage + F * G;    // [G][p][q][h]  x inverted, i < p
-  double2 *D = C + G * PQH;      // [G][p][p][h]  y inverted, j < p
   const double norm = scale / ((double)q * q * q);
-  stage_twiddles(g, tw);
   for (int64_t w = blockIdx.x; w < ngroups * cc; w += gridDim.x) {
     const int crel = (int)(w / ngroups);
     const int64_t lex0 = (w - crel * ngroups) * G;
@@ -289,57 +304,74 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
     if (!any) continue;  // uniform across the CTA
     __syncthreads();
     const double2 *src = Y + (int64_t)crel * F * ncell + lex0;
-    #pragma unroll 2
     for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
       const int f = e / G, gi = e - f * G;
       stage[e] = src[(int64_t)f * ncell + gi];
     }
     __syncthreads();
-    // x: q bins -> p outputs, e^{+2 pi i i kx / q}
-    #pragma unroll 2
-    for (int e = threadIdx.x; e < G * PQH; e += blockDim.x) {
-      const int gi = e / PQH, r = e - gi * PQH, i = r / (q * h), rem = r - i * q * h;
-      double re = 0.0, im = 0.0;
+    // x: q bins -> p outputs, e^{+2 pi i i kx / q}; line (gi, ky, kz)
+    for (int l = threadIdx.x; l < G * q * h; l += blockDim.x) {
+      const int gi = l / (q * h), rem = l - gi * q * h;
+      double2 v[q];
 #pragma unroll
-      for (int kx = 0; kx < q; ++kx) {
-        const double2 t = tw[i * q + kx], v = stage[(kx * q * h + rem) * G + gi];
-        re = fma(v.x, t.x, fma(-v.y, t.y, re));
-        im = fma(v.y, t.x, fma(v.x, t.y, im));
+      for (int kx = 0; kx < q; ++kx) v[kx] = stage[(kx * q * h + rem) * G + gi];
+      double2 *dst = C + gi * PQH + rem;
+#pragma unroll
+      for (int i = 0; i < p; ++i) {
+        double re = v[0].x, im = v[0].y;
+#pragma unroll
+        for (int kx = 1; kx < q; ++kx) {
+          const int r = (i * kx) % q;
+          re = fma(v[kx].x, g.c[r], fma(-v[kx].y, g.s[r], re));
+          im = fma(v[kx].y, g.c[r], fma(v[kx].x, g.s[r], im));
+        }
+        dst[i * q * h] = make_double2(re, im);
       }
-      C[e] = make_double2(re, im);
     }
     __syncthreads();
-    // y: q bins -> p outputs
-    #pragma unroll 2
-    for (int e = threadIdx.x; e < G * PPH; e += blockDim.x) {
-      const int gi = e / PPH, r = e - gi * PPH, i = r / (p * h), rem = r - i * p * h;
-      const int j = rem / h, kz = rem - j * h;
+    // y: q bins -> p outputs; line (gi, i, kz)
+    for (int l = threadIdx.x; l < G * p * h; l += blockDim.x) {
+      const int gi = l / (p * h), r0 = l - gi * p * h, i = r0 / h, kz = r0 - i * h;
       const double2 *c = C + gi * PQH + i * q * h + kz;
-      double re = 0.0, im = 0.0;
+      double2 v[q];
 #pragma unroll
-      for (int ky = 0; ky < q; ++ky) {
-        const double2 t = tw[j * q + ky], v = c[ky * h];
-        re = fma(v.x, t.x, fma(-v.y, t.y, re));
-        im = fma(v.y, t.x, fma(v.x, t.y, im));
+      for (int ky = 0; ky < q; ++ky) v[ky] = c[ky * h];
+      double2 *dst = D + gi * PPH + i * p * h + kz;
+#pragma unroll
+      for (int j = 0; j < p; ++j) {
+        double re = v[0].x, im = v[0].y;
+#pragma unroll
+        for (int ky = 1; ky < q; ++ky) {
+          const int r = (j * ky) % q;
+          re = fma(v[ky].x, g.c[r], fma(-v[ky].y, g.s[r], re));
+          im = fma(v[ky].y, g.c[r], fma(v[ky].x, g.s[r], im));
+        }
+        dst[j * h] = make_double2(re, im);
       }
-      D[e] = make_double2(re, im);
     }
     __syncthreads();
-    // z: Hermitian half spectrum -> p real outputs (irfft: DC imaginary
-    // part dropped, bins 1..q/2 counted twice; q is odd so no Nyquist bin)
-    #pragma unroll 2
-    for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
-      const int gi = e / P3, r = e - gi * P3, ij = r / p, k = r - ij * p;
+    // z: Hermitian half spectrum -> p real outputs (irfft: DC imaginary part
+    // dropped, bins 1..q/2 counted twice; q is odd so no Nyquist bin);
+    // line (gi, i, j)
+    for (int l = threadIdx.x; l < G * p * p; l += blockDim.x) {
+      const int gi = l / (p * p), ij = l - gi * p * p;
       const int64_t cell = (int64_t)morton3(x, y, z0 + gi);
       if (cell < cell_lo || cell >= cell_hi) continue;
       const double2 *d = D + gi * PPH + ij * h;
-      double v = d[0].x;
+      double2 v[h];
 #pragma unroll
-      for (int kz = 1; kz < h; ++kz) {
-        const double2 t = tw[k * q + kz];
-        v = fma(2.0 * d[kz].x, t.x, fma(-2.0 * d[kz].y, t.y, v));
+      for (int kz = 0; kz < h; ++kz) v[kz] = d[kz];
+      double *out = locals + (cell * m + c0 + crel) * (int64_t)P3 + ij * p;
+#pragma unroll
+      for (int k = 0; k < p; ++k) {
+        double t = v[0].x;
+#pragma unroll
+        for (int kz = 1; kz < h; ++kz) {
+          const int r = (k * kz) % q;
+          t = fma(2.0 * v[kz].x, g.c[r], fma(-2.0 * v[kz].y, g.s[r], t));
+        }
+        out[k] = norm * t;
       }
-      locals[(cell * m + c0 + crel) * (int64_t)P3 + r] = norm * v;
     }
   }
 }
@@ -381,6 +413,30 @@ short *tap_table() {
   return dev;
 }
 
+template <int P>
+int launch_fft(bool fwd, const double *moments, const double2 *Y, int level, int64_t cell_lo,
+               int64_t cell_hi, int m, int c0, int ccur, const FftGeom &g, double scale,
+               double2 *X, double *locals, cudaStream_t st) {
+  constexpr int G = fft_cells<P>();
+  using Sh = FftShape<P, G>;
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) {
+    cudaFuncSetAttribute(fft_fwd_kernel<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Sh::smem);
+    cudaFuncSetAttribute(fft_inv_kernel<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Sh::smem_inv);
+  }
+  const int64_t ncell = int64_t(1) << (3 * level);
+  const unsigned grid = (unsigned)std::min<int64_t>(ncell / G * ccur, kNumSMs * 24);
+  if (fwd) {
+    fft_fwd_kernel<P, G><<<grid, 128, Sh::smem, st>>>(moments, level, m, c0, ccur, g, X);
+    return check_launch("fft_fwd_kernel");
+  }
+  fft_inv_kernel<P, G><<<grid, 128, Sh::smem_inv, st>>>(Y, level, cell_lo, cell_hi, m, c0, ccur,
+                                                        g, scale, locals);
+  return check_launch("fft_inv_kernel");
+}
+
 }  // namespace
 }  // namespace bfmm
 
@@ -416,8 +472,6 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const short *taps = tap_table();
   double2 *X = static_cast<double2 *>(scratch);
   double2 *Y = X + ncell * cc * F;
-  const int G = fft_group(g);
-  const size_t smem_f = fft_fwd_smem(g, G), smem_i = fft_inv_smem(g, G);
   const int n = 1 << level;
   const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
   const size_t smem_s = sizeof(double2) * (kHX * kHYP * kHZP + 343);
@@ -426,53 +480,37 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_s);
   }
-  int rc = 0;
-  switch (p) {
-#define BFMM_FFT_ATTR(PP)                                                                      \
-  case PP:                                                                                     \
-    cudaFuncSetAttribute(fft_fwd_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                         (int)smem_f);                                                         \
-    cudaFuncSetAttribute(fft_inv_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                         (int)smem_i);                                                         \
-    break;
-    BFMM_FFT_ATTR(2) BFMM_FFT_ATTR(3) BFMM_FFT_ATTR(4) BFMM_FFT_ATTR(5) BFMM_FFT_ATTR(6)
-    BFMM_FFT_ATTR(7) BFMM_FFT_ATTR(8) BFMM_FFT_ATTR(9) BFMM_FFT_ATTR(10) BFMM_FFT_ATTR(11)
-    BFMM_FFT_ATTR(12)
-#undef BFMM_FFT_ATTR
-  }
-  (void)rc;
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
-    const int64_t groups = ncell / G * ccur;
-    const unsigned gcell = (unsigned)std::min<int64_t>(groups, kNumSMs * 16);
+    int rc = 0;
     switch (p) {
 #define BFMM_FFT_FWD(PP)                                                                       \
   case PP:                                                                                     \
-    fft_fwd_kernel<PP><<<gcell, 128, smem_f, st>>>(moments, level, m, c0, ccur, g, G, X);      \
+    rc = launch_fft<PP>(true, moments, nullptr, level, 0, 0, m, c0, ccur, g, 1.0, X, nullptr,  \
+                        st);                                                                   \
     break;
       BFMM_FFT_FWD(2) BFMM_FFT_FWD(3) BFMM_FFT_FWD(4) BFMM_FFT_FWD(5) BFMM_FFT_FWD(6)
       BFMM_FFT_FWD(7) BFMM_FFT_FWD(8) BFMM_FFT_FWD(9) BFMM_FFT_FWD(10) BFMM_FFT_FWD(11)
       BFMM_FFT_FWD(12)
 #undef BFMM_FFT_FWD
     }
-    if (check_launch("fft_fwd_kernel")) return 1;
+    if (rc) return rc;
     stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
         X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
         8 * (q_lo + nq));
     if (check_launch("stencil_kernel")) return 1;
-    const unsigned gi = (unsigned)std::min<int64_t>(groups, kNumSMs * 16);
     switch (p) {
 #define BFMM_FFT_INV(PP)                                                                       \
   case PP:                                                                                     \
-    fft_inv_kernel<PP><<<gi, 128, smem_i, st>>>(Y, level, 8 * q_lo, 8 * (q_lo + nq), m, c0,     \
-                                                ccur, g, G, scale, locals);                    \
+    rc = launch_fft<PP>(false, nullptr, Y, level, 8 * q_lo, 8 * (q_lo + nq), m, c0, ccur, g,   \
+                        scale, nullptr, locals, st);                                           \
     break;
       BFMM_FFT_INV(2) BFMM_FFT_INV(3) BFMM_FFT_INV(4) BFMM_FFT_INV(5) BFMM_FFT_INV(6)
       BFMM_FFT_INV(7) BFMM_FFT_INV(8) BFMM_FFT_INV(9) BFMM_FFT_INV(10) BFMM_FFT_INV(11)
       BFMM_FFT_INV(12)
 #undef BFMM_FFT_INV
     }
-    if (check_launch("fft_inv_kernel")) return 1;
+    if (rc) return rc;
   }
   return 0;
 }

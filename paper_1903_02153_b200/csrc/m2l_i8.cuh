@@ -399,7 +399,11 @@ __global__ void __maxnreg__(128)
 m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
                const int8_t *__restrict__ cs, const double *__restrict__ cpow,
                double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
-               int nsplit) {
+               int nsplit, int4 box) {
+  // box: the target cells this launch covers, in same-octant (half-
+  // resolution) coordinates: origin (box.x, box.y, box.z), box.w = packed
+  // tile counts (x tiles << 20 | y tiles << 10 | z tiles); a whole level or
+  // a Morton-aligned shard of it (a box, see i8_plane_box)
   using Sh = I8PShape<S, XT>;
   constexpr int NP = Sh::NP, NB = Sh::NB, YT = Sh::YT;
   extern __shared__ __align__(1024) uint8_t smp[];
@@ -412,15 +416,15 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
   uint64_t *done = bempty + NB;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
-  const int n = 1 << level, h = n >> 1;  // cells per axis; same-octant targets per axis
+  const int n = 1 << level;  // cells per axis
   const int o = blockIdx.z & 7, split = blockIdx.z >> 3;
   const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-  const int ybn = h / YT, zbn = h >> 3;
+  const int ybn = (box.w >> 10) & 1023, zbn = box.w & 1023;
   int tile = blockIdx.x;
-  const int zb = tile % zbn;
+  const int zb = tile % zbn + box.z / 8;
   tile /= zbn;
-  const int yb = tile % ybn;
-  const int xb = tile / ybn;
+  const int yb = tile % ybn + box.y / YT;
+  const int xb = tile / ybn + box.x / XT;
   const int col = blockIdx.y / ntn, nt = blockIdx.y - col * ntn;
   const int xs = 2 * xb * XT + ox;  // target x of the tile's first x slot (slots 2 apart)
   const int units = 28 * kc_n;
@@ -706,6 +710,31 @@ struct I8Call {
   cudaStream_t st;
 };
 
+// The plane kernel covers dense levels >= 4 (1 x 16 x 8 tiles from level 5,
+// 2 x 8 x 8 at level 4) over a box of target cells: the whole level, or a
+// Morton shard [8 q_lo, 8 (q_lo + nq)) that is an aligned power-of-two block
+// -- the low b bits of the Morton id vary, i.e. z gets ceil(b/3) of them,
+// y ceil((b-1)/3), x ceil((b-2)/3): always a box (the cells-balanced shards
+// of 2, 4, 8, ... ranks: slabs, columns, octants).  Its same-octant extents
+// must be whole tiles.  Unaligned shards and listed cells use the gather
+// kernel.  BFMM_I8_GATHER (diagnostic) forces the gather kernel.
+inline bool i8_plane_box(const I8Call &a, int XT, int YT, int4 *box) {
+  if (a.act.cells || a.level < 4 || getenv("BFMM_I8_GATHER")) return false;
+  const int64_t c0 = 8 * a.q_lo, len = 8 * a.nq;
+  if (len <= 0 || (len & (len - 1)) || c0 % len) return false;
+  int b = 0;
+  while ((int64_t(1) << b) < len) ++b;
+  const int ez = 1 << ((b + 2) / 3), ey = 1 << ((b + 1) / 3), ex = 1 << (b / 3);
+  int x0, y0, z0;
+  unmorton3((uint64_t)c0, x0, y0, z0);
+  // same-octant (half-resolution) extents and origin
+  const int hx = ex / 2, hy = ey / 2, hz = ez / 2;
+  if (hx < XT || hy < YT || hz < 8 || hx % XT || hy % YT || hz % 8) return false;
+  if (hx / XT > 1023 || hy / YT > 1023 || hz / 8 > 1023) return false;
+  if (box) *box = make_int4(x0 / 2, y0 / 2, z0 / 2, ((hx / XT) << 20) | ((hy / YT) << 10) | (hz / 8));
+  return true;
+}
+
 // coarse dense levels (<= 512 cells): one mixed-octant row set, all 316
 // offsets (see m2l_i8_kernel); BFMM_I8_OCTANT (diagnostic) forces octant mode
 inline bool i8_mixed_ok(const I8Call &a) {
@@ -742,20 +771,17 @@ int launch_i8p(const I8Call &a) {
     cudaFuncSetAttribute(m2l_i8p_kernel<S, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
   }
-  const int h = 1 << (a.level - 1);
-  dim3 grid((unsigned)((h / XT) * (h / Sh::YT) * (h / 8)), (unsigned)(a.ntn * a.m),
-            8 * a.nsplit);
+  int4 box;
+  i8_plane_box(a, XT, Sh::YT, &box);
+  const int tiles = (box.w >> 20) * ((box.w >> 10) & 1023) * (box.w & 1023);
+  dim3 grid((unsigned)tiles, (unsigned)(a.ntn * a.m), 8 * a.nsplit);
   m2l_i8p_kernel<S, XT><<<grid, kI8PThreads, Sh::smem, a.st>>>(
-      a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit);
+      a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, box);
   return check_launch("m2l_i8p_kernel");
 }
 
-// the plane kernel covers whole dense levels >= 4 (1 x 16 x 8 tiles from
-// level 5, 2 x 8 x 8 at level 4); shards and listed cells use the gather
-// kernel.  BFMM_I8_GATHER (diagnostic) forces the gather kernel.
 inline bool i8_plane_ok(const I8Call &a) {
-  return !a.act.cells && a.level >= 4 && a.q_lo == 0 &&
-         a.nq == (int64_t(1) << (3 * a.level - 3)) && !getenv("BFMM_I8_GATHER");
+  return i8_plane_box(a, a.level >= 5 ? 1 : 2, a.level >= 5 ? 16 : 8, nullptr);
 }
 
 template <int XT>

@@ -121,6 +121,7 @@ struct JitKernel {
   CUfunction locate;
   CUfunction sym;
   CUfunction direct;
+  CUfunction block;
 };
 
 std::mutex g_jit_mu;
@@ -179,6 +180,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
   names.push_back("bfmm_nf::locate_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::p2p_sym_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::direct_kernel<bfmm_nf::KUser>");
+  names.push_back("bfmm_nf::pair_block_kernel<bfmm_nf::KUser>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--std=c++17",
                                     "-default-device", "-lineinfo"};
@@ -229,7 +231,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 9; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
@@ -238,7 +240,8 @@ int jit_compile(int kind, const char *expr, int *handle) {
     if (i < 5) jk.p2p[i] = f;
     else if (i == 5) jk.locate = f;
     else if (i == 6) jk.sym = f;
-    else jk.direct = f;
+    else if (i == 7) jk.direct = f;
+    else jk.block = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -810,6 +813,49 @@ extern "C" int bfmm_direct(int handle, const double *tpts, int64_t nt,
     if (check_launch("direct_kernel")) return 1;
   }
   return 0;
+}
+
+// ---- kernel values on pair grids (M2L table build, operators.py:88-108, 244-258)
+extern "C" int bfmm_kernel_block(int handle, const double *xt, int64_t na, const double *ys,
+                                 int64_t nb, const double *shift, int nt, double *out,
+                                 int32_t *bad, bfmm_stream_t stream) {
+  if (na <= 0 || nb <= 0 || nt <= 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  const int64_t total = na * nb * (int64_t)nt;
+  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 32)), block(256);
+  const long long a1 = na, a2 = nb;
+  int *bp = reinterpret_cast<int *>(bad);
+  switch (handle) {
+    case 1: bfmm_nf::pair_block_kernel<KLaplace><<<grid, block, 0, st>>>(xt, a1, ys, a2, shift, nt, out, bp); break;
+    case 2: bfmm_nf::pair_block_kernel<KLaplaceForce><<<grid, block, 0, st>>>(xt, a1, ys, a2, shift, nt, out, bp); break;
+    case 3: bfmm_nf::pair_block_kernel<KGaussian><<<grid, block, 0, st>>>(xt, a1, ys, a2, shift, nt, out, bp); break;
+    case 4: bfmm_nf::pair_block_kernel<KExponential><<<grid, block, 0, st>>>(xt, a1, ys, a2, shift, nt, out, bp); break;
+    case 5: bfmm_nf::pair_block_kernel<KLogarithm><<<grid, block, 0, st>>>(xt, a1, ys, a2, shift, nt, out, bp); break;
+    default: {
+      JitKernel jk;
+      {
+        std::lock_guard<std::mutex> lock(g_jit_mu);
+        if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+          set_error("bfmm_kernel_block: unknown kernel handle %d", handle);
+          return 2;
+        }
+        jk = g_jit[handle - kFirstJit];
+      }
+      const double *x = xt, *y = ys, *s = shift;
+      long long b1 = a1, b2 = a2;
+      int t = nt;
+      double *o = out;
+      void *params[] = {&x, &b1, &y, &b2, &s, &t, &o, &bp};
+      if (driver().LaunchKernel(jk.block, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
+                                nullptr) != CUDA_SUCCESS) {
+        set_error("bfmm_kernel_block: cuLaunchKernel failed");
+        return 1;
+      }
+      add_launches(1);
+      return 0;
+    }
+  }
+  return check_launch("pair_block_kernel");
 }
 
 extern "C" int bfmm_level2_work(const int64_t *tleaves, const int64_t *tcounts,

@@ -24,7 +24,8 @@ from .errors import ConfigurationError, DomainError, KernelEvaluationError, Nati
 from .interp import device_interp_blob, half_interval_matrices
 from .kernel import KernelSpec
 from .plan import FmmPlan, SchemeKind
-from .tables import ChebyshevLevelBlock, M2LTable, neighbor_offsets, precompute_m2l
+from .tables import (ChebyshevLevelBlock, DeviceTableBuilder, M2LTable, neighbor_offsets,
+                     precompute_m2l)
 
 _KIND = {"r": 0, "r2": 1, "diff": 2}
 _ST_DOMAIN_SRC, _ST_DOMAIN_TGT, _ST_REF, _ST_NONFINITE, _ST_WEIGHTS = 0, 1, 2, 3, 4
@@ -110,6 +111,11 @@ class _Tree:
 class FmmEvaluator:
     """A plan bound to its kernel functor and device-resident M2L tables."""
 
+    #: where the M2L operator tables are built: "device" (GPU assembly and
+    #: QR, host SVD; tables.DeviceTableBuilder) or "host" (NumPy, the
+    #: reference's own sequence)
+    table_build = "device"
+
     def __init__(self, kernel: KernelSpec, plan: FmmPlan, cache_dir=None,
                  threads: int = 1, table: M2LTable = None, use_cache: bool = True,
                  device=None):
@@ -146,15 +152,21 @@ class FmmEvaluator:
         self.transfers_factors = self._H
         self.tree_seconds = time.perf_counter() - t0
         t0 = time.perf_counter()
+        self._handle = self._kernel_handle()
+        self._check_device_kernel()
         if table is None:
+            # operator tables built on the GPU with the near field's functor
+            # (tables.DeviceTableBuilder; host fallback per block), or read
+            # from the reference-format cache
+            self.table_builder = (DeviceTableBuilder(kernel, self._handle, self.lib, self.device,
+                                                     self._stream)
+                                  if self.table_build == "device" else None)
             table = precompute_m2l(kernel, plan, cache_dir=cache_dir, threads=self.threads,
-                                   use_cache=use_cache)
+                                   use_cache=use_cache, builder=self.table_builder)
         self.table = table
         self._upload_tables()
         self.table_seconds = time.perf_counter() - t0
         self.precompute_seconds = self.tree_seconds + self.table_seconds
-        self._handle = self._kernel_handle()
-        self._check_device_kernel()
         self.timings = {}
         self._disable_far_field = False
         self.keep_stages = False
@@ -480,7 +492,10 @@ class FmmEvaluator:
             npar = 1 << (3 * (lev - 1))
             qlo, qhi = self._cells(lev - 1, shard)  # parents of this shard's cells
             row = m * p3
-            moments[lev - 1] = torch.empty((npar * row,), dtype=torch.float64, device=self.device)
+            # a shard fills its own cells and receives only its halo: the
+            # rest of the level must read as zeros
+            alloc = torch.zeros if shard is not None else torch.empty
+            moments[lev - 1] = alloc((npar * row,), dtype=torch.float64, device=self.device)
             _native.check(self.lib.bfmm_m2m(
                 moments[lev][8 * qlo * row:].data_ptr(), moments[lev - 1][qlo * row:].data_ptr(),
                 qhi - qlo, p, m, _native.dptr(self._H), st), "bfmm_m2m")
@@ -572,13 +587,15 @@ class FmmEvaluator:
         # 8-aligned at level 2: the few extra children computed are unused)
         q_lo, nq = lo // 8, -(-hi // 8) - lo // 8
         out = torch.empty((ncell * m * p3,), dtype=torch.float64, device=self.device)
+        # shards: z outside the own cells and the received halo reads as zero
+        zalloc = torch.zeros if (shard is not None and not shard[0].full) else torch.empty
         if blk["kind"] == "cheb" and lev in active:
             # only the listed active target cells: compact lt rows
             cells, off, nact = active[lev]
             rp = blk["rp"]
             longest = int(np.max(off[1:] - off[:-1]))
             ns = self._m2l_splits(lev, m, rp, max(longest, 1))
-            z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
+            z = zalloc((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((max(nact, 1) * m * ns * rp,), dtype=torch.float64,
                              device=self.device)
             out.zero_()
@@ -586,7 +603,7 @@ class FmmEvaluator:
                 moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
-                shard[1].allgather_cells(z, m * rp, lev, shard[0])
+                shard[1].exchange_level(z, m * rp, lev, shard[0])
             self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, cells=cells, off=off)
             if nact:
                 _native.check(self.lib.bfmm_rows_gemm_scatter(
@@ -595,20 +612,22 @@ class FmmEvaluator:
         elif blk["kind"] == "cheb":
             rp = blk["rp"]
             ns = self._m2l_splits(lev, m, rp, nq)
-            z = torch.empty((ncell * m * rp,), dtype=torch.float64, device=self.device)
+            z = zalloc((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
             _native.check(self.lib.bfmm_rows_gemm(
                 moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
-                shard[1].allgather_cells(z, m * rp, lev, shard[0])  # sources from every shard
+                # the sources this shard's M2L reads: its halo (fine levels)
+                # or the whole level (coarse levels)
+                shard[1].exchange_level(z, m * rp, lev, shard[0])
             self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq)
             _native.check(self.lib.bfmm_rows_gemm(
                 lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
                 out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
         else:
             if shard is not None and not shard[0].full:
-                shard[1].allgather_cells(moments[lev], m * p3, lev, shard[0])
+                shard[1].exchange_level(moments[lev], m * p3, lev, shard[0])
             # spectra of a chunk of columns at a time (<= 16 GiB of scratch)
             nb = _native.C.c_size_t(0)
             _native.check(self.lib.bfmm_m2l_fft_scratch_bytes(lev, 1, p, _native.C.byref(nb)),
@@ -883,18 +902,41 @@ class FmmEvaluator:
         else:
             main.wait_stream(side)
         phi = torch.empty((n_tgt, m), dtype=torch.float64, device=self.device)
+        if sharded:
+            # every rank holds phi of its own contiguous range of the sorted
+            # targets: all-gather the ranges, then un-permute everywhere
+            near = self._gather_sorted_phi(phi_far, near, ttree, m, _shard)
+            phi_far = None
         _native.check(self.lib.bfmm_scatter_output(
             phi_far.data_ptr() if phi_far is not None else None, near.data_ptr(),
             ttree.perm.data_ptr(), n_tgt, m, phi.data_ptr(), status[_ST_NONFINITE:].data_ptr(), st),
             "bfmm_scatter_output")
         if not pairs_counted:
             count_pairs()
-        if sharded:
-            _shard[1].allreduce_sum(phi)  # every rank wrote only its own targets
         if ev:
             ev[6].record()
         extras = {"moments": moments, "locals": locs, "near": near, "far": phi_far, "ws": ws}
         return phi, status, ttree, stree, extras
+
+    def _gather_sorted_phi(self, phi_far, near, ttree, m, shard):
+        """phi of the sorted targets on every rank: rank r computed the rows
+        of its Morton range, [b_r, b_{r+1}) in sorted order (the trees are
+        identical on every rank, so each derives every boundary itself)."""
+        torch = _torch()
+        shards, comm = shard
+        L, n = self.plan.levels, ttree.n
+        nl = int(ttree.n_leaves.item())
+        if nl == 0:
+            return near
+        cuts = torch.tensor([shards.cells_of(r, L)[0] for r in range(comm.world)],
+                            dtype=torch.int64, device=self.device)
+        idx = torch.searchsorted(ttree.leaves[:nl], cuts)
+        pos = torch.where(idx < nl, ttree.starts[:nl][idx.clamp(max=nl - 1)],
+                          torch.full_like(idx, n))
+        b = pos.cpu().tolist() + [n]
+        lo, hi = b[comm.rank], b[comm.rank + 1]
+        own = near[lo:hi] if phi_far is None else near[lo:hi] + phi_far[lo:hi]
+        return comm.allgather_rows(own.contiguous(), [b[r + 1] - b[r] for r in range(comm.world)])
 
     # -- CUDA graph replay (use_graph) ----------------------------------------
     def _graph_ok(self, sources, targets, weights, sharded, shared):
@@ -928,7 +970,7 @@ class FmmEvaluator:
         copied inside the graph (the weights on a side stream, under the tree
         build, as in the eager path) -- graphs are keyed by the input
         buffers; other host inputs go through static device buffers.  Stage
-        timings are not split in this mode (only total / wall / near_pairs)."""
+        timings come from external event-record nodes inside the graph."""
         torch = _torch()
         t_host0 = time.perf_counter()
         src_t = sources if as_tensor else torch.from_numpy(
@@ -968,7 +1010,12 @@ class FmmEvaluator:
                 stat_in[0].copy_(src_t)
                 stat_in[1].copy_(w_t)
 
+            # stage timestamps inside the graph: external event-record
+            # nodes fire on every replay (reference timings keys, eng:505-533)
+            gev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(7)]
+
             def body():
+                gev[0].record()
                 if kind == "device":
                     xs, ws_, w_ev = src_t, w_t, None
                 elif kind == "static":
@@ -985,7 +1032,7 @@ class FmmEvaluator:
                         w_ev = torch.cuda.Event()
                         w_ev.record()
                     ws_.record_stream(main)
-                return self._device_step(xs, xs, ws_, w_ev, m, n, n, True, False, None, None)
+                return self._device_step(xs, xs, ws_, w_ev, m, n, n, True, False, None, gev)
 
             body()  # eager warm-up: lazy tables, kernel attributes
             torch.cuda.synchronize()
@@ -993,8 +1040,9 @@ class FmmEvaluator:
             l0 = self.lib.bfmm_launch_count()
             with torch.cuda.graph(g):
                 outs = body()
-            ent = self._graphs[key] = (g, stat_in, outs, int(self.lib.bfmm_launch_count() - l0))
-        g, stat_in, outs, nlaunch = ent
+            ent = self._graphs[key] = (g, stat_in, outs, int(self.lib.bfmm_launch_count() - l0),
+                                       gev)
+        g, stat_in, outs, nlaunch, gev = ent
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if stat_in is not None:
@@ -1017,11 +1065,13 @@ class FmmEvaluator:
         self._raise_flags(stat, ttree, stree)
         if not as_tensor:
             result = result.numpy()
-        total = e0.elapsed_time(e1) * 1e-3
-        self.timings = {"upload": 0.0, "distribute": 0.0, "upward": 0.0, "far_field": 0.0,
-                        "downward": 0.0, "near_field": 0.0,
-                        "near_pairs": int(stat.view(np.int64)[4]), "total": total,
-                        "wall": time.perf_counter() - t_host0}
+        ms = [gev[i].elapsed_time(gev[i + 1]) * 1e-3 for i in range(6)]
+        self.timings = {"upload": ms[0], "distribute": ms[1], "upward": ms[2],
+                        "far_field": ms[3], "downward": ms[4], "near_field": ms[5],
+                        "near_pairs": int(stat.view(np.int64)[4])}
+        self.timings["total"] = sum(ms[1:])
+        self.timings["graph_total"] = e0.elapsed_time(e1) * 1e-3
+        self.timings["wall"] = time.perf_counter() - t_host0
         return result[:, 0] if squeeze else result
 
     def _raise_flags(self, stat, ttree, stree):

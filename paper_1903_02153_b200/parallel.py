@@ -4,16 +4,23 @@ One process per GPU.  Every rank holds the full point set and weights and
 builds the same tree (a redundant, cheap sort).  Rank g of G owns the
 contiguous Morton range of cells [g * 8^l / G, (g+1) * 8^l / G) at every
 level l >= 2; because children of q are 8q..8q+7 the ranges nest, so the
-upward and downward passes of a shard never leave it.  The exchanges:
+upward and downward passes of a shard never leave it.  A Morton-aligned
+power-of-two range is a box (slabs at G = 2, columns at 4, octants at 8),
+which lets the plane-buffered int8 M2L kernel run on a shard.  The
+exchanges:
 
-* after each level's upward step, an all-gather of the level's rank-space
-  multipoles z (Chebyshev) or moments (uniform) — M2L reads sources from
-  anywhere within the 6^3 parent neighbourhood;
-* at the end, an all-reduce of phi (each rank wrote its own targets, zeros
-  elsewhere).
+* per far-field level, the rank-space multipoles z (Chebyshev) or the
+  moments (uniform) a shard's M2L reads: its own cells plus the halo of
+  cells within 3 cells of its box (the far offsets have |t|_inf <= 3,
+  octree.py:110-145).  At fine levels the halo is a thin shell (C5 level 8,
+  8 ranks: ~7 % of a shard), sent point to point (halo_exchange); at coarse
+  levels, or when the halo is most of the level, the level is all-gathered;
+* at the end, an all-gather of every rank's contiguous range of the sorted
+  targets' phi, then each rank un-permutes the whole phi.
 
 P2P needs no exchange: sources are replicated.  The collectives run through
-torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests).
+torch.distributed: NCCL over NVLink on the B200 box, or gloo (host-staged
+copies) in the multi-process tests.
 """
 
 from __future__ import annotations
@@ -102,14 +109,125 @@ class MortonShards:
         return self.world == 1
 
 
+# ---------------------------------------------------------------------------
+# halo plans
+
+def _compact3(v):
+    v = v & 0x1249249249249249
+    v = (v | (v >> 2)) & 0x10C30C30C30C30C3
+    v = (v | (v >> 4)) & 0x100F00F00F00F00F
+    v = (v | (v >> 8)) & 0x1F0000FF0000FF
+    v = (v | (v >> 16)) & 0x1F00000000FFFF
+    v = (v | (v >> 32)) & 0x1FFFFF
+    return v
+
+
+def _owner_grid(bounds, level):
+    """owner rank of every cell of a level on the (x, y, z) grid."""
+    n = 1 << level
+    ids = np.arange(8 ** level, dtype=np.int64)
+    scale = 8 ** (level - 2)
+    owner = (np.searchsorted(np.asarray(bounds[1:], dtype=np.int64) * scale, ids, side="right")
+             .astype(np.int16))
+    grid = np.empty((n, n, n), dtype=np.int16)
+    grid[_compact3(ids >> 2), _compact3(ids >> 1), _compact3(ids)] = owner
+    return grid
+
+
+def _dilate3(mask, r=3):
+    """max-norm dilation by r cells (the cube of the far offsets, |t|_inf <= 3)."""
+    out = mask.copy()
+    for ax in range(3):
+        src = out.copy()
+        for s in range(1, r + 1):
+            a = [slice(None)] * 3
+            b = [slice(None)] * 3
+            a[ax], b[ax] = slice(s, None), slice(None, -s)
+            out[tuple(a)] |= src[tuple(b)]
+            out[tuple(b)] |= src[tuple(a)]
+    return out
+
+
+def _morton_of(mask):
+    """sorted Morton ids of the True cells of an (n, n, n) mask."""
+    x, y, z = np.nonzero(mask)
+
+    def spread(v):
+        v = v.astype(np.int64) & 0x1FFFFF
+        v = (v | (v << 32)) & 0x1F00000000FFFF
+        v = (v | (v << 16)) & 0x1F0000FF0000FF
+        v = (v | (v << 8)) & 0x100F00F00F00F00F
+        v = (v | (v << 4)) & 0x10C30C30C30C30C3
+        v = (v | (v << 2)) & 0x1249249249249249
+        return v
+    return np.sort((spread(x) << 2) | (spread(y) << 1) | spread(z))
+
+
+@dataclass
+class HaloPlan:
+    """Cells this rank sends to / receives from each peer at one level."""
+    send: dict
+    recv: dict
+    halo_cells: int
+    own_cells: int
+
+
+_HALO_CACHE = {}
+
+
+def halo_plan(bounds, level, rank, world):
+    """The M2L halo of every shard at a level: shard r needs the cells within
+    3 cells (max norm) of its own, outside it; this rank sends each peer the
+    part of that halo it owns, and receives its own halo from the owners.
+    Deterministic from (bounds, level): every rank derives the same plan."""
+    key = (tuple(bounds), level, rank, world)
+    plan = _HALO_CACHE.get(key)
+    if plan is not None:
+        return plan
+    owner = _owner_grid(bounds, level)
+    mine = owner == rank
+    need_me = _dilate3(mine) & ~mine
+    send, recv = {}, {}
+    for r in range(world):
+        if r == rank:
+            continue
+        theirs = owner == r
+        rc = _morton_of(need_me & theirs)
+        if rc.size:
+            recv[r] = rc
+        sc = _morton_of(_dilate3(theirs) & ~theirs & mine)
+        if sc.size:
+            send[r] = sc
+    plan = HaloPlan(send, recv, int(need_me.sum()), int(mine.sum()))
+    if len(_HALO_CACHE) > 64:
+        _HALO_CACHE.pop(next(iter(_HALO_CACHE)))
+    _HALO_CACHE[key] = plan
+    return plan
+
+
 class ShardComm:
-    """The two exchanges of the sharded matvec over torch.distributed."""
+    """The exchanges of the sharded matvec over torch.distributed."""
+
+    #: halo exchange from this level up (coarser levels are all-gathered:
+    #: the 3-cell halo of a shard covers most of them)
+    HALO_MIN_LEVEL = 5
 
     def __init__(self, dist, group=None):
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        # gloo moves host tensors: device tensors are staged through the host
+        self.host_staged = dist.get_backend(group) == "gloo"
+        self._dev_plans = {}
+
+    def _coll(self, fn, out, inp):
+        if self.host_staged and out.is_cuda:
+            o, i = out.cpu(), inp.cpu()
+            fn(o, i, group=self.group)
+            out.copy_(o)
+        else:
+            fn(out, inp, group=self.group)
 
     def allgather_cells(self, full, row_elems: int, level: int, shards=None):
         """full: flat tensor over every cell of a level, row_elems values per
@@ -119,7 +237,7 @@ class ShardComm:
         if shards is None or shards.equal:
             lo, hi = shard_range(8 ** level, self.world, self.rank)
             mine = full[lo * row_elems:hi * row_elems].clone()
-            self.dist.all_gather_into_tensor(full, mine, group=self.group)
+            self._coll(self.dist.all_gather_into_tensor, full, mine)
             return full
         spans = [shards.cells_of(r, level) for r in range(self.world)]
         longest = max(hi - lo for lo, hi in spans) * row_elems
@@ -127,14 +245,81 @@ class ShardComm:
         mine = full.new_zeros(longest)
         mine[:(hi - lo) * row_elems] = full[lo * row_elems:hi * row_elems]
         buf = full.new_empty(self.world * longest)
-        self.dist.all_gather_into_tensor(buf, mine, group=self.group)
+        self._coll(self.dist.all_gather_into_tensor, buf, mine)
         for r, (a, b) in enumerate(spans):
             if r != self.rank:
                 full[a * row_elems:b * row_elems] = buf[r * longest:r * longest + (b - a) * row_elems]
         return full
 
+    def _plan_tensors(self, shards, level, device):
+        import torch
+        key = (tuple(shards.bounds), level, str(device))
+        t = self._dev_plans.get(key)
+        if t is None:
+            plan = halo_plan(shards.bounds, level, self.rank, self.world)
+            t = (plan,
+                 {r: torch.from_numpy(c).to(device) for r, c in plan.send.items()},
+                 {r: torch.from_numpy(c).to(device) for r, c in plan.recv.items()})
+            self._dev_plans[key] = t
+        return t
+
+    def halo_exchange(self, full, row_elems: int, level: int, shards):
+        """Point-to-point exchange of the halo rows of one level (each rank
+        filled its own range): afterwards this rank holds its own cells and
+        every cell within 3 of them, which is all its M2L reads."""
+        import torch
+        plan, send, recv = self._plan_tensors(shards, level, full.device)
+        rows = full.view(-1, row_elems)
+        ops, landing = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                continue
+            if r in send:
+                buf = rows.index_select(0, send[r])
+                if self.host_staged:
+                    buf = buf.cpu()
+                ops.append(self.dist.P2POp(self.dist.isend, buf, r, group=self.group))
+            if r in recv:
+                buf = torch.empty((recv[r].numel(), row_elems), dtype=full.dtype,
+                                  device="cpu" if self.host_staged else full.device)
+                ops.append(self.dist.P2POp(self.dist.irecv, buf, r, group=self.group))
+                landing.append((recv[r], buf))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        for cells, buf in landing:
+            rows.index_copy_(0, cells, buf.to(full.device, non_blocking=True))
+        return full
+
+    def exchange_level(self, full, row_elems: int, level: int, shards):
+        """The sources a shard's M2L needs at one level: the halo where it is
+        small, else the whole level."""
+        if level >= self.HALO_MIN_LEVEL:
+            plan = halo_plan(shards.bounds, level, self.rank, self.world)
+            if plan.halo_cells * 2 < (8 ** level - plan.own_cells):
+                return self.halo_exchange(full, row_elems, level, shards)
+        return self.allgather_cells(full, row_elems, level, shards)
+
+    def allgather_rows(self, mine, counts):
+        """All-gather of per-rank row blocks of different lengths (counts[r]
+        rows each, known on every rank): padded to the longest, gathered,
+        compacted.  Returns the concatenation in rank order."""
+        import torch
+        longest = max(counts)
+        row = mine.shape[1:]
+        pad = mine.new_zeros((longest,) + tuple(row))
+        pad[:mine.shape[0]] = mine
+        buf = mine.new_empty((self.world * longest,) + tuple(row))
+        self._coll(self.dist.all_gather_into_tensor, buf, pad)
+        return torch.cat([buf[r * longest:r * longest + counts[r]] for r in range(self.world)])
+
     def allreduce_sum(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        if self.host_staged and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
 

@@ -33,6 +33,10 @@ def test_graph_replay_bitwise_equals_eager(name, scale, cache_dir):
         got = ev.evaluate(X, weights=w)
         assert np.array_equal(got, eager)
     assert ev.timings["near_pairs"] > 0
+    # stage timings come from event nodes inside the graph (eng:505-533 keys)
+    for k in ("distribute", "upward", "far_field", "downward"):
+        assert ev.timings[k] > 0.0, k
+    assert ev.timings["total"] > 0.0
     # device tensors in, device tensor out
     dX, dw = torch.from_numpy(X).cuda(), torch.from_numpy(w).cuda()
     got = ev.evaluate(dX, weights=dw)
@@ -69,3 +73,20 @@ def test_graph_multi_column_and_fallbacks(cache_dir):
     bad[7] = 5.0
     with pytest.raises(ValueError):
         ev.evaluate(bad, weights=w)
+
+
+def test_graph_recaptures_when_a_knob_changes(cache_dir):
+    """The graph key holds every knob that changes the captured kernels: a
+    change after a capture re-captures instead of replaying stale kernels."""
+    wl, ev = _ev("C2", 1, cache_dir)
+    X, w = wl["points"], np.ascontiguousarray(wl["weights"])
+    ev.m2l_mode = "dmma"
+    dmma = ev.evaluate(X, weights=w)
+    ev.m2l_mode = "i8"
+    i8 = ev.evaluate(X, weights=w)
+    assert not np.array_equal(dmma, i8)  # the engines differ in the last bits
+    ev.use_graph = True
+    assert np.array_equal(ev.evaluate(X, weights=w), i8)
+    ev.m2l_mode = "dmma"
+    assert np.array_equal(ev.evaluate(X, weights=w), dmma)
+    assert len(ev._graphs) == 2
