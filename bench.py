@@ -501,13 +501,13 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
     levels = {}
     if wl["scheme"] == "chebyshev":
         flops = m2l_flops(ev, wl)
-        S = int(ev.i8_slices)
         for k, v in avg.items():
             if not k.startswith("m2l_l"):
                 continue
             lev = int(k.split("_l")[1])
             blk = ev._dev_block(lev)
             r, rp = ev.table.block_for_level(lev).rank, blk["rp"]
+            S, bits = ev._level_digits(lev, rp, False)
             fp64 = flops[lev] / (v * 1e-3) / 1e12
             rec = {"ms": round(v, 4), "engine": ev._level_engine(lev, m, rp),
                    "rank": r, "fp64_equiv_tflops": fp64,
@@ -517,6 +517,7 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
                 useful = flops[lev] * S * (S + 1) / 2  # digit products of the unpadded rank
                 executed = m2l_i8_ops(lev, rp, m, S)
                 rec.update({"kernel": "plane" if lev >= 4 else "gather",
+                            "digits": f"{S} x {bits}-bit",
                             "useful_int8_tops": useful / (v * 1e-3) / 1e12,
                             "executed_int8_tops": executed / (v * 1e-3) / 1e12,
                             "frac_useful": useful / (v * 1e-3) / 1e12 / peaks["i8_tops"],
@@ -565,7 +566,7 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
         lev = dom.split("_l")[1]
         if rec["engine"] == "i8":
             roof = {"kernel": f"m2l_i8{'p' if rec['kernel'] == 'plane' else ''}_kernel "
-                              f"(M2L level {lev}, int8 tcgen05, {ev.i8_slices} digits/operand)",
+                              f"(M2L level {lev}, int8 tcgen05, {rec['digits']} digits/operand)",
                     "bound": "tensor", "achieved": rec["useful_int8_tops"],
                     "peak": peaks["i8_tops"], "unit": "TFLOP/s",
                     "op_kind": "int8 tensor-core ops (1 MAC = 2), tcgen05 kind::i8",

@@ -89,6 +89,16 @@ int bfmm_group_by_octant(const int64_t *cells, int64_t n, int64_t *out, void *sc
 
 /* ---- upward pass ------------------------------------------------------- */
 
+/* P2M over leaf CELLS for sparse clouds (a few points per leaf): every
+ * cell of the geom's range [cell_lo, cell_hi) gets its moments written,
+ * zeros for empty cells (no memset of the level-L array needed); cell_start
+ * / cell_count are the tree build's dense per-cell maps.  Same moments as
+ * bfmm_p2m (engine.py:159-185).  2 <= p <= 8. */
+int bfmm_p2m_cells(const double *pts4, const double *wsorted, int m,
+                   const int32_t *cell_start, const int32_t *cell_count, int levels, int p,
+                   int scheme, const double *interp, const double *geom, double *moments,
+                   int32_t *ref_flag, bfmm_stream_t stream);
+
 /* P2M leaf_moments (engine.py:159-185).  interp (host) holds the 1-D
  * basis: scheme 0 (Chebyshev) p*p coefficients S[n][j] = c_n T_n(x_j),
  * scheme 1 (uniform) p nodes followed by p*p inverse node differences.
@@ -178,7 +188,13 @@ int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m, int rp,
  *  - cs: core digits, [316][ceil(rp/64)][ceil(rp/32)][S][64 x 32 K-major
  *    core-matrix image] int8; cpow: 2^(e_i) per rank row, ceil(rp/64)*64
  *    doubles (built on the host, engine._i8_core_slices).
- *  - S in 5..8, rp <= 256. */
+ *  - S in 5..8, rp <= 256: S signed 7-bit digits per operand (base 2^7).
+ *    S = 6 | BFMM_I8_BASE256: six signed 8-bit digits (base 2^8, 47 bits,
+ *    21 digit products instead of the 28 of S = 7 at a comparable
+ *    truncation), allowed while 6 K 2^14 < 2^31 for the K = offsets x 32 x
+ *    ceil(rp/32) terms an accumulator sums (rp <= 96; <= 64 for the
+ *    mixed-octant coarse levels). */
+#define BFMM_I8_BASE256 0x100
 size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int S);
 int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int S,
                         int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream);

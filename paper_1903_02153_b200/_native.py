@@ -30,6 +30,7 @@ SIGNATURES = {
     "bfmm_tree_build": (_I, [_P, _I64, _DP, _I, _P, _SZ, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bfmm_gather_weights": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P]),
     "bfmm_p2m": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
+    "bfmm_p2m_cells": (_I, [_P, _P, _I, _P, _P, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_p2m_sparse": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_m2m": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
     "bfmm_rows_gemm": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P]),
@@ -76,6 +77,9 @@ SIGNATURES = {
     "bfmm_level2_work": (_I, [_P, _P, _P, _I64, _P, _I, _P, _P]),
     "bfmm_device_fp64_probe": (_I, [_DP, _P]),
 }
+
+#: bfmm_m2l_i8* S flag: 8-bit digits (include/bfmm.h BFMM_I8_BASE256)
+I8_BASE256 = 0x100
 
 _lib = None
 _lock = threading.Lock()

@@ -305,6 +305,91 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
   }
 }
 
+// P2M for sparse clouds (a few points per leaf, e.g. C5's 3.8), over CELL
+// chunks: a CTA owns kP2MCells consecutive leaf cells of [cell_lo, cell_hi)
+// and writes ALL of their moments -- zeros for empty cells, so the level-L
+// array needs no memset.  The chunk's points (contiguous in sorted order)
+// get their 3 x P weights once, one thread per point, into shared memory;
+// then one thread per output (cell, column, node) sums its cell's points in
+// sorted order (the reduceat order of engine.py:176-182, the products of
+// p2m_leaf_kernel), so consecutive threads write consecutive moments.
+constexpr int kP2MCells = 32, kP2MThreads = 256, kP2MPts = 512;
+
+template <int P>
+__global__ void __launch_bounds__(kP2MThreads, 3)
+p2m_cells_kernel(const double *__restrict__ pts4, const double *__restrict__ ws, int m,
+                 const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_count,
+                 Interp ip, LeafGeom g, double *__restrict__ moments, int32_t *flag) {
+  constexpr int P3 = P * P * P;
+  __shared__ double s_w[kP2MPts][3 * P];
+  __shared__ int s_off[kP2MCells + 1];
+  __shared__ int64_t s_first;
+  __shared__ double sS[P * P], sN[P];
+  stage_basis<P>(ip, sS, sN);
+  const double inv_hw = 1.0 / g.hw;
+  const int64_t ncells = g.cell_hi - g.cell_lo;
+  const int64_t nchunks = (ncells + kP2MCells - 1) / kP2MCells;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = g.cell_lo + ch * kP2MCells;
+    const int nc = (int)(g.cell_hi - c0 < kP2MCells ? g.cell_hi - c0 : kP2MCells);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int cnt = lane < nc ? cell_count[c0 + lane] : 0;
+      int inc = cnt;  // inclusive scan of the counts
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      s_off[lane + 1] = inc;
+      if (lane == 0) s_off[0] = 0;
+      // first point of the chunk: the start of its first occupied cell
+      const unsigned occ = __ballot_sync(0xffffffffu, cnt > 0);
+      if (lane == 0) s_first = occ ? (int64_t)cell_start[c0 + __ffs(occ) - 1] : 0;
+    }
+    __syncthreads();
+    const int npts = s_off[nc];
+    const int64_t first = s_first;
+    const int nout = nc * m * P3;
+    // points in batches of kP2MPts (a crowded chunk takes several)
+    for (int b0 = 0; b0 < max(npts, 1); b0 += kP2MPts) {
+      const int nb = min(kP2MPts, npts - b0);
+      if (b0 > 0) __syncthreads();
+      for (int t = threadIdx.x; t < nb; t += kP2MThreads) {
+        const int64_t i = first + b0 + t;
+        const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+        // the point's cell: the last chunk cell whose offset is <= b0 + t
+        int lo = 0;
+#pragma unroll
+        for (int step = kP2MCells / 2; step > 0; step >>= 1)
+          if (lo + step <= nc && s_off[lo + step] <= b0 + t) lo += step;
+        int cx, cy, cz;
+        unmorton3((uint64_t)(c0 + lo), cx, cy, cz);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, inv_hw, cx, flag),
+                     &s_w[t][0]);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.y, g.lo[1], g.h, inv_hw, cy, flag),
+                     &s_w[t][P]);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag),
+                     &s_w[t][2 * P]);
+      }
+      __syncthreads();
+      for (int o = threadIdx.x; o < nout; o += kP2MThreads) {
+        const int cl = o / (m * P3), rem = o - cl * m * P3, c = rem / P3, a = rem - c * P3;
+        const int ii = a / (P * P), jj = (a / P) % P, kk = a % P;
+        const int p0 = max(s_off[cl], b0), p1 = min(s_off[cl + 1], b0 + nb);
+        double acc = 0.0;
+        for (int pt = p0; pt < p1; ++pt) {
+          const double *wt = s_w[pt - b0];
+          acc += ((wt[ii] * wt[P + jj]) * wt[2 * P + kk]) * ws[(first + pt) * m + c];
+        }
+        double *dst = moments + (c0 * m) * (int64_t)P3 + o;
+        *dst = b0 == 0 ? acc : *dst + acc;
+      }
+    }
+  }
+}
+
 // L2P for sparse leaves (a few points each, e.g. C5's 3.8): one thread per
 // sorted point instead of one warp per leaf, so no lanes idle.  The point's
 // leaf is recomputed from its coordinates (bit-identical to the tree build),
@@ -401,6 +486,28 @@ int launch_leaf(bool p2m, const LeafCall &a) {
       a.pts4, a.m, a.leaves, a.starts, a.counts, a.n_leaves, a.ip, a.g, a.locals, a.out,
       a.flag);
   return check_launch("l2p_warp_kernel");
+}
+
+template <int P>
+int launch_p2m_cells(const LeafCall &a, const int32_t *cell_start, const int32_t *cell_count) {
+  const int64_t chunks = ceil_div(a.g.cell_hi - a.g.cell_lo, kP2MCells);
+  if (chunks <= 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>(chunks, (int64_t)kNumSMs * 8);
+  p2m_cells_kernel<P><<<grid, kP2MThreads, 0, a.st>>>(a.pts4, a.ws, a.m, cell_start, cell_count,
+                                                       a.ip, a.g, a.out, a.flag);
+  return check_launch("p2m_cells_kernel");
+}
+
+inline int dispatch_p2m_cells(int p, const LeafCall &a, const int32_t *cs, const int32_t *cc) {
+  switch (p) {
+    case 2: return launch_p2m_cells<2>(a, cs, cc);
+    case 3: return launch_p2m_cells<3>(a, cs, cc);
+    case 4: return launch_p2m_cells<4>(a, cs, cc);
+    case 5: return launch_p2m_cells<5>(a, cs, cc);
+    case 6: return launch_p2m_cells<6>(a, cs, cc);
+    case 7: return launch_p2m_cells<7>(a, cs, cc);
+    default: return launch_p2m_cells<8>(a, cs, cc);
+  }
 }
 
 inline int dispatch_leaf(int p, bool p2m, const LeafCall &a) {

@@ -520,15 +520,24 @@ extern "C" int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m
 }
 
 // ---- int8 tensor-core M2L (m2l_i8.cuh) ----
-extern "C" size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int S) {
-  return (size_t)rows * ceil_div(rp, 32) * S * 32;
+// S argument: digits per operand, | BFMM_I8_BASE256 for 8-bit digits
+static void i8_digits(int Sarg, int *S, int *B) {
+  *B = (Sarg & BFMM_I8_BASE256) ? 8 : 7;
+  *S = Sarg & 0xff;
 }
 
-extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int S,
+extern "C" size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int Sarg) {
+  return (size_t)rows * ceil_div(rp, 32) * (Sarg & 0xff) * 32;
+}
+
+extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int Sarg,
                                    int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream) {
-  if (rp <= 0 || rp > 256 || S < 5 || S > 8 || rows < 0 || m < 1 || m > 65535 || rows % m) {
-    set_error("bfmm_m2l_i8_slice_z: rp=%d (1..256), S=%d (5..8), rows=%lld", rp, S,
-              (long long)rows);
+  int S, B;
+  i8_digits(Sarg, &S, &B);
+  if (rp <= 0 || rp > 256 || S < 5 || S > 8 || (B == 8 && S != 6) || rows < 0 || m < 1 ||
+      m > 65535 || rows % m) {
+    set_error("bfmm_m2l_i8_slice_z: rp=%d (1..256), S=%d (5..8; 6 for 8-bit digits), rows=%lld",
+              rp, S, (long long)rows);
     return 2;
   }
   cudaStream_t st = as_stream(stream);
@@ -540,11 +549,15 @@ extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp,
   if (check_launch("absmax_bits_kernel")) return 1;
   const int kc_n = (int)ceil_div(rp, 32);
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows * kc_n * 2, 256), 16 * kNumSMs);
-  switch (S) {
-    case 5: z_slice_kernel<5><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
-    case 6: z_slice_kernel<6><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
-    case 7: z_slice_kernel<7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
-    default: z_slice_kernel<8><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+  if (B == 8) {
+    z_slice_kernel<6, 8><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs);
+  } else {
+    switch (S) {
+      case 5: z_slice_kernel<5, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+      case 6: z_slice_kernel<6, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+      case 7: z_slice_kernel<7, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+      default: z_slice_kernel<8, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+    }
   }
   return check_launch("z_slice_kernel");
 }
@@ -570,7 +583,20 @@ extern "C" int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq) {
   return best;
 }
 
-static int i8_check(const char *fn, int level, int m, int rp, int S, int nsplit) {
+static int i8_check(const char *fn, int level, int m, int rp, int S, int B, int nsplit,
+                    bool listed) {
+  if (B == 8) {
+    // 8-bit digits: |digit product| <= 2^14, at most 6 products per
+    // accumulator, K = offsets x 32 x ceil(rp/32) terms each: the exact
+    // int32 accumulation needs 6 K 2^14 < 2^31 (189 offsets per octant; the
+    // mixed-octant rows of dense levels <= 3 walk all 316)
+    const int64_t offs = (level <= 3 && !listed) ? 316 : 189;
+    if (S != 6 || 6 * offs * 32 * ceil_div(rp, 32) * 16384 >= (int64_t(1) << 31)) {
+      set_error("%s: 8-bit digits need S = 6 and 6 K 2^14 < 2^31 (rp=%d, level=%d)", fn, rp,
+                level);
+      return 2;
+    }
+  }
   if (m < 1 || (int64_t(1) << (3 * level)) * m >= (int64_t(1) << 31)) {
     set_error("%s: 8^%d cells x %d columns exceed the 32-bit row index", fn, level, m);
     return 2;
@@ -587,9 +613,11 @@ static int i8_check(const char *fn, int level, int m, int rp, int S, int nsplit)
 }
 
 extern "C" int bfmm_m2l_i8(const int8_t *zs, const unsigned long long *zmax, const int8_t *cs,
-                           const double *cpow, double *lt, int level, int m, int rp, int S,
+                           const double *cpow, double *lt, int level, int m, int rp, int Sarg,
                            int nsplit, int64_t q_lo, int64_t nq, bfmm_stream_t stream) {
-  if (int rc = i8_check("bfmm_m2l_i8", level, m, rp, S, nsplit)) return rc;
+  int S, B;
+  i8_digits(Sarg, &S, &B);
+  if (int rc = i8_check("bfmm_m2l_i8", level, m, rp, S, B, nsplit, false)) return rc;
   const int64_t nparent = int64_t(1) << (3 * level - 3);
   if (q_lo < 0 || nq < 0 || q_lo + nq > nparent) {
     set_error("bfmm_m2l_i8: parent range [%lld, %lld) outside [0, %lld)", (long long)q_lo,
@@ -599,14 +627,16 @@ extern "C" int bfmm_m2l_i8(const int8_t *zs, const unsigned long long *zmax, con
   ensure_offsets();
   I8Call a{zs, zmax, cs, cpow, lt, level, m, rp, (int)ceil_div(rp, 32), (int)ceil_div(rp, kI8TN),
            nsplit, q_lo, nq, OctList{nullptr, {}}, as_stream(stream)};
-  return dispatch_i8(S, a);
+  return dispatch_i8(S, B, a);
 }
 
 extern "C" int bfmm_m2l_i8_cells(const int8_t *zs, const unsigned long long *zmax,
                                  const int8_t *cs, const double *cpow, double *lt, int level,
-                                 int m, int rp, int S, int nsplit, const int64_t *cells,
+                                 int m, int rp, int Sarg, int nsplit, const int64_t *cells,
                                  const int64_t *oct_off, bfmm_stream_t stream) {
-  if (int rc = i8_check("bfmm_m2l_i8_cells", level, m, rp, S, nsplit)) return rc;
+  int S, B;
+  i8_digits(Sarg, &S, &B);
+  if (int rc = i8_check("bfmm_m2l_i8_cells", level, m, rp, S, B, nsplit, true)) return rc;
   OctList act{cells, {}};
   for (int o = 0; o <= 8; ++o) {
     act.off[o] = oct_off[o];
@@ -624,7 +654,7 @@ extern "C" int bfmm_m2l_i8_cells(const int8_t *zs, const unsigned long long *zma
   ensure_offsets();
   I8Call a{zs, zmax, cs, cpow, lt, level, m, rp, (int)ceil_div(rp, 32), (int)ceil_div(rp, kI8TN),
            nsplit, 0, 0, act, as_stream(stream)};
-  return dispatch_i8(S, a);
+  return dispatch_i8(S, B, a);
 }
 
 #ifdef BFMM_I8_TRACE

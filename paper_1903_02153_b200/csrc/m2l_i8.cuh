@@ -85,9 +85,9 @@ __device__ __forceinline__ double i8_zscale(unsigned long long bits) {
 }
 
 // One TMEM lane (tile row) of the S int32 accumulators -> FP64 lt row:
-// x = sum_d 2^(-7d) acc_d (Horner, fixed order), times the z scale and the
+// x = sum_d 2^(-B d) acc_d (Horner, fixed order; B = 7 or 8 digit bits), times the z scale and the
 // rank row's core scale.  zero: no MMA ran (write zeros).
-template <int S, int W>
+template <int S, int W, int B>
 __device__ __forceinline__ void i8_drain(uint32_t tl, double *dst, double zsc, int nt, int rp,
                                          const double *__restrict__ cpow, bool zero) {
 #pragma unroll 1
@@ -108,7 +108,8 @@ __device__ __forceinline__ void i8_drain(uint32_t tl, double *dst, double zsc, i
       for (int u = 0; u < 2; ++u) {
         double x = (double)(int32_t)acc[S - 1][jj + u];
 #pragma unroll
-        for (int d = S - 2; d >= 0; --d) x = fma(x, 0.0078125, (double)(int32_t)acc[d][jj + u]);
+        constexpr double kStep = B == 8 ? 0.00390625 : 0.0078125;  // 2^-B
+        for (int d = S - 2; d >= 0; --d) x = fma(x, kStep, (double)(int32_t)acc[d][jj + u]);
         x2[u] = zero ? 0.0 : x * zsc * cpow[colb + jj + u];
       }
       *reinterpret_cast<double2 *>(dst + colb + jj) = make_double2(x2[0], x2[1]);
@@ -116,7 +117,7 @@ __device__ __forceinline__ void i8_drain(uint32_t tl, double *dst, double zsc, i
   }
 }
 
-template <int S>
+template <int S, int B>
 __global__ void __launch_bounds__(kI8Threads, 1)
 m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
               const int8_t *__restrict__ cs, const double *__restrict__ cpow,
@@ -335,7 +336,7 @@ m2l_i8_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restric
       dst = lt + ((orow * m + c) * nsplit + split) * rp;
       zsc = i8_zscale(zmax[c]);
     }
-    i8_drain<S, 16>(tmem + ((uint32_t)(32 * quarter) << 16), dst, zsc, nt, rp, cpow, false);
+    i8_drain<S, 16, B>(tmem + ((uint32_t)(32 * quarter) << 16), dst, zsc, nt, rp, cpow, false);
   }
   bfmm::tc::fence_before();
   __syncthreads();
@@ -394,7 +395,7 @@ struct I8PShape {
 
 // register cap: leaves room on the SM for near-field (P2P) CTAs running
 // concurrently on another stream
-template <int S, int XT>
+template <int S, int XT, int B>
 __global__ void __maxnreg__(128)
 m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
                const int8_t *__restrict__ cs, const double *__restrict__ cpow,
@@ -610,7 +611,7 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
     const int64_t cell = (int64_t)morton3(xs + 2 * (g % XT), 2 * (YT * yb + g / XT) + oy,
                                           2 * (8 * zb + zl) + oz);
     double *dst = lt + ((cell * m + col) * nsplit + split) * rp;
-    i8_drain<S, 8>(tmem + ((uint32_t)(32 * quarter) << 16), dst, i8_zscale(zmax[col]), nt, rp, cpow,
+    i8_drain<S, 8, B>(tmem + ((uint32_t)(32 * quarter) << 16), dst, i8_zscale(zmax[col]), nt, rp, cpow,
                 !any);
   }
   bfmm::tc::fence_before();
@@ -659,7 +660,7 @@ __global__ void absmax_bits_kernel(const double *__restrict__ z, int64_t rows, i
 // per-column scale is a per-row scale of the GEMM and each right-hand side
 // is cut independently of the others (scalings by powers of two and
 // x - rint(x) are exact in FP64).  k >= rp is zero padding.
-template <int S>
+template <int S, int B>
 __global__ void z_slice_kernel(const double *__restrict__ z, int64_t rows, int rp, int kc_n,
                                int m, const unsigned long long *__restrict__ zmax,
                                int8_t *__restrict__ zs) {
@@ -684,16 +685,40 @@ __global__ void z_slice_kernel(const double *__restrict__ z, int64_t rows, int r
       x[u] = (v == v && fabs(v) <= 1.7976931348623157e308) ? v * inv : 0.0;
     }
     int8_t *dst = zs + ((row * kc_n + kc) * S) * 32 + 16 * h;
+    if constexpr (B == 8) {
+      // base 2^8: X = rint(x 2^(8(S-1))) (|X| <= 2^(8S-10) with |x| <= 64)
+      // as S signed bytes in [-128, 127] (digit j weight 2^(-6-8j) of x /
+      // 2^6, the same leading weight as the 7-bit split); exact integer steps
+      int64_t X[16];
 #pragma unroll
-    for (int j = 0; j < S; ++j) {
-      uint32_t w[4] = {0, 0, 0, 0};
+      for (int u = 0; u < 16; ++u) X[u] = (int64_t)rint(ldexp(x[u], 8 * (S - 1)));
+      uint32_t w[S][4];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const double dg = rint(x[u]);
-        x[u] = (x[u] - dg) * 128.0;
-        w[u >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)dg) << (8 * (u & 3));
+      for (int j = S - 1; j >= 0; --j) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) w[j][q4] = 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int8_t dg = j > 0 ? (int8_t)(X[u] & 0xff) : (int8_t)X[u];
+          X[u] = (X[u] - dg) >> 8;
+          w[j][u >> 2] |= ((uint32_t)(uint8_t)dg) << (8 * (u & 3));
+        }
       }
-      *reinterpret_cast<uint4 *>(dst + j * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        *reinterpret_cast<uint4 *>(dst + j * 32) = make_uint4(w[j][0], w[j][1], w[j][2], w[j][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const double dg = rint(x[u]);
+          x[u] = (x[u] - dg) * 128.0;
+          w[u >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)dg) << (8 * (u & 3));
+        }
+        *reinterpret_cast<uint4 *>(dst + j * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
     }
   }
 }
@@ -741,12 +766,12 @@ inline bool i8_mixed_ok(const I8Call &a) {
   return !a.act.cells && a.level <= 3 && !getenv("BFMM_I8_OCTANT");
 }
 
-template <int S>
+template <int S, int B>
 int launch_i8(const I8Call &a) {
   using Sh = I8Shape<S>;
   static unsigned long long attr_set = 0;
   if (first_on_device(&attr_set)) {
-    cudaFuncSetAttribute(m2l_i8_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(m2l_i8_kernel<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
   }
   const int mixed = i8_mixed_ok(a) ? 1 : 0;
@@ -757,25 +782,25 @@ int launch_i8(const I8Call &a) {
   }
   if (rows <= 0) return 0;
   dim3 grid((unsigned)ceil_div(rows, kI8TM), (unsigned)a.ntn, (mixed ? 1 : 8) * a.nsplit);
-  m2l_i8_kernel<S><<<grid, kI8Threads, Sh::smem, a.st>>>(
+  m2l_i8_kernel<S, B><<<grid, kI8Threads, Sh::smem, a.st>>>(
       a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, a.q_lo,
       a.nq, a.act, mixed);
   return check_launch("m2l_i8_kernel");
 }
 
-template <int S, int XT>
+template <int S, int XT, int B>
 int launch_i8p(const I8Call &a) {
   using Sh = I8PShape<S, XT>;
   static unsigned long long attr_set = 0;
   if (first_on_device(&attr_set)) {
-    cudaFuncSetAttribute(m2l_i8p_kernel<S, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(m2l_i8p_kernel<S, XT, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
   }
   int4 box;
   i8_plane_box(a, XT, Sh::YT, &box);
   const int tiles = (box.w >> 20) * ((box.w >> 10) & 1023) * (box.w & 1023);
   dim3 grid((unsigned)tiles, (unsigned)(a.ntn * a.m), 8 * a.nsplit);
-  m2l_i8p_kernel<S, XT><<<grid, kI8PThreads, Sh::smem, a.st>>>(
+  m2l_i8p_kernel<S, XT, B><<<grid, kI8PThreads, Sh::smem, a.st>>>(
       a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, box);
   return check_launch("m2l_i8p_kernel");
 }
@@ -785,21 +810,24 @@ inline bool i8_plane_ok(const I8Call &a) {
 }
 
 template <int XT>
-int dispatch_i8p(int S, const I8Call &a) {
+int dispatch_i8p(int S, int B, const I8Call &a) {
+  if (B == 8) return launch_i8p<6, XT, 8>(a);
   switch (S) {
-    case 5: return launch_i8p<5, XT>(a);
-    case 6: return launch_i8p<6, XT>(a);
-    case 7: return launch_i8p<7, XT>(a);
-    default: return launch_i8p<8, XT>(a);
+    case 5: return launch_i8p<5, XT, 7>(a);
+    case 6: return launch_i8p<6, XT, 7>(a);
+    case 7: return launch_i8p<7, XT, 7>(a);
+    default: return launch_i8p<8, XT, 7>(a);
   }
 }
 
-inline int dispatch_i8(int S, const I8Call &a) {
-  if (i8_plane_ok(a)) return a.level >= 5 ? dispatch_i8p<1>(S, a) : dispatch_i8p<2>(S, a);
+// S digits of B bits (B = 8 only with S = 6, see i8_base256_ok)
+inline int dispatch_i8(int S, int B, const I8Call &a) {
+  if (i8_plane_ok(a)) return a.level >= 5 ? dispatch_i8p<1>(S, B, a) : dispatch_i8p<2>(S, B, a);
+  if (B == 8) return launch_i8<6, 8>(a);
   switch (S) {
-    case 5: return launch_i8<5>(a);
-    case 6: return launch_i8<6>(a);
-    case 7: return launch_i8<7>(a);
-    default: return launch_i8<8>(a);
+    case 5: return launch_i8<5, 7>(a);
+    case 6: return launch_i8<6, 7>(a);
+    case 7: return launch_i8<7, 7>(a);
+    default: return launch_i8<8, 7>(a);
   }
 }

@@ -69,13 +69,15 @@ def _warm_pinned_dma(device):
         _PIN_WARM = h  # kept alive: the warmed buffer must not be reused
 
 
-def _i8_core_slices(CP: np.ndarray, S: int):
+def _i8_core_slices(CP: np.ndarray, S: int, bits: int = 7):
     """Cores (316, rp, rp) [t][i][k] -> the digit planes bfmm_m2l_i8 reads
     (csrc/m2l_i8.cuh): row i is scaled by 2^-e_i (e_i the exponent of
-    max_{t,k} |C_t[i, k]|) and cut into S signed 7-bit digits,
-    C_t[i, k] = 2^e_i sum_j 2^(-6-7j) D_j[t, i, k] + O(2^(e_i - 7S)), every
-    step exact in FP64.  Returns the int8 image
-    [t][i // 64][k // 32][j][64 x 32 K-major core matrices] and 2^e_i."""
+    max_{t,k} |C_t[i, k]|) and cut into S signed digits of `bits` bits,
+    C_t[i, k] = 2^e_i sum_j 2^(-6-bits*j) D_j[t, i, k] + O(2^(e_i - bits*S)),
+    every step exact (bits = 7: repeated rint in FP64; bits = 8: the integer
+    rint(x 2^(8(S-1))) as S signed bytes, like z_slice_kernel).  Returns the
+    int8 image [t][i // 64][k // 32][j][64 x 32 K-major core matrices] and
+    2^e_i."""
     T, rp, _ = CP.shape
     kc, nt = -(-rp // 32), -(-rp // 64)
     C = np.zeros((T, nt * 64, kc * 32))
@@ -84,10 +86,19 @@ def _i8_core_slices(CP: np.ndarray, S: int):
     e = np.where(amax > 0, np.frexp(amax)[1], 0).astype(np.int64)
     x = C * np.ldexp(1.0, 6 - e)[None, :, None]
     D = np.empty((S,) + C.shape, dtype=np.int8)
-    for j in range(S):
-        d = np.rint(x)
-        D[j] = d
-        x = (x - d) * 128.0
+    if bits == 8:
+        X = np.rint(np.ldexp(x, 8 * (S - 1))).astype(np.int64)
+        for j in range(S - 1, 0, -1):
+            d = (X & 0xFF).astype(np.uint8).view(np.int8)
+            D[j] = d
+            X = (X - d.astype(np.int64)) >> 8
+        assert np.all((X >= -128) & (X <= 127))
+        D[0] = X.astype(np.int8)
+    else:
+        for j in range(S):
+            d = np.rint(x)
+            D[j] = d
+            x = (x - d) * 128.0
     # [j][t][n][k] -> [t][n // 64][k // 32][j][n>>3 & 7][k>>4 & 1][n & 7][k & 15]
     D = D.reshape(S, T, nt, 8, 8, kc, 2, 16).transpose(1, 2, 5, 0, 3, 6, 4, 7)
     return np.ascontiguousarray(D), np.ldexp(1.0, e)
@@ -183,6 +194,9 @@ class FmmEvaluator:
         # ("i8", csrc/m2l_i8.cuh; i8_slices digits of 7 bits per operand)
         self.m2l_mode = "i8"
         self.i8_slices = 7
+        # digit base of the int8 M2L ("auto": 8-bit digits where exact, see
+        # _level_digits; "base128": i8_slices 7-bit digits everywhere)
+        self.i8_digits = "auto"
         # run the near field on a second stream, concurrent with the far
         # field: the P2P is FP64-pipe bound, the int8 M2L tensor-core / L2
         # bound, so they share SMs well (C2, B200: 3.53 -> 3.31 ms).  With the
@@ -200,6 +214,9 @@ class FmmEvaluator:
         # P2M / L2P: warp per leaf ("warp"), thread per (leaf, node) / point
         # ("point"), or "auto" (thread-per-point L2P for sparse clouds)
         self.l2p_mode = "auto"
+        # P2M: warp per leaf ("leaf"), leaf-cell chunks ("cells"), or "auto"
+        # (cells for sparse clouds, see _p2m_cells)
+        self.p2m_mode = "auto"
         # coarse far-field levels on a side stream (see _far_field); the
         # finest main_levels levels stay on the calling stream
         self.stream_levels = True
@@ -285,11 +302,11 @@ class FmmEvaluator:
                 self._dev_blocks[key] = {"kind": "fft",
                                          "symbols": torch.from_numpy(sym.copy()).to(dev)}
 
-    def _i8_tables(self, blk, S):
-        key = ("i8", S)
+    def _i8_tables(self, blk, S, bits):
+        key = ("i8", S, bits)
         if key not in blk:
             torch = _torch()
-            cs, cpow = _i8_core_slices(blk["cores"].cpu().numpy(), S)
+            cs, cpow = _i8_core_slices(blk["cores"].cpu().numpy(), S, bits)
             blk[key] = (torch.from_numpy(cs.reshape(-1)).to(self.device),
                         torch.from_numpy(cpow).to(self.device))
         return blk[key]
@@ -303,30 +320,44 @@ class FmmEvaluator:
             return "i8"
         return "dmma"
 
+    def _level_digits(self, lev, rp, listed):
+        """(digits, bits) of the int8 M2L at a level.  i8_digits = "auto" (with
+        the default i8_slices = 7): six 8-bit digits (47 bits, 21 digit
+        products instead of 28) where the exact int32
+        accumulation bound allows it (rp <= 96; <= 64 for the mixed-octant
+        coarse levels, csrc/m2l_cheb.cu i8_check), else i8_slices 7-bit
+        digits; "base128": always i8_slices 7-bit digits."""
+        if self.i8_digits == "auto" and int(self.i8_slices) == 7:
+            offs = 316 if (lev <= 3 and not listed) else 189
+            if 6 * offs * 32 * (-(-rp // 32)) * 16384 < (1 << 31):
+                return 6, 8
+        return int(self.i8_slices), 7
+
     def _m2l_translate(self, z, lt, lev, m, rp, ns, blk, st, q_lo=0, nq=0, cells=None, off=None):
         """lt = the 189-offset translation of z (engine.py:228-256), on the
         level's engine (_level_engine); cells/off: listed active targets."""
         torch = _torch()
         if self._level_engine(lev, m, rp) == "i8":
-            S = int(self.i8_slices)
-            cs, cpow = self._i8_tables(blk, S)
+            S, bits = self._level_digits(lev, rp, cells is not None)
+            cs, cpow = self._i8_tables(blk, S, bits)
+            Sarg = S | (_native.I8_BASE256 if bits == 8 else 0)
             rows = z.numel() // rp
-            zs = torch.empty(int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, S)), dtype=torch.int8,
+            zs = torch.empty(int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, Sarg)), dtype=torch.int8,
                              device=self.device)
             zmax = torch.empty(m, dtype=torch.int64, device=self.device)
-            _native.check(self.lib.bfmm_m2l_i8_slice_z(z.data_ptr(), rows, m, rp, S,
+            _native.check(self.lib.bfmm_m2l_i8_slice_z(z.data_ptr(), rows, m, rp, Sarg,
                                                        zs.data_ptr(), zmax.data_ptr(), st),
                           "bfmm_m2l_i8_slice_z")
             e0 = self._kevent()
             if cells is not None:
                 _native.check(self.lib.bfmm_m2l_i8_cells(
                     zs.data_ptr(), zmax.data_ptr(), cs.data_ptr(), cpow.data_ptr(),
-                    lt.data_ptr(), lev, m, rp, S, ns, cells.data_ptr(), off.ctypes.data, st),
+                    lt.data_ptr(), lev, m, rp, Sarg, ns, cells.data_ptr(), off.ctypes.data, st),
                     "bfmm_m2l_i8_cells")
             else:
                 _native.check(self.lib.bfmm_m2l_i8(
                     zs.data_ptr(), zmax.data_ptr(), cs.data_ptr(), cpow.data_ptr(),
-                    lt.data_ptr(), lev, m, rp, S, ns, q_lo, nq, st), "bfmm_m2l_i8")
+                    lt.data_ptr(), lev, m, rp, Sarg, ns, q_lo, nq, st), "bfmm_m2l_i8")
             self._kspan(f"m2l_l{lev}", e0)
             return
         e0 = self._kevent()
@@ -474,20 +505,31 @@ class FmmEvaluator:
         torch = _torch()
         L, p = self.plan.levels, self.plan.order
         p3 = p ** 3
-        moments = {L: torch.zeros(((1 << (3 * L)) * m * p3,), dtype=torch.float64, device=self.device)}
         st = self._stream()
         lo, hi = self._cells(L, shard)
         leaf_geom = np.ascontiguousarray(np.concatenate(
             [self.plan.domain.low, [self.plan.domain.length / (1 << L), float(lo), float(hi)]]))
-        # thread-per-(leaf, node) P2M only on request: measured 20 -> 18 ms on
-        # C5 but 5 -> 10 ms on C4, whose crowded leaves serialise one thread
-        p2m = self.lib.bfmm_p2m_sparse if self.l2p_mode == "point" else self.lib.bfmm_p2m
-        _native.check(p2m(
-            tree.pts4.data_ptr(), ws.data_ptr(), m, tree.leaves.data_ptr(),
-            tree.starts.data_ptr(), tree.counts.data_ptr(), tree.n_leaves.data_ptr(),
-            tree.max_leaves, L, p, self._scheme_id, _native.dptr(self._interp),
-            _native.dptr(leaf_geom), moments[L].data_ptr(), status[_ST_REF:].data_ptr(), st),
-            "bfmm_p2m")
+        ncell = (1 << (3 * L))
+        if self._p2m_cells(tree, p):
+            # sparse cloud: P2M over leaf-cell chunks, which writes every
+            # cell of [lo, hi) (zeros for empty ones) -- no memset
+            alloc = torch.zeros if shard is not None else torch.empty
+            moments = {L: alloc((ncell * m * p3,), dtype=torch.float64, device=self.device)}
+            _native.check(self.lib.bfmm_p2m_cells(
+                tree.pts4.data_ptr(), ws.data_ptr(), m, tree.cell_start.data_ptr(),
+                tree.cell_count.data_ptr(), L, p, self._scheme_id, _native.dptr(self._interp),
+                _native.dptr(leaf_geom), moments[L].data_ptr(), status[_ST_REF:].data_ptr(), st),
+                "bfmm_p2m_cells")
+        else:
+            moments = {L: torch.zeros((ncell * m * p3,), dtype=torch.float64, device=self.device)}
+            # thread-per-(leaf, node) P2M only on request (l2p_mode "point")
+            p2m = self.lib.bfmm_p2m_sparse if self.l2p_mode == "point" else self.lib.bfmm_p2m
+            _native.check(p2m(
+                tree.pts4.data_ptr(), ws.data_ptr(), m, tree.leaves.data_ptr(),
+                tree.starts.data_ptr(), tree.counts.data_ptr(), tree.n_leaves.data_ptr(),
+                tree.max_leaves, L, p, self._scheme_id, _native.dptr(self._interp),
+                _native.dptr(leaf_geom), moments[L].data_ptr(), status[_ST_REF:].data_ptr(), st),
+                "bfmm_p2m")
         for lev in range(L, 2, -1):
             npar = 1 << (3 * (lev - 1))
             qlo, qhi = self._cells(lev - 1, shard)  # parents of this shard's cells
@@ -500,6 +542,14 @@ class FmmEvaluator:
                 moments[lev][8 * qlo * row:].data_ptr(), moments[lev - 1][qlo * row:].data_ptr(),
                 qhi - qlo, p, m, _native.dptr(self._H), st), "bfmm_m2m")
         return moments, leaf_geom
+
+    def _p2m_cells(self, tree, p):
+        """P2M over leaf-cell chunks (bfmm_p2m_cells) for sparse clouds --
+        fewer than 8 points per leaf cell on average, like the l2p "auto"
+        rule -- or on request (p2m_mode "cells")."""
+        if not 2 <= p <= 8 or self.p2m_mode == "leaf":
+            return False
+        return self.p2m_mode == "cells" or tree.n < 8 * (1 << (3 * self.plan.levels))
 
     def _active_cells(self, ttree, shard):
         """{level: (active target cells grouped by octant, host octant offsets
@@ -954,7 +1004,8 @@ class FmmEvaluator:
         # the sparse-cloud active lists read counts back on the host
         return self.far_mode == "dense" or (self.far_mode == "auto" and n >= 8 * (1 << (3 * L)))
 
-    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "far_mode", "near_mode", "overlap_near",
+    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "i8_digits", "p2m_mode", "far_mode", "near_mode",
+                    "overlap_near",
                     "near_after_far", "far_priority", "l2p_mode", "stream_levels",
                     "main_levels")
 

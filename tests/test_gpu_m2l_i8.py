@@ -3,7 +3,8 @@ FP64 tensor-core M2L (m2l_mode "dmma") and the reference fixtures.
 
 The i8 path is exact integer arithmetic on digit planes, so its error
 against FP64 is the digit truncation: about 2^(-7S) of the operand scales
-(S digits of 7 bits), and it is bitwise repeatable.
+(S digits of 7 bits) or 2^(-8S+1) (six 8-bit digits, BFMM_I8_BASE256), and
+it is bitwise repeatable.
 """
 
 import numpy as np
@@ -25,7 +26,7 @@ from paper_1903_02153_b200.kernel import workload_kernel  # noqa: E402
 PHI_TOL = 1e-10
 
 
-def _run_both(level, rp, m, S, ns, seed=0, gather=False):
+def _run_both(level, rp, m, S, ns, seed=0, gather=False, bits=7):
     lib = _native.load()
     st = _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
     g = np.random.default_rng(seed)
@@ -38,12 +39,13 @@ def _run_both(level, rp, m, S, ns, seed=0, gather=False):
     ref = torch.zeros(ncell * m * rp, dtype=torch.float64, device="cuda")
     _native.check(lib.bfmm_m2l_cheb(dz.data_ptr(), ref.data_ptr(), level, m, rp, 1, 0, nq,
                                     dc.data_ptr(), st), "cheb")
-    cs, cpow = _i8_core_slices(cores, S)
+    cs, cpow = _i8_core_slices(cores, S, bits)
+    Sarg = S | (_native.I8_BASE256 if bits == 8 else 0)
     dcs, dcp = torch.from_numpy(cs.reshape(-1)).cuda(), torch.from_numpy(cpow).cuda()
     rows = ncell * m
-    zs = torch.empty(int(lib.bfmm_m2l_i8_zs_bytes(rows, rp, S)), dtype=torch.int8, device="cuda")
+    zs = torch.empty(int(lib.bfmm_m2l_i8_zs_bytes(rows, rp, Sarg)), dtype=torch.int8, device="cuda")
     zmax = torch.empty(m, dtype=torch.int64, device="cuda")
-    _native.check(lib.bfmm_m2l_i8_slice_z(dz.data_ptr(), rows, m, rp, S, zs.data_ptr(),
+    _native.check(lib.bfmm_m2l_i8_slice_z(dz.data_ptr(), rows, m, rp, Sarg, zs.data_ptr(),
                                           zmax.data_ptr(), st), "slice")
     outs = []
     if gather:  # diagnostic switch: force the gather kernel on a dense level
@@ -52,7 +54,7 @@ def _run_both(level, rp, m, S, ns, seed=0, gather=False):
     for _ in range(2):
         lt = torch.full((rows * ns * rp,), float("nan"), dtype=torch.float64, device="cuda")
         _native.check(lib.bfmm_m2l_i8(zs.data_ptr(), zmax.data_ptr(), dcs.data_ptr(),
-                                      dcp.data_ptr(), lt.data_ptr(), level, m, rp, S, ns, 0, nq,
+                                      dcp.data_ptr(), lt.data_ptr(), level, m, rp, Sarg, ns, 0, nq,
                                       st), "i8")
         outs.append(lt)
     torch.cuda.synchronize()
@@ -81,6 +83,31 @@ def test_i8_translation_matches_dmma(level, rp, m, S, ns):
         assert err < max(2.0 ** (8 - 7 * S), 1e-14), (c, err)
 
 
+@pytest.mark.parametrize("level,rp,m,ns", [(3, 56, 1, 1), (3, 64, 2, 2), (5, 64, 1, 1),
+                                          (4, 48, 3, 2), (6, 24, 1, 1), (5, 96, 1, 3)])
+def test_i8_base256_digits_match_dmma(level, rp, m, ns):
+    """Six signed 8-bit digits (21 digit products; csrc/m2l_i8.cuh
+    z_slice_kernel<6, 8>, engine._i8_core_slices(bits=8)) where the int32
+    accumulation bound allows it."""
+    got, ref, _ = _run_both(level, rp, m, 6, ns, bits=8)
+    assert np.all(np.isfinite(got))
+    for c in range(m):
+        err = rel_l2(got[c::m], ref[c::m])
+        assert err < max(2.0 ** (10 - 8 * 6), 1e-14), (c, err)
+    if level >= 4:  # plane kernel == gather kernel, bitwise
+        _, _, a = _run_both(level, rp, m, 6, 1, bits=8)
+        _, _, b = _run_both(level, rp, m, 6, 1, gather=True, bits=8)
+        assert torch.equal(a, b)
+
+
+def test_i8_base256_rejects_plans_past_the_int32_bound():
+    lib = _native.load()
+    st = _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = lib.bfmm_m2l_i8(None, None, None, None, None, 4, 1, 128, 6 | _native.I8_BASE256, 1, 0,
+                         8 ** 3, st)
+    assert rc == 2 and b"8-bit digits" in lib.bfmm_last_error()
+
+
 def test_i8_split_blocks_past_the_last_offset_are_zero():
     # 189 offsets over 100 splits of 2: splits 95..99 have no offsets
     got, ref, _ = _run_both(2, 56, 1, 7, 100)
@@ -102,7 +129,7 @@ def test_i8_plane_and_gather_kernels_agree_bitwise(level, rp, m, S):
 
 
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2)])
-@pytest.mark.parametrize("mode,S", [("dmma", 7), ("i8", 6), ("i8", 8)])
+@pytest.mark.parametrize("mode,S", [("dmma", 7), ("i8", 6), ("i8", 7), ("i8", 8)])
 def test_m2l_engines_match_reference(name, scale, mode, S, cache_dir):
     """Both M2L engines (and other digit counts than the default) meet the
     phi bar against the reference fixtures."""
@@ -112,6 +139,8 @@ def test_m2l_engines_match_reference(name, scale, mode, S, cache_dir):
                       domain_center=wl["center"], domain_length=wl["length"], n_cols=wl["ncols"])
     ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir=cache_dir)
     ev.m2l_mode, ev.i8_slices = mode, S
+    if S == 7:
+        ev.i8_digits = "base128"  # the 7-bit split itself (auto would use 8-bit digits)
     phi = ev.evaluate(wl["points"], weights=wl["weights"])
     idx = wl["check_idx"]
     assert rel_l2(phi[idx], g["phi_idx"]) < PHI_TOL

@@ -455,3 +455,24 @@ def test_l2p_point_and_warp_kernels_agree_bitwise(scheme, cache_dir):
     ev.l2p_mode = "point"
     b = ev.evaluate(pts, weights=w)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,scale", [("C5", 2), ("C4", 2)])
+def test_p2m_cell_chunks_equal_warp_per_leaf(name, scale, cache_dir):
+    """The sparse-cloud P2M over leaf-cell chunks (bfmm_p2m_cells, zeros for
+    empty cells, no memset) gives the warp-per-leaf kernel's moments: the
+    same products in the same order (bitwise where a chunk's points fit one
+    batch, C5; crowded C4 chunks split the sums)."""
+    wl = workloads.make(name, scale)
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
+    ev.keep_stages = True
+    out = {}
+    for mode in ("leaf", "cells"):
+        ev.p2m_mode = mode
+        phi = ev.evaluate(wl["points"], weights=wl["weights"])
+        out[mode] = (phi, ev.stages["moments"][wl["levels"]].cpu().numpy())
+    if name == "C5":
+        assert np.array_equal(out["leaf"][1], out["cells"][1])
+    else:
+        assert rel_l2(out["cells"][1], out["leaf"][1]) < 1e-14
+    assert rel_l2(out["cells"][0], out["leaf"][0]) < 1e-13
