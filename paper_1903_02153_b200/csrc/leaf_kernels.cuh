@@ -313,14 +313,19 @@ l2p_warp_kernel(const double *__restrict__ pts4, int m,
 // then one thread per output (cell, column, node) sums its cell's points in
 // sorted order (the reduceat order of engine.py:176-182, the products of
 // p2m_leaf_kernel), so consecutive threads write consecutive moments.
-constexpr int kP2MCells = 32, kP2MThreads = 256, kP2MPts = 512;
+constexpr int kP2MCells = 32, kP2MThreads = 256;
+// points per batch: the 3 x P weights in <= 40 KB of static shared memory
+template <int P>
+constexpr int p2m_pts() {
+  return (40 * 1024 / (24 * P)) / 32 * 32 > 512 ? 512 : (40 * 1024 / (24 * P)) / 32 * 32;
+}
 
 template <int P>
 __global__ void __launch_bounds__(kP2MThreads, 3)
 p2m_cells_kernel(const double *__restrict__ pts4, const double *__restrict__ ws, int m,
                  const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_count,
                  Interp ip, LeafGeom g, double *__restrict__ moments, int32_t *flag) {
-  constexpr int P3 = P * P * P;
+  constexpr int P3 = P * P * P, kP2MPts = p2m_pts<P>();
   __shared__ double s_w[kP2MPts][3 * P];
   __shared__ int s_off[kP2MCells + 1];
   __shared__ int64_t s_first;
