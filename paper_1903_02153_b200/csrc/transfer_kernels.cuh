@@ -119,6 +119,159 @@ l2l_stage_kernel(const double *__restrict__ parent, double *__restrict__ child,
   }
 }
 
+// Warp per (parent, column) for large levels (C5: 2.1M parents at level 7).
+// Each of the three Kronecker stages gives every lane whole 1-D lines
+// (P inputs from each of the two halves -> P outputs) with the transfer
+// factors H[s][a][b] read at compile-time indices from the kernel
+// parameter bank (no shared-memory operand loads, unrolled on P); the
+// intermediates sit in the warp's own shared slice (__syncwarp only), so
+// ~20-30 parents per SM are in flight instead of one per 128-thread CTA.
+// Same sums in the same order as m2m_stage_kernel / l2l_stage_kernel.
+template <int P>
+constexpr int xfer_warps() { return P <= 5 ? 8 : P == 6 ? 4 : 1; }
+
+template <int P>
+__global__ void __launch_bounds__(32 * xfer_warps<P>(), P <= 5 ? 4 : 2)
+m2m_warp_kernel(const double *__restrict__ child, double *__restrict__ parent,
+                int64_t n_parent, int m, Halves hv) {
+  constexpr int P2 = P * P, P3 = P2 * P, W = xfer_warps<P>();
+  __shared__ double s_t1[W][4 * P3];  // z done: [oxy][i][j][k']
+  __shared__ double s_t2[W][2 * P3];  // y done: [ox][i][j'][k']
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *t1 = s_t1[wid], *t2 = s_t2[wid];
+  for (int64_t w = int64_t(blockIdx.x) * W + wid; w < n_parent * m; w += int64_t(gridDim.x) * W) {
+    const int64_t q = w / m;
+    const int c = (int)(w - q * m);
+    // z, summing oz: line (oxy, i, j)
+    for (int l = lane; l < 4 * P2; l += 32) {
+      const int oxy = l / P2, ij = l - oxy * P2;
+      double v[2][P];
+#pragma unroll
+      for (int oz = 0; oz < 2; ++oz) {
+        const double *src = child + ((8 * q + 2 * oxy + oz) * m + c) * (int64_t)P3 + ij * P;
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[oz][k] = src[k];
+      }
+#pragma unroll
+      for (int kp = 0; kp < P; ++kp) {
+        double s = 0.0;
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+          for (int k = 0; k < P; ++k) s = fma(hv.H[oz][kp * P + k], v[oz][k], s);
+        t1[l * P + kp] = s;
+      }
+    }
+    __syncwarp();
+    // y, summing oy: line (ox, i, k')
+    for (int l = lane; l < 2 * P2; l += 32) {
+      const int ox = l / P2, r = l - ox * P2, i = r / P, kp = r - i * P;
+      double v[2][P];
+#pragma unroll
+      for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+        for (int j = 0; j < P; ++j) v[oy][j] = t1[(2 * ox + oy) * P3 + i * P2 + j * P + kp];
+#pragma unroll
+      for (int jp = 0; jp < P; ++jp) {
+        double s = 0.0;
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+          for (int j = 0; j < P; ++j) s = fma(hv.H[oy][jp * P + j], v[oy][j], s);
+        t2[ox * P3 + i * P2 + jp * P + kp] = s;
+      }
+    }
+    __syncwarp();
+    // x, summing ox: line (j', k')
+    double *dst = parent + (q * m + c) * (int64_t)P3;
+    for (int l = lane; l < P2; l += 32) {
+      double v[2][P];
+#pragma unroll
+      for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+        for (int i = 0; i < P; ++i) v[ox][i] = t2[ox * P3 + i * P2 + l];
+#pragma unroll
+      for (int ip = 0; ip < P; ++ip) {
+        double s = 0.0;
+#pragma unroll
+        for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+          for (int i = 0; i < P; ++i) s = fma(hv.H[ox][ip * P + i], v[ox][i], s);
+        dst[ip * P2 + l] = s;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * xfer_warps<P>(), P <= 5 ? 4 : 2)
+l2l_warp_kernel(const double *__restrict__ parent, double *__restrict__ child,
+                int64_t n_parent, int m, Halves hv) {
+  constexpr int P2 = P * P, P3 = P2 * P, W = xfer_warps<P>();
+  __shared__ double s_u[W][2 * P3];  // x done: [ox][i'][j][k]
+  __shared__ double s_t[W][4 * P3];  // y done: [ox oy][i'][j'][k]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *u = s_u[wid], *t = s_t[wid];
+  for (int64_t w = int64_t(blockIdx.x) * W + wid; w < n_parent * m; w += int64_t(gridDim.x) * W) {
+    const int64_t q = w / m;
+    const int c = (int)(w - q * m);
+    const double *src0 = parent + (q * m + c) * (int64_t)P3;
+    // x, per ox: line (j, k)
+    for (int l = lane; l < P2; l += 32) {
+      double v[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) v[i] = src0[i * P2 + l];
+#pragma unroll
+      for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+        for (int ip = 0; ip < P; ++ip) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < P; ++i) s = fma(hv.H[ox][i * P + ip], v[i], s);
+          u[ox * P3 + ip * P2 + l] = s;
+        }
+    }
+    __syncwarp();
+    // y, per (ox, oy): line (ox, i', k)
+    for (int l = lane; l < 2 * P2; l += 32) {
+      const int ox = l / P2, r = l - ox * P2, ip = r / P, k = r - ip * P;
+      double v[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) v[j] = u[ox * P3 + ip * P2 + j * P + k];
+#pragma unroll
+      for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+        for (int jp = 0; jp < P; ++jp) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < P; ++j) s = fma(hv.H[oy][j * P + jp], v[j], s);
+          t[(2 * ox + oy) * P3 + ip * P2 + jp * P + k] = s;
+        }
+    }
+    __syncwarp();
+    // z, per child: line (oxy, i', j') -> the two oz children
+    for (int l = lane; l < 4 * P2; l += 32) {
+      const int oxy = l / P2, ijp = l - oxy * P2;
+      double v[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) v[k] = t[oxy * P3 + ijp * P + k];
+#pragma unroll
+      for (int oz = 0; oz < 2; ++oz) {
+        double *dst = child + ((8 * q + 2 * oxy + oz) * m + c) * (int64_t)P3 + ijp * P;
+#pragma unroll
+        for (int kp = 0; kp < P; ++kp) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < P; ++k) s = fma(hv.H[oz][k * P + kp], v[k], s);
+          dst[kp] += s;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int P>
 int launch_xfer(bool up, const double *src, double *dst, int64_t n_parent, int m,
                 const Halves &hv, cudaStream_t st) {
@@ -129,6 +282,19 @@ int launch_xfer(bool up, const double *src, double *dst, int64_t n_parent, int m
                          (int)smem);
     cudaFuncSetAttribute(l2l_stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+  }
+  if constexpr (P <= 6) {
+    if (n_parent * m >= 4096) {  // large levels: warp per (parent, column)
+      constexpr int W = xfer_warps<P>();
+      const unsigned gw =
+          (unsigned)std::min<int64_t>(ceil_div(n_parent * m, W), (int64_t)kNumSMs * 64);
+      if (up) {
+        m2m_warp_kernel<P><<<gw, 32 * W, 0, st>>>(src, dst, n_parent, m, hv);
+        return check_launch("m2m_warp_kernel");
+      }
+      l2l_warp_kernel<P><<<gw, 32 * W, 0, st>>>(src, dst, n_parent, m, hv);
+      return check_launch("l2l_warp_kernel");
+    }
   }
   const unsigned grid = (unsigned)std::min<int64_t>(n_parent * m, (int64_t)kNumSMs * 16);
   if (up) {
