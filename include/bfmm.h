@@ -99,6 +99,15 @@ int bfmm_p2m_cells(const double *pts4, const double *wsorted, int m,
                    int scheme, const double *interp, const double *geom, double *moments,
                    int32_t *ref_flag, bfmm_stream_t stream);
 
+/* L2P over leaf CELLS for sparse clouds: the locals of a chunk of
+ * consecutive cells of the geom's range are staged in shared memory, one
+ * thread per point of the chunk.  Same phi as bfmm_l2p / bfmm_l2p_points
+ * (engine.py:313-337; bitwise equal to bfmm_l2p_points).  2 <= p <= 8. */
+int bfmm_l2p_cells(const double *pts4, int m, const int32_t *cell_start,
+                   const int32_t *cell_count, int levels, int p, int scheme,
+                   const double *interp, const double *geom, const double *locals,
+                   double *phi_sorted, int32_t *ref_flag, bfmm_stream_t stream);
+
 /* P2M leaf_moments (engine.py:159-185).  interp (host) holds the 1-D
  * basis: scheme 0 (Chebyshev) p*p coefficients S[n][j] = c_n T_n(x_j),
  * scheme 1 (uniform) p nodes followed by p*p inverse node differences.

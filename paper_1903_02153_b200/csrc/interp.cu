@@ -473,6 +473,25 @@ extern "C" int bfmm_p2m_cells(const double *pts4, const double *wsorted, int m,
   return dispatch_p2m_cells(p, a, cell_start, cell_count);
 }
 
+extern "C" int bfmm_l2p_cells(const double *pts4, int m, const int32_t *cell_start,
+                              const int32_t *cell_count, int levels, int p, int scheme,
+                              const double *interp, const double *geom, const double *locals,
+                              double *phi_sorted, int32_t *ref_flag, bfmm_stream_t stream) {
+  if (p < 2 || p > 8 || m < 1 || levels < 2) {
+    set_error("bfmm_l2p_cells: unsupported p=%d m=%d levels=%d", p, m, levels);
+    return 2;
+  }
+  const LeafGeom g = make_leaf_geom(geom);
+  if (g.cell_lo < 0 || g.cell_hi > (int64_t(1) << (3 * levels)) || g.cell_lo > g.cell_hi) {
+    set_error("bfmm_l2p_cells: cell range [%lld, %lld) outside level %d", (long long)g.cell_lo,
+              (long long)g.cell_hi, levels);
+    return 2;
+  }
+  LeafCall a{pts4, nullptr, m, nullptr, nullptr, nullptr, nullptr, 0, levels, true,
+             make_interp(p, scheme, interp), g, locals, phi_sorted, ref_flag, as_stream(stream)};
+  return dispatch_l2p_cells(p, a, cell_start, cell_count);
+}
+
 extern "C" int bfmm_p2m_sparse(const double *pts4, const double *wsorted, int m,
                                const int64_t *leaves, const int64_t *starts,
                                const int64_t *counts, const int64_t *n_leaves,

@@ -493,6 +493,120 @@ int launch_leaf(bool p2m, const LeafCall &a) {
   return check_launch("l2p_warp_kernel");
 }
 
+// L2P for sparse clouds over leaf-CELL chunks: a CTA stages the locals of
+// cc consecutive cells in shared memory with coalesced loads, then one
+// thread per point of the chunk (contiguous in sorted order) contracts them
+// with the same arithmetic as l2p_point_kernel (bitwise equal).
+template <int P>
+__global__ void __launch_bounds__(kP2MThreads, 2)
+l2p_cells_kernel(const double *__restrict__ pts4, int m, int cc,
+                 const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_count,
+                 Interp ip, LeafGeom g, const double *__restrict__ locals,
+                 double *__restrict__ phi, int32_t *flag) {
+  constexpr int P3 = P * P * P;
+  extern __shared__ double sLoc[];  // [cc][m][P^3]
+  __shared__ int s_off[kP2MCells + 1];
+  __shared__ int64_t s_first;
+  __shared__ double sS[P * P], sN[P];
+  stage_basis<P>(ip, sS, sN);
+  const double inv_hw = 1.0 / g.hw;
+  const int64_t ncells = g.cell_hi - g.cell_lo;
+  const int64_t nchunks = (ncells + cc - 1) / cc;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = g.cell_lo + ch * cc;
+    const int nc = (int)(g.cell_hi - c0 < cc ? g.cell_hi - c0 : cc);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int cnt = lane < nc ? cell_count[c0 + lane] : 0;
+      int inc = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      s_off[lane + 1] = inc;
+      if (lane == 0) s_off[0] = 0;
+      const unsigned occ = __ballot_sync(0xffffffffu, cnt > 0);
+      if (lane == 0) s_first = occ ? (int64_t)cell_start[c0 + __ffs(occ) - 1] : 0;
+    }
+    const double *src = locals + c0 * (int64_t)m * P3;
+    for (int e = threadIdx.x; e < nc * m * P3; e += kP2MThreads) sLoc[e] = src[e];
+    __syncthreads();
+    const int npts = s_off[nc];
+    const int64_t first = s_first;
+    for (int t = threadIdx.x; t < npts; t += kP2MThreads) {
+      int lo = 0;
+#pragma unroll
+      for (int step = kP2MCells / 2; step > 0; step >>= 1)
+        if (lo + step <= nc && s_off[lo + step] <= t) lo += step;
+      int cx, cy, cz;
+      unmorton3((uint64_t)(c0 + lo), cx, cy, cz);
+      const int64_t i = first + t;
+      const double4 q = reinterpret_cast<const double4 *>(pts4)[i];
+      double wx[P], wy[P], wz[P];
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.x, g.lo[0], g.h, inv_hw, cx, flag), wx);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.y, g.lo[1], g.h, inv_hw, cy, flag), wy);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(q.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
+      for (int c = 0; c < m; ++c) {
+        const double *L = sLoc + (lo * m + c) * P3;
+        double sa[P];
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+          sa[a] = 0.0;
+#pragma unroll
+          for (int b = 0; b < P; ++b) {
+            const double *Lab = L + (a * P + b) * P;
+            double sb = 0.0;
+#pragma unroll
+            for (int k = 0; k < P; ++k) sb = fma(wz[k], Lab[k], sb);
+            sa[a] = fma(wx[a] * wy[b], sb, sa[a]);
+          }
+        }
+        double s = sa[0];
+#pragma unroll
+        for (int a = 1; a < P; ++a) s += sa[a];
+        phi[i * m + c] = s;
+      }
+    }
+  }
+}
+
+template <int P>
+int launch_l2p_cells(const LeafCall &a, const int32_t *cell_start, const int32_t *cell_count) {
+  constexpr int P3 = P * P * P;
+  int cc = kP2MCells;
+  while (cc > 1 && (size_t)cc * a.m * P3 * sizeof(double) > 96 * 1024) cc >>= 1;
+  const size_t smem = (size_t)cc * a.m * P3 * sizeof(double);
+  if (smem > 96 * 1024) {
+    set_error("bfmm_l2p_cells: m * p^3 = %d too large", a.m * P3);
+    return 2;
+  }
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr))
+    cudaFuncSetAttribute(l2p_cells_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         96 * 1024);
+  const int64_t chunks = ceil_div(a.g.cell_hi - a.g.cell_lo, cc);
+  if (chunks <= 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>(chunks, (int64_t)kNumSMs * 8);
+  l2p_cells_kernel<P><<<grid, kP2MThreads, smem, a.st>>>(a.pts4, a.m, cc, cell_start,
+                                                         cell_count, a.ip, a.g, a.locals, a.out,
+                                                         a.flag);
+  return check_launch("l2p_cells_kernel");
+}
+
+inline int dispatch_l2p_cells(int p, const LeafCall &a, const int32_t *cs, const int32_t *cc) {
+  switch (p) {
+    case 2: return launch_l2p_cells<2>(a, cs, cc);
+    case 3: return launch_l2p_cells<3>(a, cs, cc);
+    case 4: return launch_l2p_cells<4>(a, cs, cc);
+    case 5: return launch_l2p_cells<5>(a, cs, cc);
+    case 6: return launch_l2p_cells<6>(a, cs, cc);
+    case 7: return launch_l2p_cells<7>(a, cs, cc);
+    default: return launch_l2p_cells<8>(a, cs, cc);
+  }
+}
+
 template <int P>
 int launch_p2m_cells(const LeafCall &a, const int32_t *cell_start, const int32_t *cell_count) {
   const int64_t chunks = ceil_div(a.g.cell_hi - a.g.cell_lo, kP2MCells);

@@ -212,7 +212,8 @@ class FmmEvaluator:
         # far field's all-gathers (SURVEY §8(e) "overlap")
         self.overlap_near_sharded = True
         # P2M / L2P: warp per leaf ("warp"), thread per (leaf, node) / point
-        # ("point"), or "auto" (thread-per-point L2P for sparse clouds)
+        # ("point"), leaf-cell chunks ("cells"), or "auto" (cells for sparse
+        # clouds)
         self.l2p_mode = "auto"
         # P2M: warp per leaf ("leaf"), leaf-cell chunks ("cells"), or "auto"
         # (cells for sparse clouds, see _p2m_cells)
@@ -704,9 +705,17 @@ class FmmEvaluator:
                                             locs[lev + 1][8 * qlo * row:].data_ptr(),
                                             qhi - qlo, p, m, _native.dptr(self._H), st),
                           "bfmm_l2l")
-        # fewer than 8 points per leaf cell on average: one thread per point
-        sparse = (self.l2p_mode == "point" or
-                  (self.l2p_mode == "auto" and tree.n < 8 * (1 << (3 * L))))
+        # fewer than 8 points per leaf cell on average: leaf-cell chunks
+        # with their locals staged in shared memory (or one thread per point)
+        sparse_auto = self.l2p_mode == "auto" and tree.n < 8 * (1 << (3 * L))
+        if (self.l2p_mode == "cells" or sparse_auto) and 2 <= p <= 8:
+            _native.check(self.lib.bfmm_l2p_cells(
+                tree.pts4.data_ptr(), m, tree.cell_start.data_ptr(), tree.cell_count.data_ptr(),
+                L, p, self._scheme_id, _native.dptr(self._interp), _native.dptr(leaf_geom),
+                locs[L].data_ptr(), phi_far.data_ptr(), status[_ST_REF:].data_ptr(), st),
+                "bfmm_l2p_cells")
+            return
+        sparse = self.l2p_mode == "point" or sparse_auto
         l2p = self.lib.bfmm_l2p_points if sparse else self.lib.bfmm_l2p
         _native.check(l2p(
             tree.pts4.data_ptr(), m, tree.leaves.data_ptr(), tree.starts.data_ptr(),

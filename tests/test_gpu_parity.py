@@ -440,9 +440,9 @@ def test_active_far_field_matches_dense(ncols, distinct, cache_dir):
 
 @pytest.mark.parametrize("scheme", ["chebyshev", "uniform"])
 def test_l2p_point_and_warp_kernels_agree_bitwise(scheme, cache_dir):
-    """The thread-per-point L2P (sparse clouds) and the warp-per-leaf one do
-    the same arithmetic: identical phi, including 3 columns and crowded
-    leaves (> 32 points)."""
+    """The thread-per-point and leaf-cell-chunk L2P (sparse clouds) and the
+    warp-per-leaf one do the same arithmetic: identical phi, including 3
+    columns and crowded leaves (> 32 points)."""
     gen = np.random.default_rng(97)
     pts = np.vstack([gen.random((3000, 3)),
                      np.clip(0.4 + 0.01 * gen.standard_normal((400, 3)), 0, 1)])
@@ -455,6 +455,9 @@ def test_l2p_point_and_warp_kernels_agree_bitwise(scheme, cache_dir):
     ev.l2p_mode = "point"
     b = ev.evaluate(pts, weights=w)
     assert np.array_equal(a, b)
+    ev.l2p_mode = "cells"  # leaf-cell chunks, locals staged in shared memory
+    c = ev.evaluate(pts, weights=w)
+    assert np.array_equal(a, c)
 
 
 @pytest.mark.parametrize("name,scale", [("C5", 2), ("C4", 2)])
