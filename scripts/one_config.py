@@ -19,9 +19,16 @@ plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"], e
 ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir="/tmp/bfmm_cfg_cache")
 ev.stream_levels = False  # serial levels: clean per-kernel times
 ev.overlap_near = False
+import os  # noqa: E402
+for knob in ("i8_digits", "m2l_mode", "p2m_mode", "l2p_mode"):
+    if os.environ.get("BFMM_" + knob.upper()):
+        setattr(ev, knob, os.environ["BFMM_" + knob.upper()])
+ev.profile_kernels = bool(os.environ.get("BFMM_PROFILE"))
 X = torch.from_numpy(wl["points"]).cuda()
 W = torch.from_numpy(np.ascontiguousarray(wl["weights"])).cuda()
 for _ in range(2):
     ev.evaluate(X, weights=W)
 torch.cuda.synchronize()
 print({k: round(v * 1e3, 3) if isinstance(v, float) else v for k, v in ev.timings.items()})
+if ev.profile_kernels:
+    print({k: round(v, 3) for k, v in ev.kernel_ms.items()})
