@@ -61,13 +61,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FMM matvec points/sec (fp64) at 1/2/4/8 B200; P2P & M2L % of roofline"
 
-# FP64 flops per near-field pair interaction, per kernel functor: the FP64
-# thread instructions the P2P kernel executes per pair (2*DFMA + DMUL + DADD,
-# ncu smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum over
-# the pair count), frozen once (profiles/r01_p2p_flops.txt for gauss02,
-# profiles/r02_p2p_flops.txt for the others); plus 2m for the weight FMAs
-# beyond the first column (the figure is per single-column pair).
-P2P_FLOPS_PER_PAIR = {"gauss02": 40.0}
+# FP64 flops per near-field (target, source) pair -- the kernel evaluation
+# plus the weight FMAs of all the config's columns -- per kernel functor:
+# the FP64 thread instructions the P2P kernel executes per algorithmic pair
+# (2*DFMA + DMUL + DADD, ncu smsp__sass_thread_inst_executed_op_d{fma,mul,
+# add}_pred_on.sum / near_pairs), frozen once: gauss02 in round 1
+# (profiles/r01_p2p_flops.txt; the kernel now executes 31.8), the others in
+# round 2 (profiles/r02_p2p_flops.txt).  exp03 is C3's 16-column pair.
+P2P_FLOPS_PER_PAIR = {"gauss02": 40.0, "laplacian": 18.07, "laplacianforce": 17.74,
+                      "exp03": 86.0}
+P2P_EXECUTED_PER_PAIR = {"gauss02": 31.8, "laplacian": 18.07, "laplacianforce": 17.74,
+                         "exp03": 86.0}
 NOMINAL_FP64_TF = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: DFMA/clk/SM x SMs x clock
 
 
@@ -331,6 +335,40 @@ def m2l_i8_ops(lev, rp, m, S):
     return stages * kc * ntn * per_stage
 
 
+def active_level_work(cells, off, lev, rp, m, S):
+    """Useful far pairs and executed int8 ops of an active-cell (sparse
+    cloud) level: the valid far offsets of each listed target cell
+    (octree.py:128-145), and the gather kernel's 128-row tiles per octant
+    over its 189 offsets."""
+    from paper_1903_02153_b200.tables import OFFSETS
+    c = cells.cpu().numpy().astype(np.int64)
+    n = 1 << lev
+
+    def compact(v):
+        v = v & 0x1249249249249249
+        v = (v | (v >> 2)) & 0x10C30C30C30C30C3
+        v = (v | (v >> 4)) & 0x100F00F00F00F00F
+        v = (v | (v >> 8)) & 0x1F0000FF0000FF
+        v = (v | (v >> 16)) & 0x1F00000000FFFF
+        return (v | (v >> 32)) & 0x1FFFFF
+    xyz = [compact(c >> 2), compact(c >> 1), compact(c)]
+    pairs = 0
+    for t in OFFSETS:
+        ok = np.ones(len(c), bool)
+        for a in range(3):
+            s = xyz[a] + int(t[a])
+            ok &= (s >= 0) & (s < n)
+            if t[a] == 3:
+                ok &= (xyz[a] & 1) == 0
+            elif t[a] == -3:
+                ok &= (xyz[a] & 1) == 1
+        pairs += int(ok.sum())
+    kc, ntn = -(-rp // 32), -(-rp // 64)
+    per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
+    tiles = sum(-(-(int(off[o + 1] - off[o]) * m) // 128) for o in range(8))
+    return pairs, tiles * 189 * kc * ntn * per_stage
+
+
 def committed_traffic(config, kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu captures
     (profiles/r02_traffic.json, else r01), or None when not captured."""
@@ -491,16 +529,21 @@ def measure(cfg, args, rank, world, local_rank, dist, lib, peaks, steps, warmup,
                                 for k, v in stages_serial.items()},
            "kernels_ms": {k: round(v, 4) for k, v in sorted(avg.items())}}
     if rank == 0:
-        out["roofline"], out["m2l"] = rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms)
+        share = 1.0 / world if (world == 1 or runner.shards.balance == "cells") else None
+        out["roofline"], out["m2l"] = rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms,
+                                                share if share is not None else 1.0 / world)
     return out
 
 
-def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
-    """roofline of the dominant kernel + per-level M2L figures."""
+def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms, share=1.0):
+    """roofline of the dominant kernel + per-level M2L figures.  share: the
+    fraction of every level's (and the near field's) work one rank does
+    (1/N for the equal Morton shards of N ranks)."""
     m = wl["ncols"]
+    near_pairs = near_pairs * share
     levels = {}
     if wl["scheme"] == "chebyshev":
-        flops = m2l_flops(ev, wl)
+        flops = {lev: f * share for lev, f in m2l_flops(ev, wl).items()}
         for k, v in avg.items():
             if not k.startswith("m2l_l"):
                 continue
@@ -513,10 +556,21 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
                    "rank": r, "fp64_equiv_tflops": fp64,
                    "frac_of_dmma_peak": fp64 / peaks["dmma_tflops"],
                    "traffic": committed_traffic(cfg, k)}
+            executed = None
+            if lev in ev.active_profile:  # sparse cloud: only the listed target cells
+                cells, off = ev.active_profile[lev]
+                pairs, executed = active_level_work(cells, off, lev, rp, m, S)
+                flops[lev] = pairs * 2.0 * r * r * m
+                fp64 = flops[lev] / (v * 1e-3) / 1e12
+                rec.update({"active_cells": int(off[8]), "far_pairs": pairs,
+                            "fp64_equiv_tflops": fp64,
+                            "frac_of_dmma_peak": fp64 / peaks["dmma_tflops"]})
             if rec["engine"] == "i8":
                 useful = flops[lev] * S * (S + 1) / 2  # digit products of the unpadded rank
-                executed = m2l_i8_ops(lev, rp, m, S)
-                rec.update({"kernel": "plane" if lev >= 4 else "gather",
+                if executed is None:
+                    executed = m2l_i8_ops(lev, rp, m, S) * share
+                rec.update({"kernel": ("gather (active cells)" if lev in ev.active_profile
+                                       else "plane" if lev >= 4 else "gather"),
                             "digits": f"{S} x {bits}-bit",
                             "useful_int8_tops": useful / (v * 1e-3) / 1e12,
                             "executed_int8_tops": executed / (v * 1e-3) / 1e12,
@@ -524,7 +578,7 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
                             "frac_executed": executed / (v * 1e-3) / 1e12 / peaks["i8_tops"]})
             levels[k] = rec
     else:
-        flops = fft_flops(wl)
+        flops = {lev: f * share for lev, f in fft_flops(wl).items()}
         for k, v in avg.items():
             if not k.startswith("m2lfft_l"):
                 continue
@@ -543,12 +597,15 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms):
         pairs = near_pairs * m
         roof = {"kernel": "p2p_kernel (near field, FP64 pipe)", "bound": "fp64",
                 "pair_interactions": pairs, "pairs_per_s": pairs / (ms * 1e-3),
-                "flops_per_pair": fpp}
+                "flops_per_pair": fpp, "pair": f"(target, source) pair, all {m} column(s)"}
         if fpp is not None:
-            ach = pairs * fpp / (ms * 1e-3) / 1e12
+            ach = near_pairs * fpp / (ms * 1e-3) / 1e12
+            ex = near_pairs * P2P_EXECUTED_PER_PAIR[wl["kernel"]] / (ms * 1e-3) / 1e12
             roof.update({"achieved": ach, "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
                          "frac": ach / peaks["dfma_tflops"],
                          "frac_of_nominal_37.2": ach / NOMINAL_FP64_TF,
+                         "executed_flops_per_pair": P2P_EXECUTED_PER_PAIR[wl["kernel"]],
+                         "frac_executed": ex / peaks["dfma_tflops"],
                          "peak_source": "measured live: DFMA microbenchmark "
                                         "(bfmm_device_fp64_probe); MEASURED_PEAKS.json has no "
                                         "FP64 entry"})

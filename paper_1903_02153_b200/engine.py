@@ -51,6 +51,18 @@ def _rank_interleave(rp: int) -> np.ndarray:
 
 
 _PIN_WARM = None
+_POOL = None
+
+
+def _copy_pool():
+    """Host threads for the pageable -> pinned staging copies of NumPy inputs."""
+    global _POOL
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        n = max(1, min(8, (os.cpu_count() or 1)))
+        _POOL = (ThreadPoolExecutor(max_workers=n, thread_name_prefix="bfmm-h2d"), n)
+    return _POOL
 
 
 def _warm_pinned_dma(device):
@@ -183,6 +195,7 @@ class FmmEvaluator:
         self.keep_stages = False
         self.stages = {}
         self.profile_kernels = False
+        self.active_profile = {}  # level -> (active target cells, octant offsets)
         self.near_mode = "auto"  # "auto" | "full" | "symmetric"
         # Chebyshev M2L over every cell ("dense"), over the ancestors of
         # occupied target leaves only ("active"), or "auto": active lists for
@@ -419,16 +432,23 @@ class FmmEvaluator:
         CH = self._STAGE_ELEMS
         if getattr(self, "_stage", None) is None:
             self._stage = torch.empty(2 * CH, dtype=torch.float64).pin_memory()
+            self._stage_np = self._stage.numpy()
             self._stage_ev = [torch.cuda.Event(), torch.cuda.Event()]
             for e in self._stage_ev:
                 e.record()
         st = torch.cuda.current_stream()
+        src_np = src.numpy()
+        pool, nthr = _copy_pool()
         for i, off in enumerate(range(0, n, CH)):
             k, b = min(CH, n - off), i % 2
             self._stage_ev[b].synchronize()  # the DMA that last read this half is done
-            half = self._stage[b * CH:b * CH + k]
-            half.copy_(src[off:off + k])
-            flat[off:off + k].copy_(half, non_blocking=True)
+            dst_np = self._stage_np[b * CH:b * CH + k]
+            # the host copy in parallel slices (np.copyto releases the GIL)
+            cuts = np.linspace(0, k, nthr + 1).astype(np.int64)
+            list(pool.map(lambda j: np.copyto(dst_np[cuts[j]:cuts[j + 1]],
+                                              src_np[off + cuts[j]:off + cuts[j + 1]]),
+                          range(nthr)))
+            flat[off:off + k].copy_(self._stage[b * CH:b * CH + k], non_blocking=True)
             self._stage_ev[b].record(st)
         return dst
 
@@ -643,6 +663,8 @@ class FmmEvaluator:
         if blk["kind"] == "cheb" and lev in active:
             # only the listed active target cells: compact lt rows
             cells, off, nact = active[lev]
+            if self.profile_kernels:  # the bench's per-level work accounting
+                self.active_profile[lev] = (cells[:nact], off.copy())
             rp = blk["rp"]
             longest = int(np.max(off[1:] - off[:-1]))
             ns = self._m2l_splits(lev, m, rp, max(longest, 1))
