@@ -321,6 +321,17 @@ int bfmm_direct(int handle, const double *tpts, int64_t nt, const double *spts,
                 const double *w, int64_t ns, int m, double *out,
                 bfmm_stream_t stream);
 
+/* Near field for sparse clouds (a few points per leaf, one weight column):
+ * the same sums as bfmm_p2p in the same (neighbour-order) sequence, one
+ * thread per target and 8 consecutive target leaves per warp, without the
+ * 32-target chunk prefix (no scratch).  Replaces engine.py:349-478 like
+ * bfmm_p2p. */
+int bfmm_p2p_grouped(int handle, const double *tpts4, const int64_t *tleaves,
+                     const int64_t *tstarts, const int64_t *tcounts, const int64_t *n_tleaves,
+                     int64_t max_tleaves, const double *spts4, const int32_t *scell_start,
+                     const int32_t *scell_count, int levels, int64_t cell_lo, int64_t cell_hi,
+                     double *out, bfmm_stream_t stream);
+
 /* Locate the first non-finite kernel value in the near field in the
  * reference's enumeration order (offset, target row, source row;
  * engine.py:362-441).  *key (device, init UINT64_MAX) receives

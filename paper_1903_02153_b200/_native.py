@@ -64,6 +64,7 @@ SIGNATURES = {
     "bfmm_p2p_scratch_bytes": (_SZ, [_I64, _I64]),
     "bfmm_p2p": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _P, _P, _I, _I64, _I64, _P, _P,
                       _SZ, _P]),
+    "bfmm_p2p_grouped": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _I64, _I64, _P, _P]),
     "bfmm_p2p_symmetric_scratch_bytes": (_SZ, [_I64, _I64]),
     "bfmm_p2p_symmetric": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _I64, _I64, _I64, _D,
                                 _P, _P, _SZ, _P]),

@@ -122,6 +122,7 @@ struct JitKernel {
   CUfunction sym;
   CUfunction direct;
   CUfunction block;
+  CUfunction group;
 };
 
 std::mutex g_jit_mu;
@@ -181,6 +182,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
   names.push_back("bfmm_nf::p2p_sym_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::direct_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::pair_block_kernel<bfmm_nf::KUser>");
+  names.push_back("bfmm_nf::p2p_group_kernel<bfmm_nf::KUser>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--std=c++17",
                                     "-default-device", "-lineinfo"};
@@ -231,7 +233,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 9; ++i) {
+  for (int i = 0; i < 10; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
@@ -241,7 +243,8 @@ int jit_compile(int kind, const char *expr, int *handle) {
     else if (i == 5) jk.locate = f;
     else if (i == 6) jk.sym = f;
     else if (i == 7) jk.direct = f;
-    else jk.block = f;
+    else if (i == 8) jk.block = f;
+    else jk.group = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -336,11 +339,13 @@ __global__ void chunk_counts_kernel(const int64_t *__restrict__ counts,
                                     const int64_t *__restrict__ leaves,
                                     const int64_t *__restrict__ n_leaves,
                                     int64_t max_leaves, int64_t cell_lo,
-                                    int64_t cell_hi, int64_t *__restrict__ nch) {
+                                    int64_t cell_hi, int small_max,
+                                    int64_t *__restrict__ nch) {
+  // leaves of <= small_max points go to p2p_group_kernel instead
   const int64_t nl = *n_leaves;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
        i < max_leaves; i += int64_t(gridDim.x) * blockDim.x)
-    nch[i] = (i < nl && leaves[i] >= cell_lo && leaves[i] < cell_hi)
+    nch[i] = (i < nl && leaves[i] >= cell_lo && leaves[i] < cell_hi && counts[i] > small_max)
                  ? (counts[i] + 31) / 32 : 0;
 }
 
@@ -560,12 +565,61 @@ int launch_sym(int handle, const bfmm_nf::Args &a, double *slots, int64_t nt,
 
 using namespace bfmm;
 
+// leaves of at most this many points take the one-thread-per-target kernel
+constexpr int kSmallLeaf = 8;
+
 extern "C" int bfmm_kernel_compile(int kind, const char *expr, int *handle) {
   if (kind < 0 || kind > 2 || !expr || !handle) {
     set_error("bfmm_kernel_compile: bad arguments");
     return 2;
   }
   return jit_compile(kind, expr, handle);
+}
+
+// p2p_group_kernel over the leaves of <= small_max points
+static int launch_group(int handle, const double *tpts4, const int64_t *tleaves,
+                        const int64_t *tstarts, const int64_t *tcounts, const int64_t *n_tleaves,
+                        int64_t max_tleaves, const double *spts4, const int32_t *scell_start,
+                        const int32_t *scell_count, int levels, int64_t cell_lo, int64_t cell_hi,
+                        int small_max, double *out, cudaStream_t st) {
+  bfmm_nf::Args a = make_args(tpts4, tleaves, tstarts, tcounts, n_tleaves, spts4, nullptr, 1,
+                               scell_start, scell_count, levels, out, nullptr);
+  const int64_t warps = ceil_div(max_tleaves, bfmm_nf::kGroupLeaves);
+  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(warps, bfmm_nf::kWarps),
+                                              (int64_t)kNumSMs * 16)),
+      block(32 * bfmm_nf::kWarps);
+  const long long lo = cell_lo, hi = cell_hi;
+  const int sm = small_max;
+  switch (handle) {
+    case 1: bfmm_nf::p2p_group_kernel<KLaplace><<<grid, block, 0, st>>>(a, lo, hi, sm); break;
+    case 2: bfmm_nf::p2p_group_kernel<KLaplaceForce><<<grid, block, 0, st>>>(a, lo, hi, sm); break;
+    case 3: bfmm_nf::p2p_group_kernel<KGaussian><<<grid, block, 0, st>>>(a, lo, hi, sm); break;
+    case 4: bfmm_nf::p2p_group_kernel<KExponential><<<grid, block, 0, st>>>(a, lo, hi, sm); break;
+    case 5: bfmm_nf::p2p_group_kernel<KLogarithm><<<grid, block, 0, st>>>(a, lo, hi, sm); break;
+    default: {
+      JitKernel jk;
+      {
+        std::lock_guard<std::mutex> lock(g_jit_mu);
+        if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+          set_error("p2p_group_kernel: unknown kernel handle %d", handle);
+          return 2;
+        }
+        jk = g_jit[handle - kFirstJit];
+      }
+      bfmm_nf::Args args = a;
+      long long l1 = lo, h1 = hi;
+      int s1 = sm;
+      void *params[] = {&args, &l1, &h1, &s1};
+      if (driver().LaunchKernel(jk.group, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
+                                nullptr) != CUDA_SUCCESS) {
+        set_error("p2p_group_kernel: cuLaunchKernel failed");
+        return 1;
+      }
+      add_launches(1);
+      return 0;
+    }
+  }
+  return check_launch("p2p_group_kernel");
 }
 
 extern "C" size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves, int64_t n_targets) {
@@ -600,8 +654,17 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
   chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256),
                                                     kNumSMs * 16),
                         256, 0, st>>>(tcounts, tleaves, n_tleaves, max_tleaves,
-                                      cell_lo, cell_hi, nch);
+                                      cell_lo, cell_hi, m == 1 ? kSmallLeaf : 0, nch);
   if (check_launch("chunk_counts_kernel")) return 1;
+  if (m == 1) {
+    // one weight column: leaves of <= kSmallLeaf points (sparse clouds: C5's
+    // 3.8 per leaf, C4's sphere shell) run one thread per target
+    // (p2p_group_kernel); the 32-target chunks below cover the rest
+    if (int rc = launch_group(handle, tpts4, tleaves, tstarts, tcounts, n_tleaves, max_tleaves,
+                              spts4, scell_start, scell_count, levels, cell_lo, cell_hi,
+                              kSmallLeaf, out, st))
+      return rc;
+  }
   size_t cb = fixed - cub_off;
   if (cub::DeviceScan::InclusiveSum(static_cast<char *>(scratch) + cub_off, cb,
                                     nch, incl, (int)max_tleaves,
@@ -643,6 +706,23 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
     c0 += kMCs[mci];
   }
   return 0;
+}
+
+// Near field for sparse clouds (p2p_group_kernel): one weight column, one
+// lane per target, kGroupLeaves leaves per warp.
+// Near field for sparse clouds (p2p_group_kernel): one weight column, one
+// lane per target, kGroupLeaves leaves per warp, leaves of <= small_max
+// points only.
+extern "C" int bfmm_p2p_grouped(int handle, const double *tpts4, const int64_t *tleaves,
+                                const int64_t *tstarts, const int64_t *tcounts,
+                                const int64_t *n_tleaves, int64_t max_tleaves,
+                                const double *spts4, const int32_t *scell_start,
+                                const int32_t *scell_count, int levels, int64_t cell_lo,
+                                int64_t cell_hi, double *out, bfmm_stream_t stream) {
+  if (max_tleaves <= 0) return 0;
+  return launch_group(handle, tpts4, tleaves, tstarts, tcounts, n_tleaves, max_tleaves, spts4,
+                      scell_start, scell_count, levels, cell_lo, cell_hi, 1 << 30, out,
+                      as_stream(stream));
 }
 
 extern "C" int bfmm_p2p_locate(int handle, const double *tpts4,
@@ -748,7 +828,7 @@ extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
   int64_t *incl = nch + max_leaves;
   chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_leaves, 256), kNumSMs * 16),
                         256, 0, st>>>(counts, leaves, n_leaves, max_leaves, cell_lo, cell_hi,
-                                      nch);
+                                      0, nch);
   if (check_launch("chunk_counts_kernel")) return 1;
   size_t cb = chunk - cub_off;
   if (cub::DeviceScan::InclusiveSum(base + cub_off, cb, nch, incl, (int)max_leaves, st) !=

@@ -196,7 +196,11 @@ class FmmEvaluator:
         self.stages = {}
         self.profile_kernels = False
         self.active_profile = {}  # level -> (active target cells, octant offsets)
-        self.near_mode = "auto"  # "auto" | "full" | "symmetric"
+        # near field: "auto" / "full" (bfmm_p2p: 32-target chunks, and with
+        # one column a thread per target for leaves of <= 8 points),
+        # "grouped" (a thread per target for every leaf), or "symmetric"
+        # (transpose replay)
+        self.near_mode = "auto"
         # Chebyshev M2L over every cell ("dense"), over the ancestors of
         # occupied target leaves only ("active"), or "auto": active lists for
         # sparse clouds (fewer than 8 points per leaf cell), per level only
@@ -761,6 +765,18 @@ class FmmEvaluator:
                 ttree.max_leaves, stree.cell_start.data_ptr(), stree.cell_count.data_ptr(),
                 self.plan.levels, lo, hi, ttree.n, float(self.kernel.symmetry), near.data_ptr(),
                 scratch.data_ptr(), sb, st), "bfmm_p2p_symmetric")
+            self._kspan("p2p", e0)
+            return
+        if self.near_mode == "grouped" and m == 1:
+            # every leaf one thread per target, 8 leaves per warp (bfmm_p2p
+            # already does this for its leaves of <= 8 points)
+            e0 = self._kevent()
+            _native.check(self.lib.bfmm_p2p_grouped(
+                self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(),
+                ttree.starts.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
+                ttree.max_leaves, stree.pts4.data_ptr(), stree.cell_start.data_ptr(),
+                stree.cell_count.data_ptr(), self.plan.levels, lo, hi, near.data_ptr(), st),
+                "bfmm_p2p_grouped")
             self._kspan("p2p", e0)
             return
         e0 = self._kevent()

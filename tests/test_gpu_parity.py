@@ -479,3 +479,21 @@ def test_p2m_cell_chunks_equal_warp_per_leaf(name, scale, cache_dir):
     else:
         assert rel_l2(out["cells"][1], out["leaf"][1]) < 1e-14
     assert rel_l2(out["cells"][0], out["leaf"][0]) < 1e-13
+
+
+@pytest.mark.parametrize("name,scale", [("C5", 2), ("C4", 2)])
+def test_grouped_near_field_matches(name, scale, cache_dir):
+    """The one-thread-per-target near field (p2p_group_kernel, which
+    bfmm_p2p runs for leaves of <= 8 points) against the 32-target-chunk
+    kernel for every leaf and against the reference fixture."""
+    g = golden(f"{name.lower()}_s{scale}")
+    wl = workloads.make(name, scale)
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
+    ev.keep_stages = True
+    out = {}
+    for mode in ("auto", "grouped"):
+        ev.near_mode = mode
+        phi = ev.evaluate(wl["points"], weights=wl["weights"])
+        out[mode] = (phi, ev.stages["near"].cpu().numpy())
+        assert rel_l2(phi[wl["check_idx"]], g["phi_idx"]) < PHI_TOL
+    assert rel_l2(out["grouped"][1], out["auto"][1]) < 1e-14
