@@ -188,7 +188,7 @@ def test_order_sweep_matches_reference(cache_dir):
 
 
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2), ("C3", 2), ("C3", 1),
-                                        ("C5", 2), ("C4", 1)])
+                                        ("C5", 2), ("C4", 1), ("C5", 1)])
 def test_scaled_configs_match_reference(name, scale, cache_dir):
     g = golden(f"{name.lower()}_s{scale}")
     wl = workloads.make(name, scale)
