@@ -1241,9 +1241,11 @@ class FmmEvaluator:
         c = int(cnt.item())
         return tg[:c].cpu().numpy(), sr[:c].cpu().numpy()
 
-    def near_segments(self, points, t_index):
+    def near_segments(self, points, t_index, tree=None):
+        """(tseg, sseg) of near offset t_index (reference _neighbor_segments,
+        engine.py:401-417) for a point set's tree (or a prebuilt one)."""
         torch = _torch()
-        tr = self.partition(points)["tree"]
+        tr = tree if tree is not None else self.partition(points)["tree"]
         out = torch.empty(max(tr.max_leaves, 1), dtype=torch.int64, device=self.device)
         _native.check(self.lib.bfmm_near_pairs(self.plan.levels, t_index, tr.leaves.data_ptr(),
                                                tr.n_leaves.data_ptr(), tr.max_leaves,

@@ -364,6 +364,45 @@ def case_highorder():
     save("highorder", **out)
 
 
+def case_c5struct():
+    """Full-size C5 structure from the real reference (the full C5 evaluate
+    does not fit any host here, see case c5s1): the partition
+    (`_Partition.build`), the far-field pair lists of levels 6-8
+    (`cell_pairs_for_offset`, all 316 offsets, streamed into one sha256 per
+    level) and the 27 near-field segment lists (`_neighbor_segments`)."""
+    wl = workloads.make("C5", 0)
+    plan = plan_of(wl)
+    ev = reng.FmmEvaluator(ref_kernel(wl["kernel"]), plan, cache_dir=CACHE)
+    t0 = time.perf_counter()
+    part = reng._Partition.build(ev.tree, wl["points"])
+    out = {"perm_sha": np.array(sha(part.perm.astype(np.int64))),
+           "leaves_sha": np.array(sha(part.leaves.astype(np.int64))),
+           "starts_sha": np.array(sha(part.starts.astype(np.int64))),
+           "counts_sha": np.array(sha(part.counts.astype(np.int64))),
+           "n_leaves": np.array(len(part.leaves))}
+    print("partition", time.perf_counter() - t0, flush=True)
+    for lev in (6, 7, 8):
+        t0 = time.perf_counter()
+        htg, hsr, counts = hashlib.sha256(), hashlib.sha256(), []
+        for t in offset_set():
+            tg, sr = ev.tree.cell_pairs_for_offset(lev, tuple(t))
+            htg.update(np.ascontiguousarray(tg, dtype=np.int64).tobytes())
+            hsr.update(np.ascontiguousarray(sr, dtype=np.int64).tobytes())
+            counts.append(len(tg))
+        out[f"l{lev}_tg_sha"], out[f"l{lev}_sr_sha"] = np.array(htg.hexdigest()), np.array(hsr.hexdigest())
+        out[f"l{lev}_counts"] = np.array(counts)
+        print("level", lev, time.perf_counter() - t0, flush=True)
+    ht, hs, cnt = hashlib.sha256(), hashlib.sha256(), []
+    for t in neighbor_offsets():
+        a, b = ev._neighbor_segments(part, part, tuple(t))
+        ht.update(np.ascontiguousarray(a, dtype=np.int64).tobytes())
+        hs.update(np.ascontiguousarray(b, dtype=np.int64).tobytes())
+        cnt.append(len(a))
+    out["near_tseg_sha"], out["near_sseg_sha"] = np.array(ht.hexdigest()), np.array(hs.hexdigest())
+    out["near_counts"] = np.array(cnt)
+    save("c5_struct", **out)
+
+
 def case_eig():
     """randomized_eig on the FMM matvec, k + q = 120 columns (lin:39-104)."""
     from boxfmm.linops import evaluator_matvec, randomized_eig
@@ -454,6 +493,7 @@ CASES = {
     # 2 threads the GPU host's 196 GB allow, past the 60-min call limit)
     "c5s1": lambda: case_config("C5", 1, threads=int(os.environ.get("BOXFMM_THREADS", "4"))),
     "highorder": case_highorder,
+    "c5struct": case_c5struct,
     "c3full": lambda: case_full("C3", int(os.environ.get("BOXFMM_THREADS", "8"))),
     "c4full": lambda: case_full("C4", int(os.environ.get("BOXFMM_THREADS", "6"))),
     "c5full": lambda: case_full("C5", int(os.environ.get("BOXFMM_THREADS", "2")), direct=False),
