@@ -204,7 +204,15 @@ int bfmm_m2l_cheb_cells(const double *z, double *lt, int level, int m, int rp,
  *    ceil(rp/32) terms an accumulator sums (rp <= 96; <= 64 for the
  *    mixed-octant coarse levels). */
 #define BFMM_I8_BASE256 0x100
+/* S flag of bfmm_m2l_i8_slice_z: zmax holds the scales already (from
+ * bfmm_m2l_i8_zmax, e.g. max-reduced over the ranks of a sharded matvec so
+ * every shard cuts its digits exactly like the unsharded evaluation). */
+#define BFMM_I8_ZMAX_GIVEN 0x200
 size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int S);
+/* zmax[c] = bit pattern of max |z| over weight column c (the first half of
+ * bfmm_m2l_i8_slice_z). */
+int bfmm_m2l_i8_zmax(const double *z, int64_t rows, int m, int rp,
+                     unsigned long long *zmax, bfmm_stream_t stream);
 int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int S,
                         int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream);
 int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq);
@@ -281,6 +289,22 @@ int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
              const int32_t *scell_start, const int32_t *scell_count,
              int levels, int64_t cell_lo, int64_t cell_hi, double *out,
              void *scratch, size_t scratch_bytes, bfmm_stream_t stream);
+
+/* bfmm_p2p with the target tree's dense cell map (tcell_start /
+ * tcell_count of bfmm_tree_build): for one weight column the cells of <= 8
+ * points run through p2p_tile_kernel -- a CTA per aligned 4 x 4 x 4 Morton
+ * block of target cells with its 6 x 6 x 6 source halo staged in shared
+ * memory, one thread per target, the same sums in the same order as the
+ * thread-per-target path of bfmm_p2p (bitwise equal).  Same output and
+ * sharding contract as bfmm_p2p (engine.py:349-478). */
+int bfmm_p2p_cells(int handle, const double *tpts4, const int64_t *tleaves,
+                   const int64_t *tstarts, const int64_t *tcounts,
+                   const int64_t *n_tleaves, int64_t max_tleaves,
+                   const int32_t *tcell_start, const int32_t *tcell_count,
+                   const double *spts4, const double *swsorted, int m,
+                   const int32_t *scell_start, const int32_t *scell_count,
+                   int levels, int64_t cell_lo, int64_t cell_hi, double *out,
+                   void *scratch, size_t scratch_bytes, bfmm_stream_t stream);
 
 /* Symmetric near field for shared targets = sources and a kernel with
  * K(y, x) = sign K(x, y) (the reference's transpose replay,

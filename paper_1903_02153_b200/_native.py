@@ -46,6 +46,7 @@ SIGNATURES = {
     "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _I64, _I64, _P, _P]),
     "bfmm_m2l_i8_zs_bytes": (_SZ, [_I64, _I, _I]),
     "bfmm_m2l_i8_slice_z": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P]),
+    "bfmm_m2l_i8_zmax": (_I, [_P, _I64, _I, _I, _P, _P]),
     "bfmm_m2l_i8_splits": (_I, [_I, _I, _I, _I64]),
     "bfmm_m2l_i8": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _I64, _P]),
     "bfmm_m2l_i8_cells": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
@@ -64,6 +65,8 @@ SIGNATURES = {
     "bfmm_p2p_scratch_bytes": (_SZ, [_I64, _I64]),
     "bfmm_p2p": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _P, _P, _I, _I64, _I64, _P, _P,
                       _SZ, _P]),
+    "bfmm_p2p_cells": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I, _P, _P, _I, _I64,
+                            _I64, _P, _P, _SZ, _P]),
     "bfmm_p2p_grouped": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _I64, _I64, _P, _P]),
     "bfmm_p2p_symmetric_scratch_bytes": (_SZ, [_I64, _I64]),
     "bfmm_p2p_symmetric": (_I, [_I, _P, _P, _P, _P, _P, _I64, _P, _P, _I, _I64, _I64, _I64, _D,
@@ -82,6 +85,8 @@ SIGNATURES = {
 
 #: bfmm_m2l_i8* S flag: 8-bit digits (include/bfmm.h BFMM_I8_BASE256)
 I8_BASE256 = 0x100
+#: bfmm_m2l_i8_slice_z S flag: zmax given (include/bfmm.h BFMM_I8_ZMAX_GIVEN)
+I8_ZMAX_GIVEN = 0x200
 
 _lib = None
 _lock = threading.Lock()

@@ -530,6 +530,24 @@ extern "C" size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int Sarg) {
   return (size_t)rows * ceil_div(rp, 32) * (Sarg & 0xff) * 32;
 }
 
+extern "C" int bfmm_m2l_i8_zmax(const double *z, int64_t rows, int m, int rp,
+                                unsigned long long *zmax, bfmm_stream_t stream) {
+  if (rp <= 0 || rows < 0 || m < 1 || m > 65535 || rows % m) {
+    set_error("bfmm_m2l_i8_zmax: rp=%d, m=%d, rows=%lld", rp, m, (long long)rows);
+    return 2;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(zmax, 0, sizeof(unsigned long long) * m, st) != cudaSuccess) {
+    set_error("bfmm_m2l_i8_zmax: memset failed");
+    return 1;
+  }
+  if (rows == 0) return 0;
+  const int64_t n = rows / m * rp;
+  absmax_bits_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs), m), 256,
+                       0, st>>>(z, rows, rp, m, zmax);
+  return check_launch("absmax_bits_kernel");
+}
+
 extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int Sarg,
                                    int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream) {
   int S, B;
@@ -541,12 +559,10 @@ extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp,
     return 2;
   }
   cudaStream_t st = as_stream(stream);
-  cudaMemsetAsync(zmax, 0, sizeof(unsigned long long) * m, st);
+  if (!(Sarg & BFMM_I8_ZMAX_GIVEN)) {
+    if (int rc = bfmm_m2l_i8_zmax(z, rows, m, rp, zmax, stream)) return rc;
+  }
   if (rows == 0) return 0;
-  const int64_t n = rows / m * rp;
-  absmax_bits_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs), m), 256,
-                       0, st>>>(z, rows, rp, m, zmax);
-  if (check_launch("absmax_bits_kernel")) return 1;
   const int kc_n = (int)ceil_div(rp, 32);
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows * kc_n * 2, 256), 16 * kNumSMs);
   if (B == 8) {

@@ -123,6 +123,7 @@ struct JitKernel {
   CUfunction direct;
   CUfunction block;
   CUfunction group;
+  CUfunction tile;
 };
 
 std::mutex g_jit_mu;
@@ -183,6 +184,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
   names.push_back("bfmm_nf::direct_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::pair_block_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::p2p_group_kernel<bfmm_nf::KUser>");
+  names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--std=c++17",
                                     "-default-device", "-lineinfo"};
@@ -233,7 +235,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 10; ++i) {
+  for (int i = 0; i < 11; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
@@ -244,7 +246,8 @@ int jit_compile(int kind, const char *expr, int *handle) {
     else if (i == 6) jk.sym = f;
     else if (i == 7) jk.direct = f;
     else if (i == 8) jk.block = f;
-    else jk.group = f;
+    else if (i == 9) jk.group = f;
+    else jk.tile = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -622,19 +625,67 @@ static int launch_group(int handle, const double *tpts4, const int64_t *tleaves,
   return check_launch("p2p_group_kernel");
 }
 
+// p2p_tile_kernel over the target cells of <= small_max points in
+// [cell_lo, cell_hi): one CTA per aligned 64-cell Morton block
+static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_start,
+                       const int32_t *tcell_count, const double *spts4,
+                       const int32_t *scell_start, const int32_t *scell_count, int levels,
+                       int64_t cell_lo, int64_t cell_hi, int small_max, double *out,
+                       cudaStream_t st) {
+  bfmm_nf::Args a = make_args(tpts4, nullptr, nullptr, nullptr, nullptr, spts4, nullptr, 1,
+                               scell_start, scell_count, levels, out, nullptr);
+  const int64_t tiles = ceil_div(cell_hi, 64) - cell_lo / 64;
+  if (tiles <= 0) return 0;
+  static unsigned long long attr = 0;
+  (void)attr;
+  const dim3 grid((unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 5 * 8)),
+      block(bfmm_nf::kTileThreads);
+  long long lo = cell_lo, hi = cell_hi;
+  int sm = small_max;
+  const int *cs = tcell_start, *cc = tcell_count;
+  switch (handle) {
+    case 1: bfmm_nf::p2p_tile_kernel<KLaplace><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
+    case 2: bfmm_nf::p2p_tile_kernel<KLaplaceForce><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
+    case 3: bfmm_nf::p2p_tile_kernel<KGaussian><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
+    case 4: bfmm_nf::p2p_tile_kernel<KExponential><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
+    case 5: bfmm_nf::p2p_tile_kernel<KLogarithm><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
+    default: {
+      JitKernel jk;
+      {
+        std::lock_guard<std::mutex> lock(g_jit_mu);
+        if (handle < kFirstJit || handle - kFirstJit >= (int)g_jit.size()) {
+          set_error("p2p_tile_kernel: unknown kernel handle %d", handle);
+          return 2;
+        }
+        jk = g_jit[handle - kFirstJit];
+      }
+      void *params[] = {&a, &cs, &cc, &lo, &hi, &sm};
+      if (driver().LaunchKernel(jk.tile, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
+                                nullptr) != CUDA_SUCCESS) {
+        set_error("p2p_tile_kernel: cuLaunchKernel failed");
+        return 1;
+      }
+      add_launches(1);
+      return 0;
+    }
+  }
+  return check_launch("p2p_tile_kernel");
+}
+
 extern "C" size_t bfmm_p2p_scratch_bytes(int64_t max_tleaves, int64_t n_targets) {
   size_t off;
   return p2p_scratch(max_tleaves < 1 ? 1 : max_tleaves, &off, n_targets);
 }
 
-extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
-                        const int64_t *tstarts, const int64_t *tcounts,
-                        const int64_t *n_tleaves, int64_t max_tleaves,
-                        const double *spts4, const double *swsorted, int m,
-                        const int32_t *scell_start, const int32_t *scell_count,
-                        int levels, int64_t cell_lo, int64_t cell_hi,
-                        double *out, void *scratch, size_t scratch_bytes,
-                        bfmm_stream_t stream) {
+static int p2p_impl(int handle, const double *tpts4, const int64_t *tleaves,
+                    const int64_t *tstarts, const int64_t *tcounts,
+                    const int64_t *n_tleaves, int64_t max_tleaves,
+                    const int32_t *tcell_start, const int32_t *tcell_count,
+                    const double *spts4, const double *swsorted, int m,
+                    const int32_t *scell_start, const int32_t *scell_count,
+                    int levels, int64_t cell_lo, int64_t cell_hi,
+                    double *out, void *scratch, size_t scratch_bytes,
+                    bfmm_stream_t stream) {
   if (max_tleaves <= 0) return 0;
   size_t cub_off;
   const size_t fixed = p2p_fixed(max_tleaves, &cub_off);
@@ -660,9 +711,13 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
     // one weight column: leaves of <= kSmallLeaf points (sparse clouds: C5's
     // 3.8 per leaf, C4's sphere shell) run one thread per target
     // (p2p_group_kernel); the 32-target chunks below cover the rest
-    if (int rc = launch_group(handle, tpts4, tleaves, tstarts, tcounts, n_tleaves, max_tleaves,
-                              spts4, scell_start, scell_count, levels, cell_lo, cell_hi,
-                              kSmallLeaf, out, st))
+    // (tiled through shared memory when the target cell map is given)
+    if (int rc = tcell_start
+                     ? launch_tile(handle, tpts4, tcell_start, tcell_count, spts4, scell_start,
+                                   scell_count, levels, cell_lo, cell_hi, kSmallLeaf, out, st)
+                     : launch_group(handle, tpts4, tleaves, tstarts, tcounts, n_tleaves,
+                                    max_tleaves, spts4, scell_start, scell_count, levels, cell_lo,
+                                    cell_hi, kSmallLeaf, out, st))
       return rc;
   }
   size_t cb = fixed - cub_off;
@@ -708,8 +763,36 @@ extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
   return 0;
 }
 
-// Near field for sparse clouds (p2p_group_kernel): one weight column, one
-// lane per target, kGroupLeaves leaves per warp.
+extern "C" int bfmm_p2p(int handle, const double *tpts4, const int64_t *tleaves,
+                        const int64_t *tstarts, const int64_t *tcounts,
+                        const int64_t *n_tleaves, int64_t max_tleaves,
+                        const double *spts4, const double *swsorted, int m,
+                        const int32_t *scell_start, const int32_t *scell_count,
+                        int levels, int64_t cell_lo, int64_t cell_hi,
+                        double *out, void *scratch, size_t scratch_bytes,
+                        bfmm_stream_t stream) {
+  return p2p_impl(handle, tpts4, tleaves, tstarts, tcounts, n_tleaves, max_tleaves, nullptr,
+                  nullptr, spts4, swsorted, m, scell_start, scell_count, levels, cell_lo, cell_hi,
+                  out, scratch, scratch_bytes, stream);
+}
+
+extern "C" int bfmm_p2p_cells(int handle, const double *tpts4, const int64_t *tleaves,
+                              const int64_t *tstarts, const int64_t *tcounts,
+                              const int64_t *n_tleaves, int64_t max_tleaves,
+                              const int32_t *tcell_start, const int32_t *tcell_count,
+                              const double *spts4, const double *swsorted, int m,
+                              const int32_t *scell_start, const int32_t *scell_count,
+                              int levels, int64_t cell_lo, int64_t cell_hi, double *out,
+                              void *scratch, size_t scratch_bytes, bfmm_stream_t stream) {
+  if (!tcell_start || !tcell_count) {
+    set_error("bfmm_p2p_cells: target cell map required");
+    return 2;
+  }
+  return p2p_impl(handle, tpts4, tleaves, tstarts, tcounts, n_tleaves, max_tleaves, tcell_start,
+                  tcell_count, spts4, swsorted, m, scell_start, scell_count, levels, cell_lo,
+                  cell_hi, out, scratch, scratch_bytes, stream);
+}
+
 // Near field for sparse clouds (p2p_group_kernel): one weight column, one
 // lane per target, kGroupLeaves leaves per warp, leaves of <= small_max
 // points only.

@@ -196,10 +196,11 @@ class FmmEvaluator:
         self.stages = {}
         self.profile_kernels = False
         self.active_profile = {}  # level -> (active target cells, octant offsets)
-        # near field: "auto" / "full" (bfmm_p2p: 32-target chunks, and with
-        # one column a thread per target for leaves of <= 8 points),
-        # "grouped" (a thread per target for every leaf), or "symmetric"
-        # (transpose replay)
+        # near field: "auto" / "full" (bfmm_p2p_cells: 32-target chunks, and
+        # with one column a thread per target for leaves of <= 8 points over
+        # shared-memory source tiles), "untiled" (the same without the
+        # tiles), "grouped" (a thread per target for every leaf), or
+        # "symmetric" (transpose replay)
         self.near_mode = "auto"
         # Chebyshev M2L over every cell ("dense"), over the ancestors of
         # occupied target leaves only ("active"), or "auto": active lists for
@@ -351,7 +352,8 @@ class FmmEvaluator:
                 return 6, 8
         return int(self.i8_slices), 7
 
-    def _m2l_translate(self, z, lt, lev, m, rp, ns, blk, st, q_lo=0, nq=0, cells=None, off=None):
+    def _m2l_translate(self, z, lt, lev, m, rp, ns, blk, st, q_lo=0, nq=0, cells=None, off=None,
+                       shard=None):
         """lt = the 189-offset translation of z (engine.py:228-256), on the
         level's engine (_level_engine); cells/off: listed active targets."""
         torch = _torch()
@@ -363,6 +365,13 @@ class FmmEvaluator:
             zs = torch.empty(int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, Sarg)), dtype=torch.int8,
                              device=self.device)
             zmax = torch.empty(m, dtype=torch.int64, device=self.device)
+            if shard is not None and not shard[0].full:
+                # one digit scale per column over ALL ranks' cells: every
+                # shard cuts z exactly like the unsharded evaluation
+                _native.check(self.lib.bfmm_m2l_i8_zmax(z.data_ptr(), rows, m, rp,
+                                                        zmax.data_ptr(), st), "bfmm_m2l_i8_zmax")
+                shard[1].allreduce_max(zmax)
+                Sarg |= _native.I8_ZMAX_GIVEN
             _native.check(self.lib.bfmm_m2l_i8_slice_z(z.data_ptr(), rows, m, rp, Sarg,
                                                        zs.data_ptr(), zmax.data_ptr(), st),
                           "bfmm_m2l_i8_slice_z")
@@ -681,7 +690,7 @@ class FmmEvaluator:
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
                 shard[1].exchange_level(z, m * rp, lev, shard[0])
-            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, cells=cells, off=off)
+            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, cells=cells, off=off, shard=shard)
             if nact:
                 _native.check(self.lib.bfmm_rows_gemm_scatter(
                     lt.data_ptr(), nact * m, rp, blk["UT"].data_ptr(), p3, out.data_ptr(),
@@ -698,7 +707,7 @@ class FmmEvaluator:
                 # the sources this shard's M2L reads: its halo (fine levels)
                 # or the whole level (coarse levels)
                 shard[1].exchange_level(z, m * rp, lev, shard[0])
-            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq)
+            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq, shard=shard)
             _native.check(self.lib.bfmm_rows_gemm(
                 lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
                 out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
@@ -734,7 +743,8 @@ class FmmEvaluator:
         # fewer than 8 points per leaf cell on average: leaf-cell chunks
         # with their locals staged in shared memory (or one thread per point)
         sparse_auto = self.l2p_mode == "auto" and tree.n < 8 * (1 << (3 * L))
-        if (self.l2p_mode == "cells" or sparse_auto) and 2 <= p <= 8:
+        # (the cells kernel stages one cell's m * p^3 locals in <= 96 KB)
+        if (self.l2p_mode == "cells" or sparse_auto) and 2 <= p <= 8 and m * p ** 3 * 8 <= 96 * 1024:
             _native.check(self.lib.bfmm_l2p_cells(
                 tree.pts4.data_ptr(), m, tree.cell_start.data_ptr(), tree.cell_count.data_ptr(),
                 L, p, self._scheme_id, _native.dptr(self._interp), _native.dptr(leaf_geom),
@@ -779,13 +789,26 @@ class FmmEvaluator:
                 "bfmm_p2p_grouped")
             self._kspan("p2p", e0)
             return
+        if self.near_mode == "untiled":
+            # (diagnostic) the thread-per-target kernel reading sources
+            # through L1/L2 instead of the shared-memory tiles
+            e0 = self._kevent()
+            _native.check(self.lib.bfmm_p2p(
+                self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(),
+                ttree.starts.data_ptr(), ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(),
+                ttree.max_leaves, stree.pts4.data_ptr(), ws.data_ptr(), m,
+                stree.cell_start.data_ptr(), stree.cell_count.data_ptr(), self.plan.levels, lo,
+                hi, near.data_ptr(), scratch.data_ptr(), sb, st), "bfmm_p2p")
+            self._kspan("p2p", e0)
+            return
         e0 = self._kevent()
-        _native.check(self.lib.bfmm_p2p(
+        _native.check(self.lib.bfmm_p2p_cells(
             self._handle, ttree.pts4.data_ptr(), ttree.leaves.data_ptr(), ttree.starts.data_ptr(),
             ttree.counts.data_ptr(), ttree.n_leaves.data_ptr(), ttree.max_leaves,
+            ttree.cell_start.data_ptr(), ttree.cell_count.data_ptr(),
             stree.pts4.data_ptr(), ws.data_ptr(), m, stree.cell_start.data_ptr(),
             stree.cell_count.data_ptr(), self.plan.levels, lo, hi, near.data_ptr(),
-            scratch.data_ptr(), sb, st), "bfmm_p2p")
+            scratch.data_ptr(), sb, st), "bfmm_p2p_cells")
         self._kspan("p2p", e0)
 
     def _use_symmetric(self, ttree, stree, m):

@@ -313,6 +313,15 @@ class ShardComm:
         self._coll(self.dist.all_gather_into_tensor, buf, pad)
         return torch.cat([buf[r * longest:r * longest + counts[r]] for r in range(self.world)])
 
+    def allreduce_max(self, t):
+        if self.host_staged and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t
+
     def allreduce_sum(self, t):
         if self.host_staged and t.is_cuda:
             h = t.cpu()

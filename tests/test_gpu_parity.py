@@ -267,7 +267,11 @@ def test_linearity_in_weights(cache_dir):
     ev = bf.FmmEvaluator(bf.EXPONENTIAL, small_plan(), cache_dir=cache_dir)
     lhs = ev.evaluate(pts, weights=2.5 * u - 0.75 * v)
     rhs = 2.5 * ev.evaluate(pts, weights=u) - 0.75 * ev.evaluate(pts, weights=v)
-    assert np.max(np.abs(lhs - rhs)) / np.max(np.abs(rhs)) < 1e-12
+    # the int8 M2L cuts z under one power-of-two scale per column, so the
+    # three evaluations truncate at different absolute levels (six 8-bit
+    # digits: ~2^-40 of the scale); 1e-11 still sits 10x inside the 1e-10
+    # parity bar
+    assert np.max(np.abs(lhs - rhs)) / np.max(np.abs(rhs)) < 1e-11
 
 
 def test_far_field_actually_contributes(cache_dir):
@@ -396,7 +400,10 @@ def test_symmetric_near_field_falls_back_on_crowded_leaves(cache_dir):
     a = ev.evaluate(pts, weights=w)
     ev.near_mode = "full"
     b = ev.evaluate(pts, weights=w)
-    assert np.array_equal(a, b)  # device-side fallback runs the same kernel
+    # device-side fallback: the plain P2P over all leaves (its chunk kernel
+    # for every leaf, where "full" sends leaves of <= 8 points to the
+    # thread-per-target kernel: same pairs, different summation order)
+    assert rel_l2(a, b) < 1e-14
 
 
 def test_empty_leaves_and_clusters(cache_dir):
@@ -497,3 +504,20 @@ def test_grouped_near_field_matches(name, scale, cache_dir):
         out[mode] = (phi, ev.stages["near"].cpu().numpy())
         assert rel_l2(phi[wl["check_idx"]], g["phi_idx"]) < PHI_TOL
     assert rel_l2(out["grouped"][1], out["auto"][1]) < 1e-14
+
+
+@pytest.mark.parametrize("name,scale", [("C5", 2), ("C4", 2), ("C4", 3)])
+def test_tiled_near_field_bitwise_equals_untiled(name, scale, cache_dir):
+    """p2p_tile_kernel (sources of a 4 x 4 x 4 block's halo staged in shared
+    memory; clustered blocks over kTileCap points stream from global memory)
+    sums the same pairs in the same order as p2p_group_kernel: bitwise equal
+    near fields, for the uniform C5 and the clustered C4 (both paths)."""
+    wl = workloads.make(name, scale)
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
+    ev.keep_stages = True
+    near = {}
+    for mode in ("auto", "untiled"):
+        ev.near_mode = mode
+        ev.evaluate(wl["points"], weights=wl["weights"])
+        near[mode] = ev.stages["near"].cpu().numpy()
+    assert np.array_equal(near["auto"], near["untiled"])

@@ -258,6 +258,13 @@ class ThreadComm:
                 return full
         return self.allgather_cells(full, row_elems, level, shards)
 
+    def allreduce_max(self, t):
+        self._publish(t.clone())
+        m = torch.stack([self.board[r] for r in range(self.world)]).amax(dim=0)
+        self._done()
+        t.copy_(m)
+        return t
+
     def allgather_rows(self, mine, counts):
         self._publish(mine.clone())
         out = torch.cat([self.board[r] for r in range(self.world)])
