@@ -535,6 +535,28 @@ def measure(cfg, args, rank, world, local_rank, dist, lib, peaks, steps, warmup,
     return out
 
 
+def p2p_roofline(wl, ms, near_pairs, m, peaks):
+    """The near-field kernel against the FP64 (DFMA) peak: frozen FP64 flops
+    per (target, source) pair of the config's kernel functor."""
+    fpp = P2P_FLOPS_PER_PAIR.get(wl["kernel"])
+    pairs = near_pairs * m
+    roof = {"kernel": "p2p near field (p2p_tile_kernel / p2p_kernel, FP64 pipe)", "bound": "fp64",
+            "pair_interactions": pairs, "pairs_per_s": pairs / (ms * 1e-3),
+            "flops_per_pair": fpp, "pair": f"(target, source) pair, all {m} column(s)"}
+    if fpp is not None:
+        ach = near_pairs * fpp / (ms * 1e-3) / 1e12
+        ex = near_pairs * P2P_EXECUTED_PER_PAIR[wl["kernel"]] / (ms * 1e-3) / 1e12
+        roof.update({"achieved": ach, "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
+                     "frac": ach / peaks["dfma_tflops"],
+                     "frac_of_nominal_37.2": ach / NOMINAL_FP64_TF,
+                     "executed_flops_per_pair": P2P_EXECUTED_PER_PAIR[wl["kernel"]],
+                     "frac_executed": ex / peaks["dfma_tflops"],
+                     "peak_source": "measured live: DFMA microbenchmark "
+                                    "(bfmm_device_fp64_probe); MEASURED_PEAKS.json has no "
+                                    "FP64 entry"})
+    return roof
+
+
 def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms, share=1.0):
     """roofline of the dominant kernel + per-level M2L figures.  share: the
     fraction of every level's (and the near field's) work one rank does
@@ -587,28 +609,20 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms, share=1.0):
             levels[k] = {"ms": round(v, 4), "hadamard_tflops": tf,
                          "frac_dfma_peak": tf / peaks["dfma_tflops"],
                          "traffic": committed_traffic(cfg, k)}
-    dom = max(avg, key=avg.get) if avg else None
+    # roofline kernels: the near field and the M2L levels (the other spans --
+    # p2m, m2m, projections, l2l, l2p -- are reported in kernels_ms only)
+    cand = [k for k in avg if k == "p2p" or k.startswith("m2l")]
+    dom = max(cand, key=avg.get) if cand else None
     if dom is None:
         return None, levels
+    if dom != "p2p" and "p2p" in avg:
+        # the near field's own roofline beside the dominant M2L's
+        levels["p2p"] = p2p_roofline(wl, avg["p2p"], near_pairs, m, peaks)
+        levels["p2p"].update({"kernel_ms": avg["p2p"], "share_of_step": avg["p2p"] / step_ms})
     ms = avg[dom]
     share = ms / step_ms
     if dom == "p2p":
-        fpp = P2P_FLOPS_PER_PAIR.get(wl["kernel"])
-        pairs = near_pairs * m
-        roof = {"kernel": "p2p_kernel (near field, FP64 pipe)", "bound": "fp64",
-                "pair_interactions": pairs, "pairs_per_s": pairs / (ms * 1e-3),
-                "flops_per_pair": fpp, "pair": f"(target, source) pair, all {m} column(s)"}
-        if fpp is not None:
-            ach = near_pairs * fpp / (ms * 1e-3) / 1e12
-            ex = near_pairs * P2P_EXECUTED_PER_PAIR[wl["kernel"]] / (ms * 1e-3) / 1e12
-            roof.update({"achieved": ach, "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
-                         "frac": ach / peaks["dfma_tflops"],
-                         "frac_of_nominal_37.2": ach / NOMINAL_FP64_TF,
-                         "executed_flops_per_pair": P2P_EXECUTED_PER_PAIR[wl["kernel"]],
-                         "frac_executed": ex / peaks["dfma_tflops"],
-                         "peak_source": "measured live: DFMA microbenchmark "
-                                        "(bfmm_device_fp64_probe); MEASURED_PEAKS.json has no "
-                                        "FP64 entry"})
+        roof = p2p_roofline(wl, ms, near_pairs, m, peaks)
     elif dom.startswith("m2lfft_l"):
         rec = levels[dom]
         roof = {"kernel": f"uniform FFT M2L level {dom.split('_l')[1]} (fft_fwd + stencil + "
@@ -702,7 +716,8 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": "points/s", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
-    ev_m2l = res["m2l"]
+    ev_m2l = dict(res["m2l"] or {})
+    p2p_roof = ev_m2l.pop("p2p", None)
     line = {
         "metric": METRIC, "value": res["value"], "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["step_ms"],
@@ -714,7 +729,7 @@ def run_ours(args, rank, world, local_rank):
                    "near_field": "own stream, overlaps kernel tails",
                    "parallelism": f"dp{world}: Morton-range target shards" if world > 1
                    else "single GPU"},
-        "roofline": res["roofline"], "cpu_baseline": cpu,
+        "roofline": res["roofline"], "p2p_roofline": p2p_roof, "cpu_baseline": cpu,
         "e2e": res["e2e"], "e2e_numpy": res["e2e_numpy"],
         "gpu_launches": int(res["launches"]), "clocks": res["clocks"],
         "stages_ms": res["stages_ms"], "stages_serial_ms": res["stages_serial_ms"],

@@ -262,6 +262,28 @@ int bfmm_l2p_points(const double *pts4, int m, const int64_t *leaves,
                     const double *locals, double *phi_sorted, int32_t *ref_flag,
                     bfmm_stream_t stream);
 
+/* Leaf-pair P2M / L2P for sparse clouds, one weight column, levels >= 3,
+ * 2 <= p <= 8 (replaces engine.py:176-204 at the leaf level and
+ * :296-327 below level L-1).  A warp per parent cell q of level L-1 and its
+ * eight leaf children, whose points are contiguous in sorted order; the cell
+ * range [cell_lo, cell_hi) of geom (whole parents) is the shard.
+ *  - bfmm_p2m_pair: mom_leaf[c] (level L, every cell of the range, zeros for
+ *    empty ones -- as bfmm_p2m_cells) and mom_parent[q] (level L-1) straight
+ *    from the points with the parent's basis, i.e. M2M(M_L) exactly in exact
+ *    arithmetic: the caller skips the L -> L-1 M2M.
+ *  - bfmm_l2p_pair: phi_i = S_L(x_i) . loc_leaf[c] + S_{L-1}(x_i) .
+ *    loc_parent[q], where loc_leaf holds the level-L M2L locals WITHOUT the
+ *    parent's L2L part (which the second term supplies exactly): the caller
+ *    skips the L-1 -> L L2L. */
+int bfmm_p2m_pair(const double *pts4, const double *wsorted, const int32_t *cell_start,
+                  const int32_t *cell_count, int levels, int p, int scheme,
+                  const double *interp, const double *geom, double *mom_leaf,
+                  double *mom_parent, int32_t *ref_flag, bfmm_stream_t stream);
+int bfmm_l2p_pair(const double *pts4, const int32_t *cell_start, const int32_t *cell_count,
+                  int levels, int p, int scheme, const double *interp, const double *geom,
+                  const double *loc_leaf, const double *loc_parent, double *phi_sorted,
+                  int32_t *ref_flag, bfmm_stream_t stream);
+
 /* ---- near field (engine.py:349-478) ------------------------------------ */
 
 /* Compile (NVRTC, cached by source) a P2P kernel for a device functor.

@@ -32,6 +32,8 @@ SIGNATURES = {
     "bfmm_p2m": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_p2m_cells": (_I, [_P, _P, _I, _P, _P, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_l2p_cells": (_I, [_P, _I, _P, _P, _I, _I, _I, _DP, _DP, _P, _P, _P, _P]),
+    "bfmm_p2m_pair": (_I, [_P, _P, _P, _P, _I, _I, _I, _DP, _DP, _P, _P, _P, _P]),
+    "bfmm_l2p_pair": (_I, [_P, _P, _P, _I, _I, _I, _DP, _DP, _P, _P, _P, _P, _P]),
     "bfmm_p2m_sparse": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _DP, _DP, _P, _P, _P]),
     "bfmm_m2m": (_I, [_P, _P, _I64, _I, _I, _DP, _P]),
     "bfmm_rows_gemm": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P]),

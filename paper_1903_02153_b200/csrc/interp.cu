@@ -492,6 +492,43 @@ extern "C" int bfmm_l2p_cells(const double *pts4, int m, const int32_t *cell_sta
   return dispatch_l2p_cells(p, a, cell_start, cell_count);
 }
 
+static bool pair_args_ok(const char *what, int p, int levels, const LeafGeom &g) {
+  if (p < 2 || p > 8 || levels < 3) {
+    set_error("%s: unsupported p=%d levels=%d", what, p, levels);
+    return false;
+  }
+  if (g.cell_lo < 0 || g.cell_hi > (int64_t(1) << (3 * levels)) || g.cell_lo > g.cell_hi ||
+      g.cell_lo % 8 || g.cell_hi % 8) {
+    set_error("%s: cell range [%lld, %lld) not whole parents of level %d", what,
+              (long long)g.cell_lo, (long long)g.cell_hi, levels);
+    return false;
+  }
+  return true;
+}
+
+extern "C" int bfmm_p2m_pair(const double *pts4, const double *wsorted, const int32_t *cell_start,
+                             const int32_t *cell_count, int levels, int p, int scheme,
+                             const double *interp, const double *geom, double *mom_leaf,
+                             double *mom_parent, int32_t *ref_flag, bfmm_stream_t stream) {
+  const LeafGeom g = make_leaf_geom(geom);
+  if (!pair_args_ok("bfmm_p2m_pair", p, levels, g)) return 2;
+  LeafCall a{pts4, wsorted, 1, nullptr, nullptr, nullptr, nullptr, 0, levels, false,
+             make_interp(p, scheme, interp), g, nullptr, mom_leaf, ref_flag, as_stream(stream)};
+  return dispatch_p2m_pair(p, a, cell_start, cell_count, mom_parent);
+}
+
+extern "C" int bfmm_l2p_pair(const double *pts4, const int32_t *cell_start,
+                             const int32_t *cell_count, int levels, int p, int scheme,
+                             const double *interp, const double *geom, const double *loc_leaf,
+                             const double *loc_parent, double *phi_sorted, int32_t *ref_flag,
+                             bfmm_stream_t stream) {
+  const LeafGeom g = make_leaf_geom(geom);
+  if (!pair_args_ok("bfmm_l2p_pair", p, levels, g)) return 2;
+  LeafCall a{pts4, nullptr, 1, nullptr, nullptr, nullptr, nullptr, 0, levels, true,
+             make_interp(p, scheme, interp), g, loc_leaf, phi_sorted, ref_flag, as_stream(stream)};
+  return dispatch_l2p_pair(p, a, cell_start, cell_count, loc_parent);
+}
+
 extern "C" int bfmm_p2m_sparse(const double *pts4, const double *wsorted, int m,
                                const int64_t *leaves, const int64_t *starts,
                                const int64_t *counts, const int64_t *n_leaves,

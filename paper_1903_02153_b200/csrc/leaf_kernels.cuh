@@ -640,3 +640,265 @@ inline int dispatch_leaf(int p, bool p2m, const LeafCall &a) {
     default: return launch_leaf<8>(p2m, a);
   }
 }
+
+// ---------------------------------------------------------------------------
+// Leaf "pair" kernels for sparse clouds (one weight column): a warp owns one
+// parent cell q of level L-1 and its eight leaf children 8q .. 8q+7 (whose
+// points are contiguous in sorted order).
+//
+// p2m_pair_kernel writes the leaf moments of the eight children (as
+// p2m_cells_kernel: the same products in sorted order, zeros for empty
+// cells) AND the parent's moments straight from the points,
+//   M_{L-1}[q] = sum_{i in q} S_{L-1}(x_i) w_i,
+// which is M2M(M_L) exactly in exact arithmetic (the child's Chebyshev
+// interpolant of the parent basis polynomial is the polynomial itself, the
+// identity behind engine.py:187-204), so the level-L -> L-1 M2M pass and its
+// 16.8 GB (C5) re-read of the leaf moments disappear.
+//
+// l2p_pair_kernel evaluates phi_i = S_L(x_i) . loc_L[c] + S_{L-1}(x_i) .
+// loc_{L-1}[q] where loc_L holds ONLY the level-L M2L locals: the parent's
+// contribution L2L(loc_{L-1}) interpolated at x_i equals the parent's own
+// expansion at x_i (same identity, engine.py:296-311 then :315-327), so
+// the L-1 -> L L2L pass (a read-modify-write of the leaf locals) disappears.
+template <int P>
+constexpr int pair_warps() { return P <= 6 ? 4 : 2; }
+template <int P>
+constexpr int pair_minb() { return P == 5 ? 4 : 2; }  // <= 128 registers for C5 (p = 5)
+template <int P>
+constexpr int pair_batch() { return P <= 6 ? 64 : 32; }  // points staged per pass
+template <int P>
+constexpr size_t p2m_pair_smem() {
+  return sizeof(double) * pair_warps<P>() * pair_batch<P>() * (6 * P + 1);
+}
+template <int P>
+constexpr size_t l2p_pair_smem() {
+  return sizeof(double) * pair_warps<P>() * 9 * P * P * P;
+}
+
+// the eight children's counts of parent q: lanes < 8 hold child lane's
+// count; returns the inclusive prefix (lanes < 8) and the first point
+__device__ __forceinline__ int pair_scan(const int32_t *cell_start, const int32_t *cell_count,
+                                         int64_t q, int lane, int &total, int64_t &first) {
+  const int cnt = lane < 8 ? cell_count[8 * q + lane] : 0;
+  int inc = cnt;
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += v;
+  }
+  total = __shfl_sync(0xffffffffu, inc, 7);
+  const unsigned occ = __ballot_sync(0xffffffffu, lane < 8 && cnt > 0);
+  const int fl = occ ? __ffs(occ) - 1 : 0;
+  const int st = lane < 8 && lane == fl && occ ? cell_start[8 * q + lane] : 0;
+  first = (int64_t)__shfl_sync(0xffffffffu, st, fl);
+  return inc;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * pair_warps<P>(), pair_minb<P>())
+p2m_pair_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
+                const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_count,
+                Interp ip, LeafGeom g, double *__restrict__ mom_leaf,
+                double *__restrict__ mom_par, int32_t *flag) {
+  constexpr int P3 = P * P * P, B = pair_batch<P>(), W = pair_warps<P>(), R = 6 * P + 1;
+  extern __shared__ double s_pair[];
+  __shared__ double sS[P * P], sN[P];
+  __shared__ int s_off[W][9];
+  stage_basis<P>(ip, sS, sN);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *sw = s_pair + (size_t)wid * B * R;  // [B][R]: w_L (3P), w_{L-1} (3P), weight
+  const double inv_hw = 1.0 / g.hw, inv_hp = 1.0 / g.h, hp = 2.0 * g.h;
+  const int64_t q_lo = g.cell_lo / 8, q_hi = (g.cell_hi + 7) / 8;
+  for (int64_t q = q_lo + int64_t(blockIdx.x) * W + wid; q < q_hi; q += int64_t(gridDim.x) * W) {
+    int total;
+    int64_t first;
+    __syncwarp();  // the previous parent's readers of s_off / sw are done
+    const int inc = pair_scan(cell_start, cell_count, q, lane, total, first);
+    if (lane < 8) s_off[wid][lane + 1] = inc;
+    if (lane == 0) s_off[wid][0] = 0;
+    __syncwarp();
+    int px, py, pz;
+    unmorton3((uint64_t)q, px, py, pz);
+    for (int b0 = 0; b0 < max(total, 1); b0 += B) {
+      const int nb = min(B, total - b0);
+      __syncwarp();
+      for (int t = lane; t < nb; t += 32) {
+        const int e = b0 + t;
+        int ch = 0;
+#pragma unroll
+        for (int k = 1; k < 8; ++k) ch += s_off[wid][k] <= e ? 1 : 0;
+        const int64_t i = first + e;
+        const double4 x = reinterpret_cast<const double4 *>(pts4)[i];
+        const int cx = 2 * px + ((ch >> 2) & 1), cy = 2 * py + ((ch >> 1) & 1),
+                  cz = 2 * pz + (ch & 1);
+        double *row = sw + t * R;
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], g.h, inv_hw, cx, flag), row);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], g.h, inv_hw, cy, flag), row + P);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], g.h, inv_hw, cz, flag),
+                     row + 2 * P);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], hp, inv_hp, px, flag), row + 3 * P);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], hp, inv_hp, py, flag), row + 4 * P);
+        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], hp, inv_hp, pz, flag), row + 5 * P);
+        row[6 * P] = ws[i];
+      }
+      __syncwarp();
+      // the eight children's moments, consecutive outputs on consecutive lanes
+      double *leaf = mom_leaf + 8 * q * (int64_t)P3;
+      for (int o = lane; o < 8 * P3; o += 32) {
+        const int ch = o / P3, a = o - ch * P3;
+        const int ii = a / (P * P), jj = (a / P) % P, kk = a % P;
+        const int p0 = max(s_off[wid][ch], b0), p1 = min(s_off[wid][ch + 1], b0 + nb);
+        double acc = 0.0;
+        for (int pt = p0; pt < p1; ++pt) {
+          const double *wt = sw + (pt - b0) * R;
+          acc += ((wt[ii] * wt[P + jj]) * wt[2 * P + kk]) * wt[6 * P];
+        }
+        leaf[o] = b0 == 0 ? acc : leaf[o] + acc;
+      }
+      // the parent's moments from the same points
+      double *par = mom_par + q * (int64_t)P3;
+      for (int a = lane; a < P3; a += 32) {
+        const int ii = a / (P * P), jj = (a / P) % P, kk = a % P;
+        double acc = 0.0;
+        for (int pt = 0; pt < nb; ++pt) {
+          const double *wt = sw + pt * R + 3 * P;
+          acc += ((wt[ii] * wt[P + jj]) * wt[2 * P + kk]) * wt[3 * P];
+        }
+        par[a] = b0 == 0 ? acc : par[a] + acc;
+      }
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ double l2p_contract(const double *wx, const double *wy,
+                                               const double *wz, const double *L) {
+  double sa[P];
+#pragma unroll
+  for (int a = 0; a < P; ++a) {
+    sa[a] = 0.0;
+#pragma unroll
+    for (int b = 0; b < P; ++b) {
+      const double *Lab = L + (a * P + b) * P;
+      double sb = 0.0;
+#pragma unroll
+      for (int k = 0; k < P; ++k) sb = fma(wz[k], Lab[k], sb);
+      sa[a] = fma(wx[a] * wy[b], sb, sa[a]);
+    }
+  }
+  double s = sa[0];
+#pragma unroll
+  for (int a = 1; a < P; ++a) s += sa[a];
+  return s;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * pair_warps<P>(), pair_minb<P>())
+l2p_pair_kernel(const double *__restrict__ pts4, const int32_t *__restrict__ cell_start,
+                const int32_t *__restrict__ cell_count, Interp ip, LeafGeom g,
+                const double *__restrict__ loc_leaf, const double *__restrict__ loc_par,
+                double *__restrict__ phi, int32_t *flag) {
+  constexpr int P3 = P * P * P, W = pair_warps<P>();
+  extern __shared__ double s_pair[];
+  __shared__ double sS[P * P], sN[P];
+  __shared__ int s_off[W][9];
+  stage_basis<P>(ip, sS, sN);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *sl = s_pair + (size_t)wid * 9 * P3;  // 8 children's locals, then the parent's
+  const double inv_hw = 1.0 / g.hw, inv_hp = 1.0 / g.h, hp = 2.0 * g.h;
+  const int64_t q_lo = g.cell_lo / 8, q_hi = (g.cell_hi + 7) / 8;
+  for (int64_t q = q_lo + int64_t(blockIdx.x) * W + wid; q < q_hi; q += int64_t(gridDim.x) * W) {
+    int total;
+    int64_t first;
+    const int inc = pair_scan(cell_start, cell_count, q, lane, total, first);
+    if (total == 0) continue;  // warp-uniform
+    __syncwarp();
+    if (lane < 8) s_off[wid][lane + 1] = inc;
+    if (lane == 0) s_off[wid][0] = 0;
+    const double *src = loc_leaf + 8 * q * (int64_t)P3;
+    for (int e = lane; e < 8 * P3; e += 32) sl[e] = src[e];
+    const double *srp = loc_par + q * (int64_t)P3;
+    for (int e = lane; e < P3; e += 32) sl[8 * P3 + e] = srp[e];
+    __syncwarp();
+    int px, py, pz;
+    unmorton3((uint64_t)q, px, py, pz);
+    for (int t = lane; t < total; t += 32) {
+      int ch = 0;
+#pragma unroll
+      for (int k = 1; k < 8; ++k) ch += s_off[wid][k] <= t ? 1 : 0;
+      const int64_t i = first + t;
+      const double4 x = reinterpret_cast<const double4 *>(pts4)[i];
+      const int cx = 2 * px + ((ch >> 2) & 1), cy = 2 * py + ((ch >> 1) & 1),
+                cz = 2 * pz + (ch & 1);
+      double wx[P], wy[P], wz[P];
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], g.h, inv_hw, cx, flag), wx);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], g.h, inv_hw, cy, flag), wy);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], g.h, inv_hw, cz, flag), wz);
+      const double s_leaf = l2p_contract<P>(wx, wy, wz, sl + ch * P3);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], hp, inv_hp, px, flag), wx);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], hp, inv_hp, py, flag), wy);
+      weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], hp, inv_hp, pz, flag), wz);
+      phi[i] = s_leaf + l2p_contract<P>(wx, wy, wz, sl + 8 * P3);
+    }
+    __syncwarp();
+  }
+}
+
+template <int P>
+int launch_p2m_pair(const LeafCall &a, const int32_t *cs, const int32_t *cc, double *mom_par) {
+  constexpr size_t smem = p2m_pair_smem<P>();
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr) && smem > 48 * 1024)
+    cudaFuncSetAttribute(p2m_pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int64_t parents = (a.g.cell_hi + 7) / 8 - a.g.cell_lo / 8;
+  if (parents <= 0) return 0;
+  const unsigned grid =
+      (unsigned)std::min<int64_t>(ceil_div(parents, pair_warps<P>()), (int64_t)kNumSMs * 16);
+  p2m_pair_kernel<P><<<grid, 32 * pair_warps<P>(), smem, a.st>>>(a.pts4, a.ws, cs, cc, a.ip, a.g,
+                                                                  a.out, mom_par, a.flag);
+  return check_launch("p2m_pair_kernel");
+}
+
+template <int P>
+int launch_l2p_pair(const LeafCall &a, const int32_t *cs, const int32_t *cc,
+                    const double *loc_par) {
+  constexpr size_t smem = l2p_pair_smem<P>();
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr) && smem > 48 * 1024)
+    cudaFuncSetAttribute(l2p_pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int64_t parents = (a.g.cell_hi + 7) / 8 - a.g.cell_lo / 8;
+  if (parents <= 0) return 0;
+  const unsigned grid =
+      (unsigned)std::min<int64_t>(ceil_div(parents, pair_warps<P>()), (int64_t)kNumSMs * 16);
+  l2p_pair_kernel<P><<<grid, 32 * pair_warps<P>(), smem, a.st>>>(a.pts4, cs, cc, a.ip, a.g,
+                                                                  a.locals, loc_par, a.out, a.flag);
+  return check_launch("l2p_pair_kernel");
+}
+
+inline int dispatch_p2m_pair(int p, const LeafCall &a, const int32_t *cs, const int32_t *cc,
+                             double *mom_par) {
+  switch (p) {
+    case 2: return launch_p2m_pair<2>(a, cs, cc, mom_par);
+    case 3: return launch_p2m_pair<3>(a, cs, cc, mom_par);
+    case 4: return launch_p2m_pair<4>(a, cs, cc, mom_par);
+    case 5: return launch_p2m_pair<5>(a, cs, cc, mom_par);
+    case 6: return launch_p2m_pair<6>(a, cs, cc, mom_par);
+    case 7: return launch_p2m_pair<7>(a, cs, cc, mom_par);
+    default: return launch_p2m_pair<8>(a, cs, cc, mom_par);
+  }
+}
+
+inline int dispatch_l2p_pair(int p, const LeafCall &a, const int32_t *cs, const int32_t *cc,
+                             const double *loc_par) {
+  switch (p) {
+    case 2: return launch_l2p_pair<2>(a, cs, cc, loc_par);
+    case 3: return launch_l2p_pair<3>(a, cs, cc, loc_par);
+    case 4: return launch_l2p_pair<4>(a, cs, cc, loc_par);
+    case 5: return launch_l2p_pair<5>(a, cs, cc, loc_par);
+    case 6: return launch_l2p_pair<6>(a, cs, cc, loc_par);
+    case 7: return launch_l2p_pair<7>(a, cs, cc, loc_par);
+    default: return launch_l2p_pair<8>(a, cs, cc, loc_par);
+  }
+}

@@ -274,6 +274,111 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
   }
 }
 
+// ---- 2b. the same stencil with two x targets per thread ----------------------
+// Tile 16 x 8 x 8: thread (ix4, iy, pz) of (x, y) parity class w owns the
+// targets x_a = x0 + px + 4 ix4 and x_a + 2 (same parity), y = y0 + iy, and
+// z = z0 + pz + 2k.  A source x-column x_a + alpha, alpha' = alpha + px in
+// [-2, 5], serves target x_a with tap a = alpha (alpha' <= 3) and target
+// x_a + 2 with tap alpha - 2 (alpha' >= 0): 8 column loads per (b, 2
+// targets) instead of 12, the shared-memory operand traffic that bounds
+// stencil_kernel (ncu: FP64 pipe ~55 %, LSU busy).  Same taps, same
+// per-target accumulation order (a, b, c ascending) as stencil_kernel:
+// bitwise-equal spectra.
+constexpr int kT2X = 16, kH2X = kT2X + 6;
+// lanes: bit 0 = pz (halo z stride 1), bits 1-2 = same-parity y (stride
+// 2 * HZP = 30 = 6 mod 8), bits 3-4 = x pair index: an 8-lane LDS.128 phase
+// (pz, y) covers 16-byte slots {0,1,6,7,4,5,2,3} (mod 8) -- conflict-free.
+__global__ void __launch_bounds__(128, 2)
+stencil2_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level, int F,
+                const double2 *__restrict__ S, const short *__restrict__ tap_index,
+                int64_t cell_lo, int64_t cell_hi) {
+  extern __shared__ double2 sm2[];
+  auto halo = reinterpret_cast<double2 (*)[kHYP][kHZP]>(sm2);                    // [kH2X][kHYP][kHZP]
+  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kH2X * kHYP * kHZP);    // [7][7][7]
+  const int n = 1 << level;
+  const int64_t ncell = int64_t(1) << (3 * level);
+  const int tilesx = (n + kT2X - 1) / kT2X, tilesy = (n + kTY - 1) / kTY;
+  const int tile = blockIdx.x;
+  const int tz = tile / (tilesx * tilesy), trem = tile - tz * tilesx * tilesy;
+  const int x0 = (trem / tilesy) * kT2X, y0 = (trem % tilesy) * kTY, z0 = tz * kTZ;
+  const int f = blockIdx.y, col = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int px = w >> 1, py = w & 1;
+  const int pz = lane & 1, iy = py + 2 * ((lane >> 1) & 3), ix4 = (lane >> 3) & 3;
+  const int xa = x0 + px + 4 * ix4, y = y0 + iy;
+  bool mine = false;
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+      const int x = xa + 2 * u, z = z0 + pz + 2 * k;
+      if (x < n && y < n && z < n) {
+        const int64_t id = (int64_t)morton3(x, y, z);
+        mine |= id >= cell_lo && id < cell_hi;
+      }
+    }
+  if (!__syncthreads_or(mine)) return;
+  const double2 *Xf = X + ((int64_t)col * F + f) * ncell;
+  for (int e = tid; e < kH2X * kHY * kHZ; e += 128) {
+    const int hx = e / (kHY * kHZ), hr = e - hx * kHY * kHZ, hy = hr / kHZ, hz = hr - hy * kHZ;
+    const int sx = x0 + hx - 3, sy = y0 + hy - 3, sz = z0 + hz - 3;
+    double2 v = make_double2(0.0, 0.0);
+    if (sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n) v = Xf[lex_of(sx, sy, sz, n)];
+    halo[hx][hy][hz] = v;
+  }
+  for (int e = tid; e < 343; e += 128) {
+    const int t = tap_index[e];
+    (&taps[0][0][0])[e] = t >= 0 ? S[(int64_t)t * F + f] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 acc[2][kR];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int k = 0; k < kR; ++k) acc[u][k] = make_double2(0.0, 0.0);
+  const int hx0 = px + 4 * ix4 + 3;  // halo x of target x_a
+  // target x_a takes a = alpha' - px for alpha' in [-2, 3], target x_a + 2
+  // a = alpha' - 2 - px for alpha' in [0, 5]; with b inside alpha' each
+  // target sees its (a, b, c) taps in stencil_kernel's order
+#pragma unroll
+  for (int ap = -2; ap <= 5; ++ap) {
+#pragma unroll 2
+    for (int bp = -2; bp <= 3; ++bp) {
+      const int b = bp - py;
+      double2 seg[2 * kR + 4];
+      const double2 *col_src = &halo[hx0 + ap - px][iy + 3 + b][1];  // source z0 - 2
+#pragma unroll
+      for (int uu = 0; uu < 2 * kR + 4; ++uu) seg[uu] = col_src[uu];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if ((u == 0 && ap > 3) || (u == 1 && ap < 0)) continue;  // compile-time
+        const int a = ap - px - 2 * u;
+        const double2 *tp = &taps[a + 3][b + 3][3 - pz];
+        const bool near_col = a >= -1 && a <= 1 && b >= -1 && b <= 1;  // warp-uniform
+#pragma unroll
+        for (int cp = -2; cp <= 3; ++cp) {
+          if (near_col && (cp == 0 || cp == 1)) continue;
+          const double2 s = tp[cp];
+#pragma unroll
+          for (int k = 0; k < kR; ++k) {
+            const double2 v = seg[cp + 2 + 2 * k];
+            acc[u][k].x = fma(s.x, v.x, fma(-s.y, v.y, acc[u][k].x));
+            acc[u][k].y = fma(s.x, v.y, fma(s.y, v.x, acc[u][k].y));
+          }
+        }
+      }
+    }
+  }
+  double2 *Yf = Y + ((int64_t)col * F + f) * ncell;
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+      const int x = xa + 2 * u, z = z0 + pz + 2 * k;
+      if (x < n && y < n && z < n) Yf[lex_of(x, y, z, n)] = acc[u][k];
+    }
+}
+
 // ---- 3. inverse transform + crop + scale ------------------------------------
 template <int P, int G>
 __global__ void __launch_bounds__(128)
@@ -475,10 +580,17 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const int n = 1 << level;
   const unsigned tiles = (unsigned)(ceil_div(n, kTX) * ceil_div(n, kTY) * ceil_div(n, kTZ));
   const size_t smem_s = sizeof(double2) * (kHX * kHYP * kHZP + 343);
+  const size_t smem_s2 = sizeof(double2) * (kH2X * kHYP * kHZP + 343);
+  const unsigned tiles2 = (unsigned)(ceil_div(n, kT2X) * ceil_div(n, kTY) * ceil_div(n, kTZ));
+  // BFMM_STENCIL=1 (diagnostic): the one-x-target-per-thread kernel
+  const char *sv = getenv("BFMM_STENCIL");
+  const bool stencil1 = sv && sv[0] == '1';
   static unsigned long long attr = 0;
   if (first_on_device(&attr)) {
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_s);
+    cudaFuncSetAttribute(stencil2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_s2);
   }
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
@@ -495,10 +607,17 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
 #undef BFMM_FFT_FWD
     }
     if (rc) return rc;
-    stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
-        X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
-        8 * (q_lo + nq));
-    if (check_launch("stencil_kernel")) return 1;
+    if (stencil1) {
+      stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
+          X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
+          8 * (q_lo + nq));
+      if (check_launch("stencil_kernel")) return 1;
+    } else {
+      stencil2_kernel<<<dim3(tiles2, (unsigned)F, (unsigned)ccur), 128, smem_s2, st>>>(
+          X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
+          8 * (q_lo + nq));
+      if (check_launch("stencil2_kernel")) return 1;
+    }
     switch (p) {
 #define BFMM_FFT_INV(PP)                                                                       \
   case PP:                                                                                     \

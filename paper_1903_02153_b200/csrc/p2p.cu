@@ -124,6 +124,7 @@ struct JitKernel {
   CUfunction block;
   CUfunction group;
   CUfunction tile;
+  CUfunction tile1;
 };
 
 std::mutex g_jit_mu;
@@ -184,7 +185,8 @@ int jit_compile(int kind, const char *expr, int *handle) {
   names.push_back("bfmm_nf::direct_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::pair_block_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::p2p_group_kernel<bfmm_nf::KUser>");
-  names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser>");
+  names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser, 0>");
+  names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser, 1>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--std=c++17",
                                     "-default-device", "-lineinfo"};
@@ -235,7 +237,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 11; ++i) {
+  for (int i = 0; i < 12; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
@@ -247,7 +249,8 @@ int jit_compile(int kind, const char *expr, int *handle) {
     else if (i == 7) jk.direct = f;
     else if (i == 8) jk.block = f;
     else if (i == 9) jk.group = f;
-    else jk.tile = f;
+    else if (i == 10) jk.tile = f;
+    else jk.tile1 = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -632,6 +635,10 @@ static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_sta
                        const int32_t *scell_start, const int32_t *scell_count, int levels,
                        int64_t cell_lo, int64_t cell_hi, int small_max, double *out,
                        cudaStream_t st) {
+  // BFMM_TILE_MODE=0 (diagnostic): one thread per target (bitwise equal to
+  // p2p_group_kernel); default 1: a warp per target cell
+  const char *tm = getenv("BFMM_TILE_MODE");
+  const int mode = (tm && tm[0] == '0') ? 0 : 1;
   bfmm_nf::Args a = make_args(tpts4, nullptr, nullptr, nullptr, nullptr, spts4, nullptr, 1,
                                scell_start, scell_count, levels, out, nullptr);
   const int64_t tiles = ceil_div(cell_hi, 64) - cell_lo / 64;
@@ -643,12 +650,16 @@ static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_sta
   long long lo = cell_lo, hi = cell_hi;
   int sm = small_max;
   const int *cs = tcell_start, *cc = tcell_count;
+#define BFMM_TILE(KK)                                                                     \
+  (mode == 1 ? (bfmm_nf::p2p_tile_kernel<KK, 1><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm)) \
+             : (bfmm_nf::p2p_tile_kernel<KK, 0><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm)))
   switch (handle) {
-    case 1: bfmm_nf::p2p_tile_kernel<KLaplace><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
-    case 2: bfmm_nf::p2p_tile_kernel<KLaplaceForce><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
-    case 3: bfmm_nf::p2p_tile_kernel<KGaussian><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
-    case 4: bfmm_nf::p2p_tile_kernel<KExponential><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
-    case 5: bfmm_nf::p2p_tile_kernel<KLogarithm><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm); break;
+    case 1: BFMM_TILE(KLaplace); break;
+    case 2: BFMM_TILE(KLaplaceForce); break;
+    case 3: BFMM_TILE(KGaussian); break;
+    case 4: BFMM_TILE(KExponential); break;
+    case 5: BFMM_TILE(KLogarithm); break;
+#undef BFMM_TILE
     default: {
       JitKernel jk;
       {
@@ -660,7 +671,7 @@ static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_sta
         jk = g_jit[handle - kFirstJit];
       }
       void *params[] = {&a, &cs, &cc, &lo, &hi, &sm};
-      if (driver().LaunchKernel(jk.tile, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
+      if (driver().LaunchKernel(mode == 1 ? jk.tile1 : jk.tile, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
                                 nullptr) != CUDA_SUCCESS) {
         set_error("p2p_tile_kernel: cuLaunchKernel failed");
         return 1;

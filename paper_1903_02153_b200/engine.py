@@ -236,6 +236,10 @@ class FmmEvaluator:
         # P2M: warp per leaf ("leaf"), leaf-cell chunks ("cells"), or "auto"
         # (cells for sparse clouds, see _p2m_cells)
         self.p2m_mode = "auto"
+        # sparse clouds, one column: leaf-pair P2M / L2P (bfmm_p2m_pair /
+        # bfmm_l2p_pair), which fold the L -> L-1 M2M and the L-1 -> L L2L
+        # into the leaf kernels ("auto"), or the separate passes ("plain")
+        self.leaf_mode = "auto"
         # coarse far-field levels on a side stream (see _far_field); the
         # finest main_levels levels stay on the calling stream
         self.stream_levels = True
@@ -544,7 +548,19 @@ class FmmEvaluator:
         leaf_geom = np.ascontiguousarray(np.concatenate(
             [self.plan.domain.low, [self.plan.domain.length / (1 << L), float(lo), float(hi)]]))
         ncell = (1 << (3 * L))
-        if self._p2m_cells(tree, p):
+        pair = self._leaf_pair(tree, m)
+        e0 = self._kevent()
+        if pair:
+            # leaf moments and the parents' moments straight from the points
+            alloc = torch.zeros if shard is not None else torch.empty
+            moments = {L: alloc((ncell * p3,), dtype=torch.float64, device=self.device),
+                       L - 1: alloc((ncell // 8 * p3,), dtype=torch.float64, device=self.device)}
+            _native.check(self.lib.bfmm_p2m_pair(
+                tree.pts4.data_ptr(), ws.data_ptr(), tree.cell_start.data_ptr(),
+                tree.cell_count.data_ptr(), L, p, self._scheme_id, _native.dptr(self._interp),
+                _native.dptr(leaf_geom), moments[L].data_ptr(), moments[L - 1].data_ptr(),
+                status[_ST_REF:].data_ptr(), st), "bfmm_p2m_pair")
+        elif self._p2m_cells(tree, p):
             # sparse cloud: P2M over leaf-cell chunks, which writes every
             # cell of [lo, hi) (zeros for empty ones) -- no memset
             alloc = torch.zeros if shard is not None else torch.empty
@@ -564,7 +580,9 @@ class FmmEvaluator:
                 tree.max_leaves, L, p, self._scheme_id, _native.dptr(self._interp),
                 _native.dptr(leaf_geom), moments[L].data_ptr(), status[_ST_REF:].data_ptr(), st),
                 "bfmm_p2m")
-        for lev in range(L, 2, -1):
+        self._kspan("p2m", e0)
+        e0 = self._kevent()
+        for lev in range(L - 1 if pair else L, 2, -1):
             npar = 1 << (3 * (lev - 1))
             qlo, qhi = self._cells(lev - 1, shard)  # parents of this shard's cells
             row = m * p3
@@ -575,7 +593,18 @@ class FmmEvaluator:
             _native.check(self.lib.bfmm_m2m(
                 moments[lev][8 * qlo * row:].data_ptr(), moments[lev - 1][qlo * row:].data_ptr(),
                 qhi - qlo, p, m, _native.dptr(self._H), st), "bfmm_m2m")
+        self._kspan("m2m", e0)
         return moments, leaf_geom
+
+    def _leaf_pair(self, tree, m):
+        """Leaf-pair P2M / L2P (leaf_mode): one weight column, a sparse cloud
+        (fewer than 8 points per leaf cell on average, the cells rule),
+        2 <= p <= 8, L >= 3; off while per-level stages are kept (the leaf
+        locals then hold only the level's own M2L part)."""
+        L, p = self.plan.levels, self.plan.order
+        if self.leaf_mode == "plain" or self.keep_stages or m != 1 or L < 3 or not 2 <= p <= 8:
+            return False
+        return self.leaf_mode == "pair" or tree.n < 8 * (1 << (3 * L))
 
     def _p2m_cells(self, tree, p):
         """P2M over leaf-cell chunks (bfmm_p2m_cells) for sparse clouds --
@@ -700,17 +729,21 @@ class FmmEvaluator:
             ns = self._m2l_splits(lev, m, rp, nq)
             z = zalloc((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
+            e0 = self._kevent()
             _native.check(self.lib.bfmm_rows_gemm(
                 moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
                 z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+            self._kspan(f"projv_l{lev}", e0)
             if shard is not None and not shard[0].full:
                 # the sources this shard's M2L reads: its halo (fine levels)
                 # or the whole level (coarse levels)
                 shard[1].exchange_level(z, m * rp, lev, shard[0])
             self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq, shard=shard)
+            e0 = self._kevent()
             _native.check(self.lib.bfmm_rows_gemm(
                 lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
                 out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
+            self._kspan(f"proju_l{lev}", e0)
         else:
             if shard is not None and not shard[0].full:
                 shard[1].exchange_level(moments[lev], m * p3, lev, shard[0])
@@ -734,12 +767,29 @@ class FmmEvaluator:
         L, p = self.plan.levels, self.plan.order
         st = self._stream()
         row = m * p ** 3
-        for lev in range(2, L):
+        pair = self._leaf_pair(tree, m)
+        e0 = self._kevent()
+        for lev in range(2, L - 1 if pair else L):
             qlo, qhi = self._cells(lev, shard)
             _native.check(self.lib.bfmm_l2l(locs[lev][qlo * row:].data_ptr(),
                                             locs[lev + 1][8 * qlo * row:].data_ptr(),
                                             qhi - qlo, p, m, _native.dptr(self._H), st),
                           "bfmm_l2l")
+        self._kspan("l2l", e0)
+        e0 = self._kevent()
+        self._l2p(locs, tree, m, leaf_geom, status, phi_far, pair, st)
+        self._kspan("l2p", e0)
+
+    def _l2p(self, locs, tree, m, leaf_geom, status, phi_far, pair, st):
+        L, p = self.plan.levels, self.plan.order
+        if pair:
+            # the parents' complete locals enter through their own basis
+            _native.check(self.lib.bfmm_l2p_pair(
+                tree.pts4.data_ptr(), tree.cell_start.data_ptr(), tree.cell_count.data_ptr(),
+                L, p, self._scheme_id, _native.dptr(self._interp), _native.dptr(leaf_geom),
+                locs[L].data_ptr(), locs[L - 1].data_ptr(), phi_far.data_ptr(),
+                status[_ST_REF:].data_ptr(), st), "bfmm_l2p_pair")
+            return
         # fewer than 8 points per leaf cell on average: leaf-cell chunks
         # with their locals staged in shared memory (or one thread per point)
         sparse_auto = self.l2p_mode == "auto" and tree.n < 8 * (1 << (3 * L))
@@ -1074,7 +1124,8 @@ class FmmEvaluator:
         # the sparse-cloud active lists read counts back on the host
         return self.far_mode == "dense" or (self.far_mode == "auto" and n >= 8 * (1 << (3 * L)))
 
-    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "i8_digits", "p2m_mode", "far_mode", "near_mode",
+    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "i8_digits", "p2m_mode", "leaf_mode", "far_mode",
+                    "near_mode",
                     "overlap_near",
                     "near_after_far", "far_priority", "l2p_mode", "stream_levels",
                     "main_levels")

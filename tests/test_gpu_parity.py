@@ -507,17 +507,62 @@ def test_grouped_near_field_matches(name, scale, cache_dir):
 
 
 @pytest.mark.parametrize("name,scale", [("C5", 2), ("C4", 2), ("C4", 3)])
-def test_tiled_near_field_bitwise_equals_untiled(name, scale, cache_dir):
+def test_tiled_near_field_bitwise_equals_untiled(name, scale, cache_dir, monkeypatch):
     """p2p_tile_kernel (sources of a 4 x 4 x 4 block's halo staged in shared
-    memory; clustered blocks over kTileCap points stream from global memory)
-    sums the same pairs in the same order as p2p_group_kernel: bitwise equal
-    near fields, for the uniform C5 and the clustered C4 (both paths)."""
+    memory; clustered blocks over kTileCap points stream from global memory):
+    its thread-per-target mode sums the same pairs in the same order as
+    p2p_group_kernel (bitwise equal near fields, uniform C5 and clustered C4,
+    both paths); the default warp-per-cell mode (lane partial sums, fixed
+    butterfly) agrees to rounding."""
     wl = workloads.make(name, scale)
     ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan_of(wl), cache_dir=cache_dir)
     ev.keep_stages = True
     near = {}
-    for mode in ("auto", "untiled"):
-        ev.near_mode = mode
+    for mode in ("auto", "untiled", "auto0"):
+        if mode == "auto0":
+            monkeypatch.setenv("BFMM_TILE_MODE", "0")
+        ev.near_mode = mode[:4] if mode == "auto0" else mode
         ev.evaluate(wl["points"], weights=wl["weights"])
         near[mode] = ev.stages["near"].cpu().numpy()
-    assert np.array_equal(near["auto"], near["untiled"])
+    assert np.array_equal(near["auto0"], near["untiled"])
+    assert rel_l2(near["auto"], near["untiled"]) < 1e-14
+
+
+@pytest.mark.parametrize("name,scale", [("C5", 2), ("C4", 2), ("uniform", 0)])
+def test_leaf_pair_matches_separate_passes(name, scale, cache_dir):
+    """Leaf-pair P2M / L2P (parent moments straight from the points, the
+    parent's locals evaluated through its own basis -- no L -> L-1 M2M and
+    no L-1 -> L L2L) against the separate passes, and against the reference
+    fixture where one exists (engine.py:176-204, 296-327)."""
+    if name == "uniform":
+        pts, w = unit_cloud(20000, seed=77)
+        w = w[:, 0]
+        plan = bf.FmmPlan(levels=5, order=4, scheme="uniform", eps=1e-6,
+                          domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+        kern, g = bf.EXPONENTIAL, None
+    else:
+        wl = workloads.make(name, scale)
+        pts, w, plan = wl["points"], wl["weights"], plan_of(wl)
+        kern, g = workload_kernel(wl["kernel"]), golden(f"{name.lower()}_s{scale}")
+    ev = bf.FmmEvaluator(kern, plan, cache_dir=cache_dir)
+    out = {}
+    for mode in ("pair", "plain"):
+        ev.leaf_mode = mode
+        out[mode] = ev.evaluate(pts, weights=w)
+    assert rel_l2(out["pair"], out["plain"]) < 1e-13
+    if g is not None:
+        assert rel_l2(out["pair"][wl["check_idx"]], g["phi_idx"]) < PHI_TOL
+
+
+def test_stencil_two_targets_per_thread_bitwise(cache_dir, monkeypatch):
+    """stencil2_kernel (two x targets per thread, 16 x 8 x 8 tiles) against
+    stencil_kernel: same taps in the same order per target, so phi is
+    bitwise equal (uniform scheme, engine.py:258-292)."""
+    pts, w = unit_cloud(30000, seed=91, ncols=3)
+    plan = bf.FmmPlan(levels=5, order=4, scheme="uniform", eps=1e-6,
+                      domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
+    ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
+    a = ev.evaluate(pts, weights=w)
+    monkeypatch.setenv("BFMM_STENCIL", "1")
+    b = ev.evaluate(pts, weights=w)
+    assert np.array_equal(a, b)
