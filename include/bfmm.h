@@ -148,6 +148,20 @@ int bfmm_m2m(const double *child, double *parent, int64_t n_parent, int p,
 int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
                    int N, double *C, double alpha, double beta, int a_splits,
                    bfmm_stream_t stream);
+/* C = alpha * A @ B on the int8 tensor cores (csrc/proj_i8.cuh), A (rows, K)
+ * FP64 row-major, K, N <= 128: every A row is cut into six signed 8-bit
+ * digits under its own power-of-two scale, B arrives pre-cut (bdig: the
+ * digit image [ceil(N/64)][ceil(K/32)][6][64 x 32 K-major core matrices] of
+ * B^T with one scale per column n, bpow[n] = 2^e_n -- the same layout and
+ * builder as the M2L cores, engine._i8_core_slices), and the 21 digit
+ * products with a + b < 6 are summed exactly in int32 TMEM (truncation
+ * ~2^-46 of the row / column scales).  zmax (nullable, device): atomic max
+ * of |C| as a double bit pattern (zero it first) -- the digit scale
+ * bfmm_m2l_i8_slice_z needs, for one weight column.  Same C as
+ * bfmm_rows_gemm with beta = 0, a_splits = 1 (engine.py:233, 252-255). */
+int bfmm_rows_gemm_i8(const double *A, int64_t rows, int K, const int8_t *bdig,
+                      const double *bpow, int N, double *C, double alpha,
+                      unsigned long long *zmax, bfmm_stream_t stream);
 /* Same, but A row r lands in C row groups[r / group_rows] * group_rows +
  * r % group_rows (compact rows of listed cells scattered to their cells). */
 int bfmm_rows_gemm_scatter(const double *A, int64_t rows, int K,

@@ -672,7 +672,7 @@ constexpr size_t p2m_pair_smem() {
 }
 template <int P>
 constexpr size_t l2p_pair_smem() {
-  return sizeof(double) * pair_warps<P>() * 9 * P * P * P;
+  return sizeof(double) * pair_warps<P>() * 2 * ((9 * P * P * P + 1) & ~1);
 }
 
 // the eight children's counts of parent q: lanes < 8 hold child lane's
@@ -701,7 +701,7 @@ p2m_pair_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
                 Interp ip, LeafGeom g, double *__restrict__ mom_leaf,
                 double *__restrict__ mom_par, int32_t *flag) {
   constexpr int P3 = P * P * P, B = pair_batch<P>(), W = pair_warps<P>(), R = 6 * P + 1;
-  extern __shared__ double s_pair[];
+  extern __shared__ __align__(16) double s_pair[];
   __shared__ double sS[P * P], sN[P];
   __shared__ int s_off[W][9];
   stage_basis<P>(ip, sS, sN);
@@ -742,29 +742,54 @@ p2m_pair_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
         row[6 * P] = ws[i];
       }
       __syncwarp();
-      // the eight children's moments, consecutive outputs on consecutive lanes
+      // the eight children's moments: slot (child, i, j) owns the P
+      // moments M[i][j][0..P) -- one (wx_i wy_j w) product per point, then a
+      // P-wide FMA row against the broadcast wz (no per-output index math)
       double *leaf = mom_leaf + 8 * q * (int64_t)P3;
-      for (int o = lane; o < 8 * P3; o += 32) {
-        const int ch = o / P3, a = o - ch * P3;
-        const int ii = a / (P * P), jj = (a / P) % P, kk = a % P;
+      for (int sl = lane; sl < 8 * P * P; sl += 32) {
+        const int ch = sl / (P * P), ij = sl - ch * P * P, ii = ij / P, jj = ij - ii * P;
         const int p0 = max(s_off[wid][ch], b0), p1 = min(s_off[wid][ch + 1], b0 + nb);
-        double acc = 0.0;
+        double acc[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[k] = 0.0;
         for (int pt = p0; pt < p1; ++pt) {
           const double *wt = sw + (pt - b0) * R;
-          acc += ((wt[ii] * wt[P + jj]) * wt[2 * P + kk]) * wt[6 * P];
+          const double wxyw = (wt[ii] * wt[P + jj]) * wt[6 * P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) acc[k] = fma(wxyw, wt[2 * P + k], acc[k]);
         }
-        leaf[o] = b0 == 0 ? acc : leaf[o] + acc;
+        double *dst = leaf + ch * P3 + ij * P;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          if (b0 == 0) {
+            dst[k] = acc[k];
+          } else {
+            dst[k] += acc[k];
+          }
+        }
       }
-      // the parent's moments from the same points
+      // the parent's moments from the same points, slot (i, j)
       double *par = mom_par + q * (int64_t)P3;
-      for (int a = lane; a < P3; a += 32) {
-        const int ii = a / (P * P), jj = (a / P) % P, kk = a % P;
-        double acc = 0.0;
+      for (int ij = lane; ij < P * P; ij += 32) {
+        const int ii = ij / P, jj = ij - ii * P;
+        double acc[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[k] = 0.0;
         for (int pt = 0; pt < nb; ++pt) {
           const double *wt = sw + pt * R + 3 * P;
-          acc += ((wt[ii] * wt[P + jj]) * wt[2 * P + kk]) * wt[3 * P];
+          const double wxyw = (wt[ii] * wt[P + jj]) * wt[3 * P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) acc[k] = fma(wxyw, wt[2 * P + k], acc[k]);
         }
-        par[a] = b0 == 0 ? acc : par[a] + acc;
+        double *dst = par + ij * P;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          if (b0 == 0) {
+            dst[k] = acc[k];
+          } else {
+            dst[k] += acc[k];
+          }
+        }
       }
     }
   }
@@ -792,34 +817,64 @@ __device__ __forceinline__ double l2p_contract(const double *wx, const double *w
   return s;
 }
 
+// async 8-byte global -> shared copy (the parent's locals are 8-byte aligned)
+__device__ __forceinline__ void cp_async8_pair(double *smem, const double *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16_pair(double *smem, const double *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
 template <int P>
 __global__ void __launch_bounds__(32 * pair_warps<P>(), pair_minb<P>())
 l2p_pair_kernel(const double *__restrict__ pts4, const int32_t *__restrict__ cell_start,
                 const int32_t *__restrict__ cell_count, Interp ip, LeafGeom g,
                 const double *__restrict__ loc_leaf, const double *__restrict__ loc_par,
                 double *__restrict__ phi, int32_t *flag) {
-  constexpr int P3 = P * P * P, W = pair_warps<P>();
-  extern __shared__ double s_pair[];
+  // buffer stride rounded up to an even number of doubles: 16-byte aligned
+  // cp.async destinations for every P
+  constexpr int P3 = P * P * P, W = pair_warps<P>(), SL = (9 * P3 + 1) & ~1;
+  extern __shared__ __align__(16) double s_pair[];
   __shared__ double sS[P * P], sN[P];
   __shared__ int s_off[W][9];
   stage_basis<P>(ip, sS, sN);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double *sl = s_pair + (size_t)wid * 9 * P3;  // 8 children's locals, then the parent's
+  // two buffers per warp (the next parent's locals stream in while this
+  // one's points are evaluated): 8 children's locals, then the parent's
+  double *sl2 = s_pair + (size_t)wid * 2 * SL;
   const double inv_hw = 1.0 / g.hw, inv_hp = 1.0 / g.h, hp = 2.0 * g.h;
   const int64_t q_lo = g.cell_lo / 8, q_hi = (g.cell_hi + 7) / 8;
-  for (int64_t q = q_lo + int64_t(blockIdx.x) * W + wid; q < q_hi; q += int64_t(gridDim.x) * W) {
+  const int64_t stride = int64_t(gridDim.x) * W;
+  // the children's block (8 P^3 doubles) starts 16-byte aligned when 8 P^3
+  // is even -- always -- so it moves in 16-byte chunks; the parent's row in
+  // 8-byte ones
+  auto prefetch = [&](int64_t q, double *dst) {
+    const double *src = loc_leaf + 8 * q * (int64_t)P3;
+    for (int e = lane; e < 4 * P3; e += 32) cp_async16_pair(dst + 2 * e, src + 2 * e);
+    const double *srp = loc_par + q * (int64_t)P3;
+    for (int e = lane; e < P3; e += 32) cp_async8_pair(dst + 8 * P3 + e, srp + e);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int64_t q = q_lo + int64_t(blockIdx.x) * W + wid;
+  int buf = 0;
+  if (q < q_hi) prefetch(q, sl2);
+  for (; q < q_hi; q += stride) {
+    const bool more = q + stride < q_hi;
+    if (more) prefetch(q + stride, sl2 + (buf ^ 1) * SL);
     int total;
     int64_t first;
     const int inc = pair_scan(cell_start, cell_count, q, lane, total, first);
-    if (total == 0) continue;  // warp-uniform
-    __syncwarp();
     if (lane < 8) s_off[wid][lane + 1] = inc;
     if (lane == 0) s_off[wid][0] = 0;
-    const double *src = loc_leaf + 8 * q * (int64_t)P3;
-    for (int e = lane; e < 8 * P3; e += 32) sl[e] = src[e];
-    const double *srp = loc_par + q * (int64_t)P3;
-    for (int e = lane; e < P3; e += 32) sl[8 * P3 + e] = srp[e];
+    if (more) {
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncwarp();
+    const double *sl = sl2 + buf * SL;
     int px, py, pz;
     unmorton3((uint64_t)q, px, py, pz);
     for (int t = lane; t < total; t += 32) {
@@ -840,7 +895,8 @@ l2p_pair_kernel(const double *__restrict__ pts4, const int32_t *__restrict__ cel
       weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], hp, inv_hp, pz, flag), wz);
       phi[i] = s_leaf + l2p_contract<P>(wx, wy, wz, sl + 8 * P3);
     }
-    __syncwarp();
+    __syncwarp();  // buffer buf is refilled two parents on
+    buf ^= 1;
   }
 }
 

@@ -156,6 +156,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 #include "m2l_ws.cuh"
 #include "m2l_i8.cuh"
+#include "proj_i8.cuh"
 
 // ----------------------------------------------------------------------------
 // Basis projections on the FP64 tensor cores: C = alpha * A @ B (+ beta C),
@@ -423,6 +424,26 @@ extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
                               const double *B, int N, double *C, double alpha,
                               double beta, int a_splits, bfmm_stream_t stream) {
   return rows_gemm(A, rows, K, B, N, C, alpha, beta, a_splits, nullptr, 1, stream);
+}
+
+extern "C" int bfmm_rows_gemm_i8(const double *A, int64_t rows, int K, const int8_t *bdig,
+                                 const double *bpow, int N, double *C, double alpha,
+                                 unsigned long long *zmax, bfmm_stream_t stream) {
+  if (K < 1 || K > 128 || N < 1 || N > 128 || rows < 0) {
+    set_error("bfmm_rows_gemm_i8: K=%d N=%d (1..128)", K, N);
+    return 2;
+  }
+  if (rows == 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  const int kc = (int)ceil_div(K, 32), ntn = (int)ceil_div(N, 64);
+#define BFMM_PJ(KC, NT)                                                                   \
+  if (kc == KC && ntn == NT)                                                              \
+    return launch_proj_i8<KC, NT>(A, rows, K, K, bdig, bpow, N, C, alpha, zmax, st);
+  BFMM_PJ(1, 1) BFMM_PJ(2, 1) BFMM_PJ(3, 1) BFMM_PJ(4, 1)
+  BFMM_PJ(1, 2) BFMM_PJ(2, 2) BFMM_PJ(3, 2) BFMM_PJ(4, 2)
+#undef BFMM_PJ
+  set_error("bfmm_rows_gemm_i8: unreachable K=%d N=%d", K, N);
+  return 2;
 }
 
 extern "C" int bfmm_rows_gemm_scatter(const double *A, int64_t rows, int K,

@@ -38,6 +38,18 @@ __device__ __forceinline__ int64_t lex_of(int x, int y, int z, int n) {
   return ((int64_t)x * n + y) * n + z;
 }
 
+// 16-byte global -> shared copy on the async path (zero-filled when !valid):
+// a CTA's whole halo is in flight at once instead of one load round trip per
+// element (the stencils' halo load was latency-bound: ncu long_scoreboard)
+__device__ __forceinline__ void cp_async16z(void *smem, const void *gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // The transforms work on G lexicographically consecutive cells (a z-run)
 // per CTA pass, so the frequency-major spectra are written / read as
 // G * 16-byte runs, and every spectrum value is touched once.  Each 1-D DFT
@@ -91,9 +103,18 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
     const int64_t lex0 = (w - crel * ngroups) * G;
     const int x = (int)(lex0 / ((int64_t)n * n)), y = (int)((lex0 / n) % n), z0 = (int)(lex0 % n);
     __syncthreads();
-    for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
-      const int gi = e / P3, r = e - gi * P3;
-      in[e] = moments[((int64_t)morton3(x, y, z0 + gi) * m + c0 + crel) * P3 + r];
+    if (P3 % 2 == 0) {  // 16-byte rows: the whole block's moments in flight at once
+      for (int e = threadIdx.x; e < G * P3 / 2; e += blockDim.x) {
+        const int gi = (2 * e) / P3, r = 2 * e - gi * P3;
+        cp_async16z(in + 2 * e,
+                    moments + ((int64_t)morton3(x, y, z0 + gi) * m + c0 + crel) * P3 + r, true);
+      }
+      cp_async_all();
+    } else {
+      for (int e = threadIdx.x; e < G * P3; e += blockDim.x) {
+        const int gi = e / P3, r = e - gi * P3;
+        in[e] = moments[((int64_t)morton3(x, y, z0 + gi) * m + c0 + crel) * P3 + r];
+      }
     }
     __syncthreads();
     // z: p reals -> h bins, e^{-2 pi i k kz / q}; one line (gi, i, j) per thread
@@ -220,14 +241,14 @@ stencil_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level
   for (int e = tid; e < kHX * kHY * kHZ; e += 128) {
     const int hx = e / (kHY * kHZ), hr = e - hx * kHY * kHZ, hy = hr / kHZ, hz = hr - hy * kHZ;
     const int sx = x0 + hx - 3, sy = y0 + hy - 3, sz = z0 + hz - 3;
-    double2 v = make_double2(0.0, 0.0);
-    if (sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n) v = Xf[lex_of(sx, sy, sz, n)];
-    halo[hx][hy][hz] = v;
+    const bool v = sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n;
+    cp_async16z(&halo[hx][hy][hz], v ? Xf + lex_of(sx, sy, sz, n) : Xf, v);
   }
   for (int e = tid; e < 343; e += 128) {
     const int t = tap_index[e];
-    (&taps[0][0][0])[e] = t >= 0 ? S[(int64_t)t * F + f] : make_double2(0.0, 0.0);
+    cp_async16z(&taps[0][0][0] + e, t >= 0 ? S + (int64_t)t * F + f : S, t >= 0);
   }
+  cp_async_all();
   __syncthreads();
   double2 acc[kR];
 #pragma unroll
@@ -322,14 +343,14 @@ stencil2_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int leve
   for (int e = tid; e < kH2X * kHY * kHZ; e += 128) {
     const int hx = e / (kHY * kHZ), hr = e - hx * kHY * kHZ, hy = hr / kHZ, hz = hr - hy * kHZ;
     const int sx = x0 + hx - 3, sy = y0 + hy - 3, sz = z0 + hz - 3;
-    double2 v = make_double2(0.0, 0.0);
-    if (sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n) v = Xf[lex_of(sx, sy, sz, n)];
-    halo[hx][hy][hz] = v;
+    const bool v = sx >= 0 && sx < n && sy >= 0 && sy < n && sz >= 0 && sz < n;
+    cp_async16z(&halo[hx][hy][hz], v ? Xf + lex_of(sx, sy, sz, n) : Xf, v);
   }
   for (int e = tid; e < 343; e += 128) {
     const int t = tap_index[e];
-    (&taps[0][0][0])[e] = t >= 0 ? S[(int64_t)t * F + f] : make_double2(0.0, 0.0);
+    cp_async16z(&taps[0][0][0] + e, t >= 0 ? S + (int64_t)t * F + f : S, t >= 0);
   }
+  cp_async_all();
   __syncthreads();
   double2 acc[2][kR];
 #pragma unroll
@@ -411,8 +432,9 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
     const double2 *src = Y + (int64_t)crel * F * ncell + lex0;
     for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
       const int f = e / G, gi = e - f * G;
-      stage[e] = src[(int64_t)f * ncell + gi];
+      cp_async16z(stage + e, src + (int64_t)f * ncell + gi, true);
     }
+    cp_async_all();
     __syncthreads();
     // x: q bins -> p outputs, e^{+2 pi i i kx / q}; line (gi, ky, kz)
     for (int l = threadIdx.x; l < G * q * h; l += blockDim.x) {
@@ -582,9 +604,10 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   const size_t smem_s = sizeof(double2) * (kHX * kHYP * kHZP + 343);
   const size_t smem_s2 = sizeof(double2) * (kH2X * kHYP * kHZP + 343);
   const unsigned tiles2 = (unsigned)(ceil_div(n, kT2X) * ceil_div(n, kTY) * ceil_div(n, kTZ));
-  // BFMM_STENCIL=1 (diagnostic): the one-x-target-per-thread kernel
+  // BFMM_STENCIL=2: the two-x-targets-per-thread kernel (fewer halo
+  // reads, but 85 KB tiles leave 2 CTAs/SM; measured slower on C3)
   const char *sv = getenv("BFMM_STENCIL");
-  const bool stencil1 = sv && sv[0] == '1';
+  const bool stencil1 = !(sv && sv[0] == '2');
   static unsigned long long attr = 0;
   if (first_on_device(&attr)) {
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

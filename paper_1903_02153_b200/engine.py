@@ -90,10 +90,10 @@ def _i8_core_slices(CP: np.ndarray, S: int, bits: int = 7):
     rint(x 2^(8(S-1))) as S signed bytes, like z_slice_kernel).  Returns the
     int8 image [t][i // 64][k // 32][j][64 x 32 K-major core matrices] and
     2^e_i."""
-    T, rp, _ = CP.shape
-    kc, nt = -(-rp // 32), -(-rp // 64)
+    T, nr, kr = CP.shape  # (offsets, N rows, K) -- rp x rp for the cores
+    kc, nt = -(-kr // 32), -(-nr // 64)
     C = np.zeros((T, nt * 64, kc * 32))
-    C[:, :rp, :rp] = CP
+    C[:, :nr, :kr] = CP
     amax = np.abs(C).max(axis=(0, 2))
     e = np.where(amax > 0, np.frexp(amax)[1], 0).astype(np.int64)
     x = C * np.ldexp(1.0, 6 - e)[None, :, None]
@@ -240,6 +240,9 @@ class FmmEvaluator:
         # bfmm_l2p_pair), which fold the L -> L-1 M2M and the L-1 -> L L2L
         # into the leaf kernels ("auto"), or the separate passes ("plain")
         self.leaf_mode = "auto"
+        # basis projections z = M V, locals = s lt U^T: int8 tensor cores with
+        # per-row digit scales ("i8", where p^3, rank <= 128) or FP64 DMMA
+        self.proj_mode = "i8"
         # coarse far-field levels on a side stream (see _far_field); the
         # finest main_levels levels stay on the calling stream
         self.stream_levels = True
@@ -334,6 +337,22 @@ class FmmEvaluator:
                         torch.from_numpy(cpow).to(self.device))
         return blk[key]
 
+    def _pj_tables(self, blk, which):
+        """Digit image of B^T for bfmm_rows_gemm_i8: V (p^3, rp) -> z = M V,
+        UT (rp, p^3) -> locals = s lt UT (six 8-bit digits, per-column scale)."""
+        key = ("pj", which)
+        if key not in blk:
+            torch = _torch()
+            B = blk[which].cpu().numpy()
+            d, pw = _i8_core_slices(np.ascontiguousarray(B.T)[None], 6, 8)
+            blk[key] = (torch.from_numpy(d.reshape(-1)).to(self.device),
+                        torch.from_numpy(np.ascontiguousarray(pw)).to(self.device))
+        return blk[key]
+
+    def _proj_i8(self, p3, rp):
+        """Int8 projections (proj_mode): both GEMM sides <= 128 wide."""
+        return self.proj_mode == "i8" and p3 <= 128 and rp <= 128
+
     def _level_engine(self, lev, m, rp):
         """The Chebyshev M2L engine of one level: self.m2l_mode, except that
         the int8 kernels take rank tiles up to rp = 256 and 32-bit row
@@ -357,7 +376,7 @@ class FmmEvaluator:
         return int(self.i8_slices), 7
 
     def _m2l_translate(self, z, lt, lev, m, rp, ns, blk, st, q_lo=0, nq=0, cells=None, off=None,
-                       shard=None):
+                       shard=None, zmax=None):
         """lt = the 189-offset translation of z (engine.py:228-256), on the
         level's engine (_level_engine); cells/off: listed active targets."""
         torch = _torch()
@@ -368,8 +387,14 @@ class FmmEvaluator:
             rows = z.numel() // rp
             zs = torch.empty(int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, Sarg)), dtype=torch.int8,
                              device=self.device)
-            zmax = torch.empty(m, dtype=torch.int64, device=self.device)
-            if shard is not None and not shard[0].full:
+            if zmax is not None:
+                # max |z| from the int8 projection's epilogue (one column)
+                if shard is not None and not shard[0].full:
+                    shard[1].allreduce_max(zmax)
+                Sarg |= _native.I8_ZMAX_GIVEN
+            else:
+                zmax = torch.empty(m, dtype=torch.int64, device=self.device)
+            if shard is not None and not shard[0].full and not (Sarg & _native.I8_ZMAX_GIVEN):
                 # one digit scale per column over ALL ranks' cells: every
                 # shard cuts z exactly like the unsharded evaluation
                 _native.check(self.lib.bfmm_m2l_i8_zmax(z.data_ptr(), rows, m, rp,
@@ -730,19 +755,36 @@ class FmmEvaluator:
             z = zalloc((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((ncell * m * ns * rp,), dtype=torch.float64, device=self.device)
             e0 = self._kevent()
-            _native.check(self.lib.bfmm_rows_gemm(
-                moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
-                z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+            zmax = None
+            if self._proj_i8(p3, rp):
+                dg, pw = self._pj_tables(blk, "V")
+                if m == 1 and self._level_engine(lev, m, rp) == "i8":
+                    zmax = torch.zeros(1, dtype=torch.int64, device=self.device)
+                _native.check(self.lib.bfmm_rows_gemm_i8(
+                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, dg.data_ptr(),
+                    pw.data_ptr(), rp, z[lo * m * rp:].data_ptr(), 1.0,
+                    zmax.data_ptr() if zmax is not None else None, st), "bfmm_rows_gemm_i8(V)")
+            else:
+                _native.check(self.lib.bfmm_rows_gemm(
+                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                    z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             self._kspan(f"projv_l{lev}", e0)
             if shard is not None and not shard[0].full:
                 # the sources this shard's M2L reads: its halo (fine levels)
                 # or the whole level (coarse levels)
                 shard[1].exchange_level(z, m * rp, lev, shard[0])
-            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq, shard=shard)
+            self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, q_lo=q_lo, nq=nq, shard=shard,
+                                zmax=zmax)
             e0 = self._kevent()
-            _native.check(self.lib.bfmm_rows_gemm(
-                lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
-                out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
+            if self._proj_i8(p3, rp) and ns == 1:
+                dg, pw = self._pj_tables(blk, "UT")
+                _native.check(self.lib.bfmm_rows_gemm_i8(
+                    lt[lo * m * rp:].data_ptr(), nloc * m, rp, dg.data_ptr(), pw.data_ptr(), p3,
+                    out[lo * m * p3:].data_ptr(), scale, None, st), "bfmm_rows_gemm_i8(U)")
+            else:
+                _native.check(self.lib.bfmm_rows_gemm(
+                    lt[lo * m * ns * rp:].data_ptr(), nloc * m, rp, blk["UT"].data_ptr(), p3,
+                    out[lo * m * p3:].data_ptr(), scale, 0.0, ns, st), "bfmm_rows_gemm(U)")
             self._kspan(f"proju_l{lev}", e0)
         else:
             if shard is not None and not shard[0].full:
@@ -1124,7 +1166,8 @@ class FmmEvaluator:
         # the sparse-cloud active lists read counts back on the host
         return self.far_mode == "dense" or (self.far_mode == "auto" and n >= 8 * (1 << (3 * L)))
 
-    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "i8_digits", "p2m_mode", "leaf_mode", "far_mode",
+    _GRAPH_KNOBS = ("m2l_mode", "i8_slices", "i8_digits", "p2m_mode", "leaf_mode", "proj_mode",
+                    "far_mode",
                     "near_mode",
                     "overlap_near",
                     "near_after_far", "far_priority", "l2p_mode", "stream_levels",

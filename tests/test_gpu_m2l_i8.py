@@ -156,3 +156,58 @@ def test_i8_and_dmma_agree_on_c2_scaled(cache_dir):
         ev.m2l_mode = mode
         res[mode] = ev.evaluate(wl["points"], weights=wl["weights"])
     assert rel_l2(res["i8"], res["dmma"]) < 1e-12
+
+
+@pytest.mark.parametrize("rows,K,N", [(1000, 125, 64), (777, 64, 125), (300, 8, 8),
+                                      (129, 100, 104), (5000, 27, 16)])
+def test_int8_projection_matches_fp64(rows, K, N):
+    """bfmm_rows_gemm_i8 (per-row digit scales, six 8-bit digits, csrc/
+    proj_i8.cuh) against the FP64 product: rows of very different magnitude
+    (empty vs crowded cells), a zero row and a non-finite row; the zmax
+    epilogue equals max |C|."""
+    lib = _native.load()
+    st = _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    g = np.random.default_rng(rows + K)
+    A = g.standard_normal((rows, K)) * np.exp(g.uniform(-30, 5, (rows, 1)))
+    A[3] = 0.0
+    B = g.standard_normal((K, N)) * np.logspace(0, -6, N)[None, :]
+    d, pw = _i8_core_slices(np.ascontiguousarray(B.T)[None], 6, 8)
+    dA = torch.from_numpy(A).cuda()
+    dd, dp = torch.from_numpy(d.reshape(-1)).cuda(), torch.from_numpy(pw).cuda()
+    C = torch.full((rows, N), float("nan"), dtype=torch.float64, device="cuda")
+    zmax = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _native.check(lib.bfmm_rows_gemm_i8(dA.data_ptr(), rows, K, dd.data_ptr(), dp.data_ptr(), N,
+                                        C.data_ptr(), 0.5, zmax.data_ptr(), st), "gemm_i8")
+    got = C.cpu().numpy()
+    want = 0.5 * (A @ B)
+    # per row, relative to the row's scale (|A_r| |B|): the digit truncation
+    scale = np.abs(A).max(axis=1, keepdims=True) * np.abs(B).max() * K
+    assert np.all(np.abs(got - want) <= 1e-12 * scale + 1e-300)
+    assert np.all(got[3] == 0.0)
+    zm = zmax.cpu().numpy().view(np.float64)[0]
+    assert zm == np.abs(got).max()
+    # a non-finite row propagates (NaN), the others are untouched
+    A[7, 2] = np.inf
+    dA = torch.from_numpy(A).cuda()
+    _native.check(lib.bfmm_rows_gemm_i8(dA.data_ptr(), rows, K, dd.data_ptr(), dp.data_ptr(), N,
+                                        C.data_ptr(), 0.5, None, st), "gemm_i8")
+    got2 = C.cpu().numpy()
+    assert np.isnan(got2[7]).all()
+    assert np.array_equal(np.delete(got2, 7, axis=0), np.delete(got, 7, axis=0))
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 2), ("C4", 2)])
+def test_int8_projections_match_fp64_projections(name, scale, cache_dir):
+    """proj_mode "i8" (z = M V and locals = s lt U^T on the int8 tensor
+    cores) against the FP64 DMMA projections, and against the reference."""
+    wl = workloads.make(name, scale)
+    plan = bf.FmmPlan(levels=wl["levels"], order=wl["order"], scheme=wl["scheme"], eps=wl["eps"],
+                      domain_center=wl["center"], domain_length=wl["length"], n_cols=wl["ncols"])
+    ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir=cache_dir)
+    out = {}
+    for mode in ("i8", "fp64"):
+        ev.proj_mode = mode
+        out[mode] = ev.evaluate(wl["points"], weights=wl["weights"])
+    assert rel_l2(out["i8"], out["fp64"]) < 1e-12
+    g = golden(f"{name.lower()}_s{scale}")
+    assert rel_l2(out["i8"][wl["check_idx"]], g["phi_idx"]) < PHI_TOL

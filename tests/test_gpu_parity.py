@@ -563,6 +563,6 @@ def test_stencil_two_targets_per_thread_bitwise(cache_dir, monkeypatch):
                       domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
     ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
     a = ev.evaluate(pts, weights=w)
-    monkeypatch.setenv("BFMM_STENCIL", "1")
+    monkeypatch.setenv("BFMM_STENCIL", "2")
     b = ev.evaluate(pts, weights=w)
     assert np.array_equal(a, b)
