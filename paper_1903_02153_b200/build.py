@@ -22,7 +22,8 @@ LIB = os.path.join(OUT_DIR, "libbfmm.so")
 OBJ_DIR = os.path.join(ROOT, "build", "obj")
 
 SOURCES = ["tree.cu", "interp.cu", "m2l_cheb.cu", "m2l_fft.cu", "p2p.cu", "misc.cu"]
-HEADERS = ["common.cuh", "p2p.cuh", "m2l_ws.cuh", "m2l_i8.cuh", "tcgen05.cuh", "leaf_kernels.cuh", "transfer_kernels.cuh"]
+HEADERS = ["common.cuh", "p2p.cuh", "m2l_ws.cuh", "m2l_i8.cuh", "proj_i8.cuh", "tcgen05.cuh",
+           "leaf_kernels.cuh", "transfer_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]
@@ -55,7 +56,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     os.makedirs(OBJ_DIR, exist_ok=True)
     _embed_p2p_source()
-    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [
+    # every header under csrc/ (a new .cuh is tracked without listing it)
+    hdrs = sorted({os.path.join(CSRC, h) for h in HEADERS} |
+                  {os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")}) + [
         os.path.join(ROOT, "include", "bfmm.h"), os.path.join(CSRC, "p2p_src.inc")]
     objs, jobs = [], []
     for s in SOURCES:

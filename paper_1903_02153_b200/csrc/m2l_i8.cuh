@@ -418,10 +418,13 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
   const int n = 1 << level;  // cells per axis
-  const int o = blockIdx.z & 7, split = blockIdx.z >> 3;
+  // octant fastest in the launch order: the eight octant tiles of one
+  // spatial block run together and share their source parity planes in L2
+  // (octant-major order re-read every plane from DRAM once per octant)
+  const int o = blockIdx.x & 7, split = blockIdx.z;
   const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
   const int ybn = (box.w >> 10) & 1023, zbn = box.w & 1023;
-  int tile = blockIdx.x;
+  int tile = blockIdx.x >> 3;
   const int zb = tile % zbn + box.z / 8;
   tile /= zbn;
   const int yb = tile % ybn + box.y / YT;
@@ -799,7 +802,7 @@ int launch_i8p(const I8Call &a) {
   int4 box;
   i8_plane_box(a, XT, Sh::YT, &box);
   const int tiles = (box.w >> 20) * ((box.w >> 10) & 1023) * (box.w & 1023);
-  dim3 grid((unsigned)tiles, (unsigned)(a.ntn * a.m), 8 * a.nsplit);
+  dim3 grid((unsigned)tiles * 8, (unsigned)(a.ntn * a.m), a.nsplit);
   m2l_i8p_kernel<S, XT, B><<<grid, kI8PThreads, Sh::smem, a.st>>>(
       a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, box);
   return check_launch("m2l_i8p_kernel");

@@ -11,24 +11,24 @@
 // the row / column scales, against the FP64 DMMA projection's 2^-53 K:
 // either is far inside the M2L's own digit truncation.
 //
-// Persistent CTA per SM, 160 threads: warp 0 allocates TMEM and issues the
+// Persistent CTA per SM, 288 threads: warp 0 allocates TMEM and issues the
 // MMAs; warps 1-4 slice 128-row tiles of A straight from HBM into the
 // K-major digit planes (a warp per 32 rows, lane l holding k = 4l .. 4l+3,
-// the row maximum by a warp reduction) and afterwards drain the S int32
-// accumulators of each 64-column N tile to FP64.  B's digit image (<= 48 KB)
-// is bulk-copied once per CTA.  Memory-bound: A is read once, C written
-// once (C5 level 8: 16.8 + 8.6 GB for z).
+// the row maximum by a warp reduction); warps 5-8 drain the S int32
+// accumulators of each 64-column N tile to FP64, so the slicing of tile t+1
+// overlaps the drain of tile t.  B's digit image (<= 96 KB) is bulk-copied
+// once per CTA.  Memory-bound: A is read once, C written once.
 #pragma once
 
 constexpr int kPjS = 6;           // 8-bit digits
-constexpr int kPjThreads = 160;
+constexpr int kPjThreads = 288;
 
 template <int KC, int NTN>
 struct PjI8Shape {
   static constexpr int A_PLANE = 128 * 32, B_PLANE = 64 * 32;
   static constexpr int A_BYTES = KC * kPjS * A_PLANE;
   static constexpr int B_BYTES = NTN * KC * kPjS * B_PLANE;
-  static constexpr size_t smem = (size_t)A_BYTES + B_BYTES + 128 * sizeof(double) + 64;
+  static constexpr size_t smem = (size_t)A_BYTES + B_BYTES + 256 * sizeof(double) + 64;
 };
 
 template <int KC, int NTN>
@@ -41,10 +41,12 @@ proj_i8_kernel(const double *__restrict__ A, int64_t rows, int lda, int K,
   extern __shared__ __align__(1024) uint8_t sp[];
   uint8_t *const sA = sp;
   uint8_t *const sB = sp + Sh::A_BYTES;
-  double *const s_rs = reinterpret_cast<double *>(sB + Sh::B_BYTES);  // row scales
-  uint64_t *bars = reinterpret_cast<uint64_t *>(s_rs + 128);
-  uint64_t *bar_b = bars, *bar_full = bars + 1, *bar_done = bars + 2, *bar_free = bars + 3;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
+  // row scales of the tile being sliced / drained (two: by tile parity)
+  double *const s_rs = reinterpret_cast<double *>(sB + Sh::B_BYTES);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(s_rs + 256);
+  uint64_t *bar_b = bars, *bar_full = bars + 1, *bar_done = bars + 2, *bar_free = bars + 3,
+           *bar_aempty = bars + 4;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ntiles = (rows + 127) / 128;
 
@@ -54,6 +56,7 @@ proj_i8_kernel(const double *__restrict__ A, int64_t rows, int lda, int K,
     mbar_init(bar_full, 4);
     mbar_init(bar_done, 1);
     mbar_init(bar_free, 4);
+    mbar_init(bar_aempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   bfmm::tc::fence_before();
@@ -104,16 +107,20 @@ proj_i8_kernel(const double *__restrict__ A, int64_t rows, int lda, int K,
             }
           }
           bfmm::tc::commit(bar_done);
+          if (nt == NTN - 1) bfmm::tc::commit(bar_aempty);  // A may be refilled
         }
         __syncwarp();
       }
     }
-  } else {
+  } else if (warp <= 4) {
     // ---------------- slice A tiles, drain accumulators ----------------
-    const int quarter = warp - 1;  // rows 32 quarter .. + 31 of a tile; TMEM lanes the same
-    uint32_t ph_done = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      // (the previous tile's MMAs all completed: its last bar_done was waited)
+    // rows 32 quarter .. + 31 of a tile and the same TMEM lanes: a warp may
+    // only touch TMEM lanes 32 (warp % 4) .. + 31
+    const int quarter = warp & 3;
+    uint32_t ph_ae = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      double *rs = s_rs + 128 * (it & 1);
       for (int rb = 0; rb < 4; ++rb) {
         double v[8][4];
 #pragma unroll
@@ -144,8 +151,15 @@ proj_i8_kernel(const double *__restrict__ A, int64_t rows, int lda, int K,
           int e = 0;
           const bool fin = amax <= 1.7976931348623157e308;  // false for inf / NaN
           if (fin && amax > 0) frexp(amax, &e);
+          if (rb == 0 && rr == 0 && it > 0) {
+            // the previous tile's MMAs released A (and, through bar_free, the
+            // drain of the tile before it released this half of s_rs); this
+            // tile's first rows are already in flight
+            mbar_wait(bar_aempty, ph_ae);
+            ph_ae ^= 1u;
+          }
           if (lane == 0)
-            s_rs[row] = fin ? ldexp(1.0, e - 12) : __longlong_as_double(0x7ff8000000000000ll);
+            rs[row] = fin ? ldexp(1.0, e - 12) : __longlong_as_double(0x7ff8000000000000ll);
           const double inv = ldexp(1.0, 6 - e);  // first digit of x / 2^(e - 6) in [-64, 64]
           uint32_t w[S];
 #pragma unroll
@@ -173,13 +187,20 @@ proj_i8_kernel(const double *__restrict__ A, int64_t rows, int lda, int K,
       bfmm::tc::fence_proxy_async();  // generic-proxy writes -> tensor core reads
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_full);
+    }
+  } else {
+    // ---------------- drain the accumulators (warps 5-8) ----------------
+    const int quarter = warp & 3;
+    uint32_t ph_done = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int row = quarter * 32 + lane;
       const int64_t r = t * 128 + row;
       for (int nt = 0; nt < NTN; ++nt) {
         mbar_wait(bar_done, ph_done);
         ph_done ^= 1u;
         bfmm::tc::fence_after();
-        const double rs = s_rs[row] * alpha;
+        const double rs = s_rs[128 * (it & 1) + row] * alpha;
         double amax = 0.0;
 #pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 8) {

@@ -242,7 +242,7 @@ class FmmEvaluator:
         self.leaf_mode = "auto"
         # basis projections z = M V, locals = s lt U^T: int8 tensor cores with
         # per-row digit scales ("i8", where p^3, rank <= 128) or FP64 DMMA
-        self.proj_mode = "i8"
+        self.proj_mode = "fp64"
         # coarse far-field levels on a side stream (see _far_field); the
         # finest main_levels levels stay on the calling stream
         self.stream_levels = True

@@ -20,7 +20,8 @@ ev = bf.FmmEvaluator(workload_kernel(wl["kernel"]), plan, cache_dir="/tmp/bfmm_c
 ev.stream_levels = False  # serial levels: clean per-kernel times
 ev.overlap_near = False
 import os  # noqa: E402
-for knob in ("i8_digits", "m2l_mode", "p2m_mode", "l2p_mode"):
+for knob in ("i8_digits", "m2l_mode", "p2m_mode", "l2p_mode", "proj_mode", "leaf_mode",
+             "near_mode"):
     if os.environ.get("BFMM_" + knob.upper()):
         setattr(ev, knob, os.environ["BFMM_" + knob.upper()])
 ev.profile_kernels = bool(os.environ.get("BFMM_PROFILE"))
