@@ -812,6 +812,8 @@ inline bool i8_plane_ok(const I8Call &a) {
   return i8_plane_box(a, a.level >= 5 ? 1 : 2, a.level >= 5 ? 16 : 8, nullptr);
 }
 
+#include "m2l_i8p2.cuh"
+
 template <int XT>
 int dispatch_i8p(int S, int B, const I8Call &a) {
   if (B == 8) return launch_i8p<6, XT, 8>(a);
@@ -825,6 +827,10 @@ int dispatch_i8p(int S, int B, const I8Call &a) {
 
 // S digits of B bits (B = 8 only with S = 6, see i8_base256_ok)
 inline int dispatch_i8(int S, int B, const I8Call &a) {
+  int4 box2;
+  // six 8-bit digits on dense levels >= 5: the CTA-pair plane kernel
+  // (BFMM_I8_1CTA, diagnostic: the single-CTA one)
+  if (B == 8 && S == 6 && i8p2_ok(a, &box2)) return launch_i8p2(a, box2);
   if (i8_plane_ok(a)) return a.level >= 5 ? dispatch_i8p<1>(S, B, a) : dispatch_i8p<2>(S, B, a);
   if (B == 8) return launch_i8<6, 8>(a);
   switch (S) {
