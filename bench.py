@@ -309,6 +309,13 @@ def _valid_offsets(o):
     return out
 
 
+def _pair_kernel(lev, S):
+    """The CTA-pair plane kernel runs the level (csrc/m2l_i8p2.cuh, i8p2_ok):
+    six 8-bit digits, dense level >= 5 (even z-tile count: always for whole
+    levels >= 5)."""
+    return S == 6 and lev >= 5 and not os.environ.get("BFMM_I8_1CTA")
+
+
 def m2l_i8_ops(lev, rp, m, S):
     """int8 operations the tcgen05 M2L executes at one level: per (tile,
     offset, 32-wide k chunk, 64-wide rank tile) stage, S(S+1)/2 digit
@@ -318,6 +325,10 @@ def m2l_i8_ops(lev, rp, m, S):
     n = 1 << lev
     kc, ntn = -(-rp // 32), -(-rp // 64)
     per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
+    if _pair_kernel(lev, S):
+        # m2l_i8p2_kernel: digit pairs (2k, 2k+1) per MMA, 24 products (the
+        # 21 of a + b < 6 plus 3 that land in a dropped accumulator)
+        per_stage = 2.0 * 128 * 64 * 32 * 24
     if lev >= 4:
         h = n // 2
         xt = 1 if lev >= 5 else 2
@@ -592,6 +603,7 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms, share=1.0):
                 if executed is None:
                     executed = m2l_i8_ops(lev, rp, m, S) * share
                 rec.update({"kernel": ("gather (active cells)" if lev in ev.active_profile
+                                       else "plane pair" if _pair_kernel(lev, S)
                                        else "plane" if lev >= 4 else "gather"),
                             "digits": f"{S} x {bits}-bit",
                             "useful_int8_tops": useful / (v * 1e-3) / 1e12,
@@ -636,8 +648,10 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms, share=1.0):
         rec = levels[dom]
         lev = dom.split("_l")[1]
         if rec["engine"] == "i8":
-            roof = {"kernel": f"m2l_i8{'p' if rec['kernel'] == 'plane' else ''}_kernel "
-                              f"(M2L level {lev}, int8 tcgen05, {rec['digits']} digits/operand)",
+            kname = {"plane": "m2l_i8p_kernel", "plane pair":
+                     "m2l_i8p2_kernel (CTA pair, cta_group::2)"}.get(rec["kernel"], "m2l_i8_kernel")
+            roof = {"kernel": f"{kname} (M2L level {lev}, int8 tcgen05, {rec['digits']} "
+                              "digits/operand)",
                     "bound": "tensor", "achieved": rec["useful_int8_tops"],
                     "peak": peaks["i8_tops"], "unit": "TFLOP/s",
                     "op_kind": "int8 tensor-core ops (1 MAC = 2), tcgen05 kind::i8",

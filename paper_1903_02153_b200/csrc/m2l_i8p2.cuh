@@ -84,6 +84,7 @@ __device__ __forceinline__ void commit_pair(uint64_t *bar) {
 // then the TMEM drain, 6 forwards each landed core block to the leader
 constexpr int kI8P2Threads = 224;
 
+template <int NBMAX>
 struct I8P2Shape {
   static constexpr int S = 6, XT = 1, YT = 16;
   static constexpr int ROWS = (YT + 4) * XT * 12;
@@ -94,17 +95,20 @@ struct I8P2Shape {
   static constexpr int BUDGET = BFMM_I8P_SMEM_KB * 1024 - 512;
   static constexpr int NP = 3;
   static constexpr int NB_FIT = (BUDGET - NP * PLANE) / B_STAGE;
-  static constexpr int NB = NB_FIT > 12 ? 12 : NB_FIT;
+  static constexpr int NB = NB_FIT > NBMAX ? NBMAX : NB_FIT;
   static constexpr size_t smem = (size_t)NP * PLANE + (size_t)NB * B_STAGE +
                                  (2 * NP + 3 * NB + 1) * 8 + 16;
 };
 
+// NBMAX = 12: the whole SM's shared memory; NBMAX = 6 (BFMM_I8_COSCHED):
+// ~176 KB, leaving room for one near-field tile CTA beside it on each SM
+template <int NBMAX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8P2Threads, 1)
 m2l_i8p2_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
                 const int8_t *__restrict__ cs, const double *__restrict__ cpow,
                 double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
                 int nsplit, int4 box) {
-  using Sh = I8P2Shape;
+  using Sh = I8P2Shape<NBMAX>;
   constexpr int S = Sh::S, NP = Sh::NP, NB = Sh::NB, YT = Sh::YT, XT = Sh::XT;
   extern __shared__ __align__(1024) uint8_t smp[];
   uint8_t *const planes = smp;
@@ -354,17 +358,22 @@ inline bool i8p2_ok(const I8Call &a, int4 *box) {
   return (box->w & 1023) % 2 == 0;
 }
 
-inline int launch_i8p2(const I8Call &a, int4 box) {
-  using Sh = I8P2Shape;
+template <int NBMAX>
+int launch_i8p2_nb(const I8Call &a, int4 box) {
+  using Sh = I8P2Shape<NBMAX>;
   static unsigned long long attr_set = 0;
   if (first_on_device(&attr_set)) {
-    cudaFuncSetAttribute(m2l_i8p2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(m2l_i8p2_kernel<NBMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Sh::smem);
   }
   const int tiles = (box.w >> 20) * ((box.w >> 10) & 1023) * (box.w & 1023);
   dim3 grid((unsigned)tiles * 8, (unsigned)(a.ntn * a.m), a.nsplit);
-  m2l_i8p2_kernel<<<grid, kI8P2Threads, Sh::smem, a.st>>>(a.zs, a.zmax, a.cs, a.cpow, a.lt,
-                                                         a.level, a.m, a.rp, a.kc_n, a.ntn,
-                                                         a.nsplit, box);
+  m2l_i8p2_kernel<NBMAX><<<grid, kI8P2Threads, Sh::smem, a.st>>>(
+      a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, box);
   return check_launch("m2l_i8p2_kernel");
+}
+
+inline int launch_i8p2(const I8Call &a, int4 box) {
+  const char *cs = getenv("BFMM_I8_COSCHED");
+  return (cs && cs[0] == '1') ? launch_i8p2_nb<6>(a, box) : launch_i8p2_nb<12>(a, box);
 }
