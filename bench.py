@@ -420,7 +420,8 @@ def _max_over_ranks(dist, v):
     if dist is None:
         return v
     import torch
-    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -681,11 +682,20 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_1903_02153_b200 import _native
 
+    # BFMM_BENCH_BACKEND=gloo with BFMM_BENCH_SHARE_GPU=1: a functional run of
+    # the N-rank code path with every rank on cuda:0 and host-staged
+    # exchanges (no kernel waits on another rank; its timing means nothing)
+    backend = os.environ.get("BFMM_BENCH_BACKEND", "nccl")
+    if os.environ.get("BFMM_BENCH_SHARE_GPU"):
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
         assert dist.get_world_size() == world == args.gpus, (dist.get_world_size(), args.gpus)
     lib = _native.load()
     stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -218,3 +218,29 @@ def test_bench_reference_arm_runs_on_cpu():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_table_cache_concurrent_writers(tmp_path):
+    """Ranks of a multi-GPU run build and cache the same M2L table at once:
+    every writer renames its own temporary file (no shared .tmp name)."""
+    import threading as th
+
+    import paper_1903_02153_b200 as bf
+    from paper_1903_02153_b200.tables import precompute_m2l
+    plan = bf.FmmPlan(levels=3, order=3, eps=1e-4, domain_center=(0.5, 0.5, 0.5),
+                      domain_length=1.0)
+    errs = []
+
+    def build():
+        try:
+            precompute_m2l(bf.LAPLACIAN, plan, cache_dir=str(tmp_path))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [th.Thread(target=build) for _ in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert not list(tmp_path.glob("*.tmp"))
