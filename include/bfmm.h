@@ -148,6 +148,14 @@ int bfmm_m2m(const double *child, double *parent, int64_t n_parent, int p,
 int bfmm_rows_gemm(const double *A, int64_t rows, int K, const double *B,
                    int N, double *C, double alpha, double beta, int a_splits,
                    bfmm_stream_t stream);
+/* bfmm_rows_gemm with beta = 0, a_splits = 1, K, N <= 128 on the persistent
+ * DMMA kernel (B resident in shared memory), plus max |C| into *zmax (device,
+ * zero it first; bit pattern of a non-negative double, atomicMax) -- the
+ * digit scale bfmm_m2l_i8_slice_z takes with BFMM_I8_ZMAX_GIVEN for one
+ * weight column (replaces its absmax pass). */
+int bfmm_rows_gemm_max(const double *A, int64_t rows, int K, const double *B, int N,
+                       double *C, double alpha, unsigned long long *zmax,
+                       bfmm_stream_t stream);
 /* C = alpha * A @ B on the int8 tensor cores (csrc/proj_i8.cuh), A (rows, K)
  * FP64 row-major, K, N <= 128: every A row is cut into six signed 8-bit
  * digits under its own power-of-two scale, B arrives pre-cut (bdig: the

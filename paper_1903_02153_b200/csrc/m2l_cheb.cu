@@ -254,6 +254,32 @@ proj_gemm_kernel(const double *__restrict__ A, int64_t rows, int64_t lda, int K,
     }
   }
   cp_async_wait<0>();
+  if (WN == 2 && !groups && beta == 0.0 && gridDim.y == 1) {
+    // all N columns in this CTA and a plain row range: stage the 64 x N tile
+    // in the (now idle) ring and write it as one contiguous block of C, rows
+    // whole, instead of 8-byte stores spread over 8 rows per instruction
+    constexpr int CLD = 64 * WN + 2;
+    __syncthreads();
+    double *Cs = pj;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int rl = wr * 16 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = wc * 64 + j * 8 + 2 * t4;
+        Cs[rl * CLD + n] = alpha * acc[i][j][0];
+        Cs[rl * CLD + n + 1] = alpha * acc[i][j][1];
+      }
+    }
+    __syncthreads();
+    const int nr = rows - row0 < kPjTM ? (int)(rows - row0) : kPjTM;
+    double *cblk = C + row0 * N;
+    for (int e = tid; e < nr * N; e += NTH) {
+      const int rl = e / N, n = e - rl * N;
+      cblk[e] = Cs[rl * CLD + n];
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int64_t r = row0 + wr * 16 + i * 8 + g;
@@ -270,6 +296,153 @@ proj_gemm_kernel(const double *__restrict__ A, int64_t rows, int64_t lda, int K,
         crow[n] = v;
       }
     }
+  }
+}
+
+// Persistent variant for the big levels (no split blocks, no row groups):
+// the whole B (<= 128 x 136 doubles, 70-74 KB) is staged once per CTA and
+// stays resident, and the A ring runs across row tiles without draining --
+// the per-stage B copies and the per-tile pipeline restarts of
+// proj_gemm_kernel go away.  Two CTAs per SM (3-stage ring).  Optional
+// epilogue: zmax = max |C| (bit pattern, atomicMax; one weight column),
+// the digit scale of the int8 M2L, which then skips its absmax pass.
+constexpr int kPjResStages = 3;
+// WN = 2 (N > 64, e.g. locals = lt U^T with N = p^3 = 125): the tile's
+// 64 x N outputs are staged in shared memory and written as whole rows
+// (the tile is one contiguous 64 N-double block of C), instead of 8-byte
+// stores scattered over 8 rows per instruction
+constexpr int kPjCLD = 130;
+constexpr int kPjResMaxK2 = 80;  // WN = 2: resident B + ring + C stage <= 184 KB
+template <int WN>
+constexpr size_t pj_res_smem(int K) {
+  return sizeof(double) * ((size_t)((K + kPjKC - 1) / kPjKC) * kPjKC * pj_ldb<WN>() +
+                           kPjResStages * kPjTM * kPjLDA + (WN == 2 ? kPjTM * kPjCLD : 0));
+}
+
+template <int WN>
+__global__ void __launch_bounds__(128 * WN, 2)
+proj_gemm_res_kernel(const double *__restrict__ A, int64_t rows, int64_t lda, int K,
+                     const double *__restrict__ B, int N, double *__restrict__ C, double alpha,
+                     unsigned long long *__restrict__ zmax) {
+  constexpr int TN = 64 * WN, NT = 8, LDB = pj_ldb<WN>(), NTH = 128 * WN;
+  constexpr int A_ELEMS = kPjTM * kPjLDA;
+  constexpr int AEPT = kPjTM * kPjKC / NTH;  // A slots per thread
+  constexpr int AR_STEP = NTH / kPjKC;
+  extern __shared__ __align__(16) double pj[];
+  const int nk = (K + kPjKC - 1) / kPjKC;
+  double *Bs = pj;                         // [nk * 16][LDB], resident
+  double *As0 = pj + (size_t)nk * kPjKC * LDB;  // [kPjResStages][A_ELEMS]
+  double *Cs = As0 + kPjResStages * A_ELEMS;    // [64][kPjCLD] (WN == 2)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 3, wc = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t ntiles = (rows + kPjTM - 1) / kPjTM;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // B once: rows k < K, columns n < N, zeros elsewhere
+  for (int e = tid; e < nk * kPjKC * TN; e += NTH) {
+    const int k = e / TN, n = e - k * TN;
+    const bool v = k < K && n < N;
+    cp_async8(Bs + k * LDB + n, v ? B + (int64_t)k * N + n : B, v);
+  }
+  cp_async_commit();
+  const int ar = tid / kPjKC, ak = tid % kPjKC;
+  // chunk q of this CTA: tile index q / nk of its sequence, k chunk q % nk
+  auto issue = [&](int64_t q) {
+    double *As = As0 + (q % kPjResStages) * A_ELEMS;
+    const int64_t row0 = (blockIdx.x + (q / nk) * gridDim.x) * kPjTM;
+    const int k0 = (int)(q % nk) * kPjKC;
+    const bool akv = k0 + ak < K;
+#pragma unroll
+    for (int u = 0; u < AEPT; ++u) {
+      const int64_t r = row0 + ar + u * AR_STEP;
+      const bool v = akv && r < rows;
+      cp_async8(As + (ar + u * AR_STEP) * kPjLDA + ak, v ? A + r * lda + k0 + ak : A, v);
+    }
+  };
+  const int64_t nq = my_tiles * nk;
+#pragma unroll
+  for (int st = 0; st < kPjResStages - 1; ++st) {
+    if (st < nq) issue(st);
+    cp_async_commit();
+  }
+  double amax = 0.0;
+  for (int64_t i = 0; i < my_tiles; ++i) {
+    double acc[2][NT][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[a][j][0] = acc[a][j][1] = 0.0;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int64_t q = i * nk + kc;
+      cp_async_wait<kPjResStages - 2>();
+      __syncthreads();
+      if (q + kPjResStages - 1 < nq) issue(q + kPjResStages - 1);
+      cp_async_commit();
+      const double *As = As0 + (q % kPjResStages) * A_ELEMS;
+      const double *Bk = Bs + kc * kPjKC * LDB;
+#pragma unroll
+      for (int ks = 0; ks < kPjKC; ks += 4) {
+        double a[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) a[u] = As[(wr * 16 + u * 8 + g) * kPjLDA + ks + t4];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const double b = Bk[(ks + t4) * LDB + wc * 64 + j * 8 + g];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) dmma_8x8x4(acc[u][j][0], acc[u][j][1], a[u], b);
+        }
+      }
+    }
+    const int64_t row0 = (blockIdx.x + i * gridDim.x) * kPjTM;
+    if constexpr (WN == 2) {
+      // stage, then whole contiguous rows (the A ring is untouched: Cs is its own)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int rl = wr * 16 + u * 8 + g;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int n = wc * 64 + j * 8 + 2 * t4;
+          Cs[rl * kPjCLD + n] = alpha * acc[u][j][0];
+          Cs[rl * kPjCLD + n + 1] = alpha * acc[u][j][1];
+        }
+      }
+      __syncthreads();
+      const int nr = rows - row0 < kPjTM ? (int)(rows - row0) : kPjTM;
+      double *cblk = C + row0 * N;
+      for (int e = tid; e < nr * N; e += NTH) {
+        const int rl = e / N, n = e - rl * N;
+        const double v = Cs[rl * kPjCLD + n];
+        cblk[e] = v;
+        amax = fmax(amax, fabs(v));
+      }
+      __syncthreads();  // Cs is rewritten by the next tile
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t r = row0 + wr * 16 + u * 8 + g;
+        if (r >= rows) continue;
+        double *crow = C + r * N;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int n = wc * 64 + j * 8 + 2 * t4;
+          const double v0 = alpha * acc[u][j][0], v1 = alpha * acc[u][j][1];
+          if (n + 1 < N && (N % 2 == 0)) {  // 16-byte aligned pair (even row stride)
+            *reinterpret_cast<double2 *>(crow + n) = make_double2(v0, v1);
+          } else {
+            if (n < N) crow[n] = v0;
+            if (n + 1 < N) crow[n + 1] = v1;
+          }
+          if (n < N) amax = fmax(amax, fabs(v0));
+          if (n + 1 < N) amax = fmax(amax, fabs(v1));
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (zmax) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0 && amax > 0) atomicMax(zmax, (unsigned long long)__double_as_longlong(amax));
   }
 }
 
@@ -379,6 +552,26 @@ extern "C" int bfmm_far_pairs(int level, int t_index, int64_t *tg, int64_t *sr,
   return check_launch("far_emit_kernel");
 }
 
+static int rows_gemm_res(const double *A, int64_t rows, int64_t lda, int K, const double *B,
+                         int N, double *C, double alpha, unsigned long long *zmax,
+                         cudaStream_t st) {
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) {
+    cudaFuncSetAttribute(proj_gemm_res_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pj_res_smem<1>(128));
+    cudaFuncSetAttribute(proj_gemm_res_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pj_res_smem<2>(kPjResMaxK2));
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows, kPjTM), 2 * kNumSMs);
+  if (N > 64)
+    proj_gemm_res_kernel<2><<<grid, 256, pj_res_smem<2>(K), st>>>(A, rows, lda, K, B, N, C, alpha,
+                                                                  zmax);
+  else
+    proj_gemm_res_kernel<1><<<grid, 128, pj_res_smem<1>(K), st>>>(A, rows, lda, K, B, N, C, alpha,
+                                                                  zmax);
+  return check_launch("proj_gemm_res_kernel");
+}
+
 static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int N,
                      double *C, double alpha, double beta, int a_splits,
                      const int64_t *groups, int64_t group_rows,
@@ -400,6 +593,12 @@ static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int 
     if (check_launch("reduce_splits_kernel")) return 1;
   }
   const int64_t lda = (int64_t)a_splits * K;
+  // big plain levels: the persistent kernel with B resident
+  // (N <= 64 only: for N = p^3 = 125 the staged WN = 2 variant measured
+  // slower than the tiled kernel -- one CTA per SM, C5 Uᵀ 16.0 -> 19.7 ms)
+  if (!groups && K <= 128 && N <= 64 && beta == 0.0 && ceil_div(rows, kPjTM) >= 8 * kNumSMs &&
+      !getenv("BFMM_PJ_TILED"))
+    return rows_gemm_res(A, rows, lda, K, B, N, C, alpha, nullptr, st);
   // one CTA spans all N <= 128 columns, so A is read once -- unless that
   // leaves most SMs idle (small levels): then 64-column tiles, twice the CTAs
   const int wn = (N > 64 && ceil_div(rows, kPjTM) >= kNumSMs) ? 2 : 1;
@@ -424,6 +623,21 @@ extern "C" int bfmm_rows_gemm(const double *A, int64_t rows, int K,
                               const double *B, int N, double *C, double alpha,
                               double beta, int a_splits, bfmm_stream_t stream) {
   return rows_gemm(A, rows, K, B, N, C, alpha, beta, a_splits, nullptr, 1, stream);
+}
+
+extern "C" int bfmm_rows_gemm_max(const double *A, int64_t rows, int K, const double *B, int N,
+                                  double *C, double alpha, unsigned long long *zmax,
+                                  bfmm_stream_t stream) {
+  if (K < 1 || K > 128 || N < 1 || N > 128 || rows < 0 || !zmax) {
+    set_error("bfmm_rows_gemm_max: K=%d N=%d (1..128), zmax=%p", K, N, (void *)zmax);
+    return 2;
+  }
+  if (rows == 0) return 0;
+  if (N > 64 && K > kPjResMaxK2) {
+    set_error("bfmm_rows_gemm_max: K=%d > %d with N=%d > 64", K, kPjResMaxK2, N);
+    return 2;
+  }
+  return rows_gemm_res(A, rows, K, K, B, N, C, alpha, zmax, as_stream(stream));
 }
 
 extern "C" int bfmm_rows_gemm_i8(const double *A, int64_t rows, int K, const int8_t *bdig,

@@ -764,6 +764,14 @@ class FmmEvaluator:
                     moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, dg.data_ptr(),
                     pw.data_ptr(), rp, z[lo * m * rp:].data_ptr(), 1.0,
                     zmax.data_ptr() if zmax is not None else None, st), "bfmm_rows_gemm_i8(V)")
+            elif (m == 1 and self._level_engine(lev, m, rp) == "i8" and p3 <= 128
+                  and (rp <= 64 or p3 <= 80) and nloc >= 8 * 148 * 64):
+                # big level, one column: the persistent projection also
+                # returns max |z|, the int8 M2L's digit scale (no absmax pass)
+                zmax = torch.zeros(1, dtype=torch.int64, device=self.device)
+                _native.check(self.lib.bfmm_rows_gemm_max(
+                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                    z[lo * m * rp:].data_ptr(), 1.0, zmax.data_ptr(), st), "bfmm_rows_gemm_max(V)")
             else:
                 _native.check(self.lib.bfmm_rows_gemm(
                     moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
