@@ -45,6 +45,56 @@ __device__ __forceinline__ void weights_s(const double *sS, const double *sN, in
   }
 }
 
+// weights_s at two coordinates (a leaf's and its parent's frame) sharing
+// every basis load from shared memory; same arithmetic per output as
+// weights_s (bitwise equal to two calls)
+template <int P>
+__device__ __forceinline__ void weights2_s(const double *sS, const double *sN, int scheme,
+                                           double x, double y, double *w, double *v) {
+  if (scheme == 0) {
+    x = fmin(1.0, fmax(-1.0, x));
+    y = fmin(1.0, fmax(-1.0, y));
+    double T[P], U[P];
+    T[0] = 1.0;
+    U[0] = 1.0;
+    if (P > 1) {
+      T[1] = x;
+      U[1] = y;
+    }
+#pragma unroll
+    for (int n = 2; n < P; ++n) {
+      T[n] = fma(2.0 * x, T[n - 1], -T[n - 2]);
+      U[n] = fma(2.0 * y, U[n - 1], -U[n - 2]);
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      double s = 0.0, t = 0.0;
+#pragma unroll
+      for (int n = 0; n < P; ++n) {
+        const double b = sS[n * P + j];
+        s = fma(T[n], b, s);
+        t = fma(U[n], b, t);
+      }
+      w[j] = s;
+      v[j] = t;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      double a = 1.0, b = 1.0;
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        if (k != j) {
+          const double nk = sN[k], f = sS[j * P + k];
+          a *= (x - nk) * f;
+          b *= (y - nk) * f;
+        }
+      w[j] = a;
+      v[j] = b;
+    }
+  }
+}
+
 template <int P>
 __device__ __forceinline__ void stage_basis(const Interp &ip, double *sS, double *sN) {
   // static indices into the parameter block (a dynamic index would make the
@@ -732,13 +782,12 @@ p2m_pair_kernel(const double *__restrict__ pts4, const double *__restrict__ ws,
         const int cx = 2 * px + ((ch >> 2) & 1), cy = 2 * py + ((ch >> 1) & 1),
                   cz = 2 * pz + (ch & 1);
         double *row = sw + t * R;
-        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], g.h, inv_hw, cx, flag), row);
-        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], g.h, inv_hw, cy, flag), row + P);
-        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], g.h, inv_hw, cz, flag),
-                     row + 2 * P);
-        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], hp, inv_hp, px, flag), row + 3 * P);
-        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], hp, inv_hp, py, flag), row + 4 * P);
-        weights_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], hp, inv_hp, pz, flag), row + 5 * P);
+        weights2_s<P>(sS, sN, ip.scheme, ref_coord_m(x.x, g.lo[0], g.h, inv_hw, cx, flag),
+                      ref_coord_m(x.x, g.lo[0], hp, inv_hp, px, flag), row, row + 3 * P);
+        weights2_s<P>(sS, sN, ip.scheme, ref_coord_m(x.y, g.lo[1], g.h, inv_hw, cy, flag),
+                      ref_coord_m(x.y, g.lo[1], hp, inv_hp, py, flag), row + P, row + 4 * P);
+        weights2_s<P>(sS, sN, ip.scheme, ref_coord_m(x.z, g.lo[2], g.h, inv_hw, cz, flag),
+                      ref_coord_m(x.z, g.lo[2], hp, inv_hp, pz, flag), row + 2 * P, row + 5 * P);
         row[6 * P] = ws[i];
       }
       __syncwarp();
