@@ -125,7 +125,6 @@ struct JitKernel {
   CUfunction group;
   CUfunction tile;
   CUfunction tile1;
-  CUfunction tile2;
 };
 
 std::mutex g_jit_mu;
@@ -188,7 +187,6 @@ int jit_compile(int kind, const char *expr, int *handle) {
   names.push_back("bfmm_nf::p2p_group_kernel<bfmm_nf::KUser>");
   names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser, 0>");
   names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser, 1>");
-  names.push_back("bfmm_nf::p2p_tile_kernel<bfmm_nf::KUser, 2>");
   for (auto &n : names) nvrtcAddNameExpression(prog, n.c_str());
   std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--std=c++17",
                                     "-default-device", "-lineinfo"};
@@ -239,7 +237,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     return 3;
   }
   JitKernel jk;
-  for (int i = 0; i < 13; ++i) {
+  for (int i = 0; i < 12; ++i) {
     CUfunction f;
     if (d.ModuleGetFunction(&f, mod, lowered[i].c_str()) != CUDA_SUCCESS) {
       set_error("bfmm_kernel_compile: missing %s", names[i].c_str());
@@ -252,8 +250,7 @@ int jit_compile(int kind, const char *expr, int *handle) {
     else if (i == 8) jk.block = f;
     else if (i == 9) jk.group = f;
     else if (i == 10) jk.tile = f;
-    else if (i == 11) jk.tile1 = f;
-    else jk.tile2 = f;
+    else jk.tile1 = f;
   }
   g_jit.push_back(jk);
   *handle = kFirstJit + (int)g_jit.size() - 1;
@@ -641,7 +638,7 @@ static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_sta
   // BFMM_TILE_MODE=0 (diagnostic): one thread per target (bitwise equal to
   // p2p_group_kernel); default 1: a warp per target cell
   const char *tm = getenv("BFMM_TILE_MODE");
-  const int mode = (tm && tm[0] == '0') ? 0 : (tm && tm[0] == '1') ? 1 : 2;
+  const int mode = (tm && tm[0] == '0') ? 0 : 1;
   bfmm_nf::Args a = make_args(tpts4, nullptr, nullptr, nullptr, nullptr, spts4, nullptr, 1,
                                scell_start, scell_count, levels, out, nullptr);
   const int64_t tiles = ceil_div(cell_hi, 64) - cell_lo / 64;
@@ -654,8 +651,7 @@ static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_sta
   int sm = small_max;
   const int *cs = tcell_start, *cc = tcell_count;
 #define BFMM_TILE(KK)                                                                     \
-  (mode == 2 ? (bfmm_nf::p2p_tile_kernel<KK, 2><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm)) \
-   : mode == 1 ? (bfmm_nf::p2p_tile_kernel<KK, 1><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm)) \
+  (mode == 1 ? (bfmm_nf::p2p_tile_kernel<KK, 1><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm)) \
              : (bfmm_nf::p2p_tile_kernel<KK, 0><<<grid, block, 0, st>>>(a, cs, cc, lo, hi, sm)))
   switch (handle) {
     case 1: BFMM_TILE(KLaplace); break;
@@ -675,7 +671,7 @@ static int launch_tile(int handle, const double *tpts4, const int32_t *tcell_sta
         jk = g_jit[handle - kFirstJit];
       }
       void *params[] = {&a, &cs, &cc, &lo, &hi, &sm};
-      if (driver().LaunchKernel(mode == 2 ? jk.tile2 : mode == 1 ? jk.tile1 : jk.tile, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
+      if (driver().LaunchKernel(mode == 1 ? jk.tile1 : jk.tile, grid.x, 1, 1, block.x, 1, 1, 0, (CUstream)st, params,
                                 nullptr) != CUDA_SUCCESS) {
         set_error("p2p_tile_kernel: cuLaunchKernel failed");
         return 1;
