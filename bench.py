@@ -325,9 +325,10 @@ def m2l_i8_ops(lev, rp, m, S):
     n = 1 << lev
     kc, ntn = -(-rp // 32), -(-rp // 64)
     per_stage = 2.0 * 128 * 64 * 32 * S * (S + 1) / 2
-    if _pair_kernel(lev, S):
-        # m2l_i8p2_kernel: digit pairs (2k, 2k+1) per MMA, 24 products (the
-        # 21 of a + b < 6 plus 3 that land in a dropped accumulator)
+    if _pair_kernel(lev, S) and os.environ.get("BFMM_I8P2_N128") == "1":
+        # unsplit m2l_i8p2_kernel: digit pairs (2k, 2k+1) per MMA, 24 products
+        # (the 21 of a + b < 6 plus 3 that land in a dropped accumulator); the
+        # default split variant runs those three as N = 64 MMAs: exactly 21
         per_stage = 2.0 * 128 * 64 * 32 * 24
     if lev >= 4:
         h = n // 2

@@ -15,6 +15,13 @@
 // ~138).  Accumulator d = a + b keeps the single-CTA TMEM layout (64
 // columns per digit sum), so the drain is the same.
 //
+// SPLIT (the default): the three pairs with a + 2k = 5 drop their wasted
+// half instead -- they run as N = 64 MMAs of digit 2k alone, whose B half
+// from CTA r is rank rows 32r .. 32r+31 of digit 2k.  Each CTA therefore
+// also stages those half planes of digits 0, 2, 4 (3 KB more per stage):
+// 9 MMAs of N = 128 + 3 of N = 64, exactly the 21 digit products (12.5 %
+// less tensor work per stage), bitwise the same accumulators 0..5.
+//
 // Synchronisation: only the leader (cluster rank 0) issues MMAs.  Both CTAs'
 // plane-producer warps arrive on the LEADER's plane-full barrier (count 8,
 // shared::cluster addresses); each CTA's core-block loader waits for its own
@@ -84,14 +91,16 @@ __device__ __forceinline__ void commit_pair(uint64_t *bar) {
 // then the TMEM drain, 6 forwards each landed core block to the leader
 constexpr int kI8P2Threads = 224;
 
-template <int NBMAX>
+template <int NBMAX, bool SPLIT>
 struct I8P2Shape {
   static constexpr int S = 6, XT = 1, YT = 16;
   static constexpr int ROWS = (YT + 4) * XT * 12;
   static constexpr int HALF = ROWS * 16;
   static constexpr int PLANE = S * 2 * HALF;
   static constexpr int B_PLANE = kI8TN * 32;  // one digit plane, 64 rank rows x 32 k
-  static constexpr int B_STAGE = 3 * B_PLANE;  // this CTA's three digits
+  static constexpr int B_HALF = B_PLANE / 2;   // 32 rank rows of one digit
+  // this CTA's three digits (+ its halves of digits 0, 2, 4 when SPLIT)
+  static constexpr int B_STAGE = 3 * B_PLANE + (SPLIT ? 3 * B_HALF : 0);
   static constexpr int BUDGET = BFMM_I8P_SMEM_KB * 1024 - 512;
   static constexpr int NP = 3;
   static constexpr int NB_FIT = (BUDGET - NP * PLANE) / B_STAGE;
@@ -102,13 +111,13 @@ struct I8P2Shape {
 
 // NBMAX = 12: the whole SM's shared memory; NBMAX = 6 (BFMM_I8_COSCHED):
 // ~176 KB, leaving room for one near-field tile CTA beside it on each SM
-template <int NBMAX>
+template <int NBMAX, bool SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8P2Threads, 1)
 m2l_i8p2_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restrict__ zmax,
                 const int8_t *__restrict__ cs, const double *__restrict__ cpow,
                 double *__restrict__ lt, int level, int m, int rp, int kc_n, int ntn,
                 int nsplit, int4 box) {
-  using Sh = I8P2Shape<NBMAX>;
+  using Sh = I8P2Shape<NBMAX, SPLIT>;
   constexpr int S = Sh::S, NP = Sh::NP, NB = Sh::NB, YT = Sh::YT, XT = Sh::XT;
   extern __shared__ __align__(1024) uint8_t smp[];
   uint8_t *const planes = smp;
@@ -207,6 +216,15 @@ m2l_i8p2_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restr
             for (int a = 0; a < S; ++a) {
 #pragma unroll
               for (int k = 0; 2 * k + a < S; ++k) {
+                if (SPLIT && 2 * k + a == S - 1) {
+                  // digit 2k alone (N = 64): rank rows 0-31 from CTA 0's
+                  // half plane, 32-63 from CTA 1's -> accumulator S - 1
+                  mma_i8_pair(tmem + (uint32_t)((a + 2 * k) * kI8TN),
+                              dA + (uint64_t)((a * 2 * Sh::HALF) >> 4),
+                              dBs + (uint64_t)((3 * Sh::B_PLANE + k * Sh::B_HALF) >> 4),
+                              bfmm::tc::idesc_i8(256, 64), (!first || a > 0) ? 1u : 0u);
+                  continue;
+                }
                 // rows 0-63 of B: digit 2k (CTA 0's plane k), rows 64-127:
                 // digit 2k + 1 (CTA 1's plane k) -> accumulators a+2k, a+2k+1
                 mma_i8_pair(tmem + (uint32_t)((a + 2 * k) * kI8TN),
@@ -251,6 +269,13 @@ m2l_i8p2_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restr
           for (int j = 0; j < 3; ++j)  // digits 2j + rank
             bulk_g2s(bring + bs * Sh::B_STAGE + j * Sh::B_PLANE,
                      blk + (2 * j + (int)rank) * Sh::B_PLANE, Sh::B_PLANE, &bfull[bs]);
+          if (SPLIT) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j)  // rank rows 32 rank .. of digit 2j
+              bulk_g2s(bring + bs * Sh::B_STAGE + 3 * Sh::B_PLANE + j * Sh::B_HALF,
+                       blk + 2 * j * Sh::B_PLANE + (int)rank * Sh::B_HALF, Sh::B_HALF,
+                       &bfull[bs]);
+          }
           if (++bs == NB) {
             bs = 0;
             bph ^= 1u;
@@ -358,22 +383,28 @@ inline bool i8p2_ok(const I8Call &a, int4 *box) {
   return (box->w & 1023) % 2 == 0;
 }
 
-template <int NBMAX>
+template <int NBMAX, bool SPLIT>
 int launch_i8p2_nb(const I8Call &a, int4 box) {
-  using Sh = I8P2Shape<NBMAX>;
+  using Sh = I8P2Shape<NBMAX, SPLIT>;
   static unsigned long long attr_set = 0;
   if (first_on_device(&attr_set)) {
-    cudaFuncSetAttribute(m2l_i8p2_kernel<NBMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Sh::smem);
+    cudaFuncSetAttribute(m2l_i8p2_kernel<NBMAX, SPLIT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem);
   }
   const int tiles = (box.w >> 20) * ((box.w >> 10) & 1023) * (box.w & 1023);
   dim3 grid((unsigned)tiles * 8, (unsigned)(a.ntn * a.m), a.nsplit);
-  m2l_i8p2_kernel<NBMAX><<<grid, kI8P2Threads, Sh::smem, a.st>>>(
+  m2l_i8p2_kernel<NBMAX, SPLIT><<<grid, kI8P2Threads, Sh::smem, a.st>>>(
       a.zs, a.zmax, a.cs, a.cpow, a.lt, a.level, a.m, a.rp, a.kc_n, a.ntn, a.nsplit, box);
   return check_launch("m2l_i8p2_kernel");
 }
 
+// BFMM_I8P2_N128=1: the unsplit variant (24 products, 12 N = 128 MMAs)
 inline int launch_i8p2(const I8Call &a, int4 box) {
   const char *cs = getenv("BFMM_I8_COSCHED");
-  return (cs && cs[0] == '1') ? launch_i8p2_nb<6>(a, box) : launch_i8p2_nb<12>(a, box);
+  const char *un = getenv("BFMM_I8P2_N128");
+  if (un && un[0] == '1')
+    return (cs && cs[0] == '1') ? launch_i8p2_nb<6, false>(a, box)
+                                : launch_i8p2_nb<12, false>(a, box);
+  return (cs && cs[0] == '1') ? launch_i8p2_nb<6, true>(a, box)
+                              : launch_i8p2_nb<12, true>(a, box);
 }

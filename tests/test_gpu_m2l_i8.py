@@ -128,6 +128,28 @@ def test_i8_plane_and_gather_kernels_agree_bitwise(level, rp, m, S):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("level,rp,m", [(5, 64, 1), (5, 96, 2), (6, 64, 1)])
+def test_i8_cta_pair_variants_agree_bitwise(level, rp, m, monkeypatch):
+    """Six 8-bit digits at dense levels >= 5 run the CTA-pair kernel
+    (m2l_i8p2_kernel).  Its default form issues the three a + 2k = 5 digit
+    pairs as N = 64 MMAs (exactly the 21 products); the unsplit form
+    (BFMM_I8P2_N128) runs 24 and drops 3 in an unread accumulator; the
+    single-CTA plane kernel (BFMM_I8_1CTA) runs the 21 one CTA at a time.
+    Same integer sums in accumulators 0..5, so all three are bitwise equal."""
+    outs = []
+    for env in ({}, {"BFMM_I8P2_N128": "1"}, {"BFMM_I8_1CTA": "1"}):
+        for k in ("BFMM_I8P2_N128", "BFMM_I8_1CTA"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        got, ref, lt = _run_both(level, rp, m, 6, 1, bits=8)
+        for c in range(m):
+            assert rel_l2(got[c::m], ref[c::m]) < 2.0 ** (10 - 8 * 6)
+        outs.append(lt)
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[2])
+
+
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C5", 3), ("C4", 2)])
 @pytest.mark.parametrize("mode,S", [("dmma", 7), ("i8", 6), ("i8", 7), ("i8", 8)])
 def test_m2l_engines_match_reference(name, scale, mode, S, cache_dir):
