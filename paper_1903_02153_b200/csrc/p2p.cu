@@ -21,8 +21,8 @@ namespace {
 // eval_fast: the hot-loop body; bodies with exp use the flagged fast exp
 // (bfmm_exp_fast), the others are eval itself.
 struct KLaplace {
-  // cheap body: keep 6 CTAs/SM (<= 80 registers) for latency-bound sparse leaves
-  static constexpr int kMinBlocks = 6;
+  // cheap body: keep 5 CTAs/SM (<= 96 registers) for latency-bound sparse leaves
+  static constexpr int kMinBlocks = 5;
   __device__ __forceinline__ static double eval(double dx, double dy, double dz) {
     const double r2 = dx * dx + dy * dy + dz * dz;
     return r2 == 0.0 ? 0.0 : rsqrt(r2);
@@ -34,6 +34,15 @@ struct KLaplace {
     const double v = bfmm_nf::bfmm_rsqrt_fast(r2, b);
     bfmm_nf::flag_set(bad, b && r2 != 0.0);
     return r2 == 0.0 ? 0.0 : v;
+  }
+  // flag-free hot-loop body (p2p.cuh, bfmm_rsqrt_raw)
+  static constexpr bool kAccFlag = true;
+  template <bool ZT>
+  __device__ __forceinline__ static void accum_fast(double dx, double dy, double dz, double w,
+                                                    double &acc) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    const double v = bfmm_nf::bfmm_rsqrt_raw(r2);
+    if (!ZT || bfmm_nf::bfmm_nonzero_bits(r2)) acc = fma(v, w, acc);
   }
 };
 // 1/r^4, r = 0 -> 0
@@ -49,6 +58,14 @@ struct KLaplaceForce {
     const double v = bfmm_nf::bfmm_rcp_fast(r2 * r2, b);
     bfmm_nf::flag_set(bad, b && r2 != 0.0);
     return r2 == 0.0 ? 0.0 : v;
+  }
+  static constexpr bool kAccFlag = true;
+  template <bool ZT>
+  __device__ __forceinline__ static void accum_fast(double dx, double dy, double dz, double w,
+                                                    double &acc) {
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    const double v = bfmm_nf::bfmm_rcp_raw(r2 * r2);
+    if (!ZT || bfmm_nf::bfmm_nonzero_bits(r2)) acc = fma(v, w, acc);
   }
 };
 // exp(-r^2)
@@ -339,20 +356,24 @@ int launch_locate(int handle, const bfmm_nf::Args &a,
   return check_launch("locate_kernel");
 }
 
-// 32-target chunks per target leaf; leaves outside [cell_lo, cell_hi) (other
-// ranks' shards) get none.
+// Work units per target leaf: 32-target chunks, or (wide, one weight column)
+// 64-target units while the leaf has 64 left and 32-target chunks for the
+// remainder (p2p_kernel decodes the same split); leaves outside
+// [cell_lo, cell_hi) (other ranks' shards) get none.
 __global__ void chunk_counts_kernel(const int64_t *__restrict__ counts,
                                     const int64_t *__restrict__ leaves,
                                     const int64_t *__restrict__ n_leaves,
                                     int64_t max_leaves, int64_t cell_lo,
-                                    int64_t cell_hi, int small_max,
+                                    int64_t cell_hi, int small_max, int wide,
                                     int64_t *__restrict__ nch) {
   // leaves of <= small_max points go to p2p_group_kernel instead
   const int64_t nl = *n_leaves;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
        i < max_leaves; i += int64_t(gridDim.x) * blockDim.x)
     nch[i] = (i < nl && leaves[i] >= cell_lo && leaves[i] < cell_hi && counts[i] > small_max)
-                 ? (counts[i] + 31) / 32 : 0;
+                 ? (wide ? (counts[i] >> 6) + (((counts[i] & 63) + 31) >> 5)
+                         : (counts[i] + 31) / 32)
+                 : 0;
 }
 
 // chunk -> leaf map from the inclusive chunk prefix (entries past cap are
@@ -515,6 +536,7 @@ bfmm_nf::Args make_args(const double *tpts4, const int64_t *tleaves,
   a.work_ctr = nullptr;
   a.chunk_leaf = nullptr;
   a.chunk_cap = 0;
+  a.wide = m == 1 ? 1 : 0;  // must match chunk_counts_kernel's unit split
   return a;
 }
 
@@ -716,7 +738,8 @@ static int p2p_impl(int handle, const double *tpts4, const int64_t *tleaves,
   chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_tleaves, 256),
                                                     kNumSMs * 16),
                         256, 0, st>>>(tcounts, tleaves, n_tleaves, max_tleaves,
-                                      cell_lo, cell_hi, m == 1 ? kSmallLeaf : 0, nch);
+                                      cell_lo, cell_hi, m == 1 ? kSmallLeaf : 0, m == 1 ? 1 : 0,
+                                      nch);
   if (check_launch("chunk_counts_kernel")) return 1;
   if (m == 1) {
     // one weight column: leaves of <= kSmallLeaf points (sparse clouds: C5's
@@ -922,7 +945,7 @@ extern "C" int bfmm_p2p_symmetric(int handle, const double *pts4,
   int64_t *incl = nch + max_leaves;
   chunk_counts_kernel<<<(unsigned)std::min<int64_t>(ceil_div(max_leaves, 256), kNumSMs * 16),
                         256, 0, st>>>(counts, leaves, n_leaves, max_leaves, cell_lo, cell_hi,
-                                      0, nch);
+                                      0, 1, nch);
   if (check_launch("chunk_counts_kernel")) return 1;
   size_t cb = chunk - cub_off;
   if (cub::DeviceScan::InclusiveSum(base + cub_off, cb, nch, incl, (int)max_leaves, st) !=

@@ -332,6 +332,69 @@ def test_exp_out_of_range_arguments(expr, edge, cache_dir):
             ev.evaluate(pts, weights=w)
 
 
+def _near_brute(pts, tgt, w, levels, fn):
+    """Brute-force near field on the unit cube: sources in the 27 neighbour
+    leaves of each target, K(0) = 0 (kernel.py:149-180)."""
+    n = 1 << levels
+    cs = np.clip(np.floor(pts * n).astype(np.int64), 0, n - 1)
+    ct = np.clip(np.floor(tgt * n).astype(np.int64), 0, n - 1)
+    out = np.zeros(len(tgt))
+    for i0 in range(0, len(tgt), 400):
+        d2 = ((tgt[i0:i0 + 400, None, :] - pts[None, :, :]) ** 2).sum(-1)
+        near = (np.abs(ct[i0:i0 + 400, None, :] - cs[None, :, :]) <= 1).all(-1)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            kv = np.where(d2 == 0.0, 0.0, fn(d2))
+        out[i0:i0 + 400] = (np.where(near, kv, 0.0) * w[None, :]).sum(1)
+    return out
+
+
+@pytest.mark.parametrize("kname,distinct", [("laplacian", False), ("laplacianforce", False),
+                                            ("laplacian", True), ("laplacianforce", True)])
+def test_singular_kernels_crowded_leaves_and_coincident_points(kname, distinct, cache_dir):
+    """The flag-free 1/r and 1/r^4 bodies (csrc/p2p.cuh, accum_fast): leaves
+    of hundreds of points (64-target wide units plus 32-target remainders),
+    exact duplicates inside a leaf (r = 0 contributes 0, kernel.py:149-180)
+    and -- with distinct targets -- targets that coincide with sources."""
+    gen = np.random.default_rng(77)
+    crowd = np.clip(0.55 + 0.02 * gen.standard_normal((2500, 3)), 0.0, 1.0 - 1e-12)
+    pts = np.vstack([crowd, gen.random((3000, 3)), crowd[:40], crowd[100:103]])
+    w = gen.standard_normal(len(pts))
+    fn = (lambda d2: 1.0 / np.sqrt(d2)) if kname == "laplacian" else (lambda d2: 1.0 / (d2 * d2))
+    kern = bf.LAPLACIAN if kname == "laplacian" else workload_kernel("laplacianforce")
+    ev = bf.FmmEvaluator(kern, small_plan(levels=3, order=3), cache_dir=cache_dir)
+    ev._disable_far_field = True
+    if distinct:
+        tgt = np.vstack([pts[5:900:3], gen.random((700, 3)), crowd[2000:2200]])
+        got = ev.evaluate(pts, targets=tgt, weights=w)
+    else:
+        tgt = pts
+        got = ev.evaluate(pts, weights=w)
+    ref = _near_brute(pts, tgt, w, 3, fn)
+    assert np.all(np.isfinite(got))
+    assert rel_l2(got, ref) < 1e-12
+
+
+def test_laplace_subnormal_distances_take_exact_path(cache_dir):
+    """Pairs whose r^2 is subnormal (points ~1e-160 apart next to the origin)
+    break the hardware rsqrt seed (flush-to-zero): the sum turns non-finite,
+    which is the flag that sends the tile through the exact body."""
+    gen = np.random.default_rng(78)
+    pts = gen.random((2000, 3))
+    # on one axis, so r^2 = dx * dx is a single rounding on both sides
+    tiny = np.array([[0.0, 0.0, 0.0], [1e-160, 0.0, 0.0], [3e-160, 0.0, 0.0],
+                     [7e-160, 0.0, 0.0]])
+    pts = np.vstack([pts, tiny])
+    w = gen.standard_normal(len(pts))
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(levels=3, order=3), cache_dir=cache_dir)
+    ev._disable_far_field = True
+    got = ev.evaluate(pts, weights=w)
+    ref = _near_brute(pts, pts, w, 3, lambda d2: 1.0 / np.sqrt(d2))
+    assert np.all(np.isfinite(got))
+    # elementwise: the four tiny targets sum three ~1e160 terms of mixed sign
+    assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-10
+    assert np.max(np.abs(got[-4:])) > 1e150
+
+
 def test_rejects_bad_inputs(cache_dir):
     pts, w = unit_cloud(100, seed=0)
     ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
