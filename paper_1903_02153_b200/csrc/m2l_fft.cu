@@ -400,6 +400,129 @@ stencil2_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int leve
     }
 }
 
+// ---- 2c. the stencil with both z parities per thread (the default) -----------
+// ncu on full C3 (profiles/r02_ncu_c3_stencil_variants.txt): stencil_kernel
+// keeps the shared-memory data pipe 85 % busy -- 40 % of its wavefronts are
+// bank-conflict replays (a wavefront serves lanes with distinct 16-byte
+// slots mod 8 across the WHOLE warp, and its 16 distinct source addresses
+// all fall on even slots) -- and spends a quarter of its instructions on the
+// per-element halo index arithmetic.  Here
+//  * a thread owns 4 CONSECUTIVE z targets (both parities) of its (x, y):
+//    the 8 sources of an (a, b) column feed 24 complex MACs and the 7 taps
+//    c = -3..3 of the column serve both parities (15 LDS.128 per 96 DFMAs
+//    instead of 18);
+//  * the y parity takes over the role z parity plays in stencil_kernel: a
+//    lane pair (py = 0, 1) reads the SAME source column y0 + 2 jy + 3 + b'
+//    with taps b = b' - py (octree.py:128-145), so the +-3 skips stay
+//    divergence-free;
+//  * halo rows are skewed by one slot for every other x pair
+//    (z index + ((hx >> 1) & 1), rows of 15), so the 16 distinct source
+//    addresses of a warp -- 4 y (stride 30 = 6 mod 8) x 4 x -- cover every
+//    slot exactly twice: 2 wavefronts per LDS.128, the minimum;
+//  * a thread copies whole halo rows (14 contiguous values, immediate
+//    offsets) instead of one element per loop trip.
+// Tile 8 x 8 x 8, 128 threads: warp = (z half, x parity), lane = (py, jy, jx).
+// Same taps in the same per-target order (a, b, c ascending) as
+// stencil_kernel: bitwise-equal spectra (only zero taps are skipped
+// differently).
+constexpr int kH3ZP = kHZ + 1;  // 15: odd z stride + room for the skew; y needs no padding
+constexpr int kZT = 4;          // z targets per thread
+__global__ void __launch_bounds__(128, 4)
+stencil3_kernel(const double2 *__restrict__ X, double2 *__restrict__ Y, int level, int F,
+                const double2 *__restrict__ S, const short *__restrict__ tap_index,
+                int64_t cell_lo, int64_t cell_hi) {
+  extern __shared__ double2 sm2[];
+  auto halo = reinterpret_cast<double2 (*)[kHY][kH3ZP]>(sm2);                  // [kHX][kHY][kH3ZP]
+  auto taps = reinterpret_cast<double2 (*)[7][7]>(sm2 + kHX * kHY * kH3ZP);   // [7][7][7]
+  const int n = 1 << level;
+  const int64_t ncell = int64_t(1) << (3 * level);
+  const int tilesx = (n + kTX - 1) / kTX, tilesy = (n + kTY - 1) / kTY;
+  const int tile = blockIdx.x;
+  const int tz = tile / (tilesx * tilesy), trem = tile - tz * tilesx * tilesy;
+  const int x0 = (trem / tilesy) * kTX, y0 = (trem % tilesy) * kTY, z0 = tz * kTZ;
+  const int f = blockIdx.y, col = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int px = w & 1, zb = kZT * (w >> 1), py = lane & 1;
+  const int ix = px + 2 * ((lane >> 3) & 3), iy = py + 2 * ((lane >> 1) & 3);
+  const int x = x0 + ix, y = y0 + iy;
+  // shard filter: skip the tile when none of its targets is ours
+  if (cell_lo > 0 || cell_hi < ncell) {
+    bool mine = false;
+#pragma unroll
+    for (int k = 0; k < kZT; ++k) {
+      const int z = z0 + zb + k;
+      if (x < n && y < n && z < n) {
+        const int64_t id = (int64_t)morton3(x, y, z);
+        mine |= id >= cell_lo && id < cell_hi;
+      }
+    }
+    if (!__syncthreads_or(mine)) return;
+  }
+  const double2 *Xf = X + ((int64_t)col * F + f) * ncell;
+  for (int r = tid; r < kHX * kHY; r += 128) {
+    const int hx = r / kHY, hy = r - hx * kHY;
+    const int sx = x0 + hx - 3, sy = y0 + hy - 3;
+    const bool vr = sx >= 0 && sx < n && sy >= 0 && sy < n;
+    const double2 *row = Xf + (vr ? lex_of(sx, sy, 0, n) : 0);
+    double2 *dst = &halo[hx][hy][(hx >> 1) & 1];
+#pragma unroll
+    for (int hz = 0; hz < kHZ; ++hz) {
+      const int sz = z0 + hz - 3;
+      const bool v = vr && sz >= 0 && sz < n;
+      cp_async16z(dst + hz, row + (v ? sz : 0), v);
+    }
+  }
+  for (int e = tid; e < 343; e += 128) {
+    const int t = tap_index[e];
+    cp_async16z(&taps[0][0][0] + e, t >= 0 ? S + (int64_t)t * F + f : S, t >= 0);
+  }
+  cp_async_all();
+  __syncthreads();
+  double2 acc[kZT];
+#pragma unroll
+  for (int k = 0; k < kZT; ++k) acc[k] = make_double2(0.0, 0.0);
+  // target z0 + zb + zi (zi = 2k + pz) takes c = c' - pz, c' in [-2, 3],
+  // from source z0 + zb + 2k + c' = seg[c' + 2 + 2k] with tap tp[c + 3]
+#pragma unroll 1
+  for (int ap = -2; ap <= 3; ++ap) {
+    const int a = ap - px;
+    const int hx = ix + 3 + a;
+#pragma unroll 2
+    for (int bp = -2; bp <= 3; ++bp) {
+      const int b = bp - py;
+      double2 seg[kZT + 4];
+      // source z0 + zb - 2 = halo z index zb + 1, plus the row's skew
+      const double2 *col_src = &halo[hx][iy + 3 + b][zb + 1 + ((hx >> 1) & 1)];
+#pragma unroll
+      for (int u = 0; u < kZT + 4; ++u) seg[u] = col_src[u];
+      const double2 *tp = &taps[a + 3][b + 3][0];
+      // zero taps |c| <= 1 of the near columns: skipped where the column is
+      // near for both y parities of the warp (b' in {0, 1})
+      const bool near_col = a >= -1 && a <= 1 && (bp == 0 || bp == 1);  // warp-uniform
+#pragma unroll
+      for (int c = -3; c <= 3; ++c) {
+        if (near_col && c >= -1 && c <= 1) continue;
+        const double2 s = tp[c + 3];
+#pragma unroll
+        for (int zi = 0; zi < kZT; ++zi) {
+          const int pz = zi & 1, cp = c + pz;
+          if (cp < -2 || cp > 3) continue;  // compile-time: the parity rule
+          const double2 v = seg[cp + 2 + (zi - pz)];
+          acc[zi].x = fma(s.x, v.x, fma(-s.y, v.y, acc[zi].x));
+          acc[zi].y = fma(s.x, v.y, fma(s.y, v.x, acc[zi].y));
+        }
+      }
+    }
+  }
+  double2 *Yf = Y + ((int64_t)col * F + f) * ncell;
+  if (x < n && y < n) {
+    double2 *dst = Yf + lex_of(x, y, z0 + zb, n);
+#pragma unroll
+    for (int k = 0; k < kZT; ++k)
+      if (z0 + zb + k < n) dst[k] = acc[k];
+  }
+}
+
 // ---- 3. inverse transform + crop + scale ------------------------------------
 template <int P, int G>
 __global__ void __launch_bounds__(128)
@@ -607,13 +730,17 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
   // BFMM_STENCIL=2: the two-x-targets-per-thread kernel (fewer halo
   // reads, but 85 KB tiles leave 2 CTAs/SM; measured slower on C3)
   const char *sv = getenv("BFMM_STENCIL");
-  const bool stencil1 = !(sv && sv[0] == '2');
+  const int stencil = sv && sv[0] >= '1' && sv[0] <= '3' ? sv[0] - '0' : 3;
+  const bool stencil1 = stencil == 1;
+  const size_t smem_s3 = sizeof(double2) * (kHX * kHY * kH3ZP + 343);
   static unsigned long long attr = 0;
   if (first_on_device(&attr)) {
     cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_s);
     cudaFuncSetAttribute(stencil2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_s2);
+    cudaFuncSetAttribute(stencil3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_s3);
   }
   for (int c0 = 0; c0 < m; c0 += cc) {
     const int ccur = std::min(cc, m - c0);
@@ -630,7 +757,12 @@ extern "C" int bfmm_m2l_fft(const double *moments, double *locals, int level,
 #undef BFMM_FFT_FWD
     }
     if (rc) return rc;
-    if (stencil1) {
+    if (stencil == 3) {
+      stencil3_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), 128, smem_s3, st>>>(
+          X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
+          8 * (q_lo + nq));
+      if (check_launch("stencil3_kernel")) return 1;
+    } else if (stencil1) {
       stencil_kernel<<<dim3(tiles, (unsigned)F, (unsigned)ccur), dim3(kTX, kTY, 2), smem_s, st>>>(
           X, Y, level, (int)F, reinterpret_cast<const double2 *>(symbols), taps, 8 * q_lo,
           8 * (q_lo + nq));

@@ -617,15 +617,20 @@ def test_leaf_pair_matches_separate_passes(name, scale, cache_dir):
         assert rel_l2(out["pair"][wl["check_idx"]], g["phi_idx"]) < PHI_TOL
 
 
-def test_stencil_two_targets_per_thread_bitwise(cache_dir, monkeypatch):
-    """stencil2_kernel (two x targets per thread, 16 x 8 x 8 tiles) against
-    stencil_kernel: same taps in the same order per target, so phi is
-    bitwise equal (uniform scheme, engine.py:258-292)."""
+def test_stencil_variants_bitwise(cache_dir, monkeypatch):
+    """The three FFT-M2L stencil kernels -- stencil_kernel (4 same-parity z
+    targets per thread), stencil2_kernel (two x targets per thread) and the
+    default stencil3_kernel (a whole z column per thread) -- apply the same
+    taps in the same order per target, so phi is bitwise equal (uniform
+    scheme, engine.py:258-292).  Level 5 has interior and boundary tiles;
+    level 2 (n = 4) is smaller than a tile."""
     pts, w = unit_cloud(30000, seed=91, ncols=3)
     plan = bf.FmmPlan(levels=5, order=4, scheme="uniform", eps=1e-6,
                       domain_center=(0.5, 0.5, 0.5), domain_length=1.0)
     ev = bf.FmmEvaluator(bf.EXPONENTIAL, plan, cache_dir=cache_dir)
-    a = ev.evaluate(pts, weights=w)
-    monkeypatch.setenv("BFMM_STENCIL", "2")
-    b = ev.evaluate(pts, weights=w)
-    assert np.array_equal(a, b)
+    out = {}
+    for mode in ("3", "1", "2"):
+        monkeypatch.setenv("BFMM_STENCIL", mode)
+        out[mode] = ev.evaluate(pts, weights=w)
+    assert np.array_equal(out["3"], out["1"])
+    assert np.array_equal(out["2"], out["1"])
