@@ -632,6 +632,7 @@ def rooflines(cfg, wl, ev, avg, peaks, near_pairs, step_ms, share=1.0):
     if dom != "p2p" and "p2p" in avg:
         # the near field's own roofline beside the dominant M2L's
         levels["p2p"] = p2p_roofline(wl, avg["p2p"], near_pairs, m, peaks)
+        levels["p2p"]["traffic"] = committed_traffic(cfg, "p2p")
         levels["p2p"].update({"kernel_ms": avg["p2p"], "share_of_step": avg["p2p"] / step_ms})
     ms = avg[dom]
     share = ms / step_ms
