@@ -712,10 +712,21 @@ inline int dispatch_leaf(int p, bool p2m, const LeafCall &a) {
 // the L-1 -> L L2L pass (a read-modify-write of the leaf locals) disappears.
 template <int P>
 constexpr int pair_warps() { return P <= 6 ? 4 : 2; }
+// tuning overrides (scripts/pair_sweep.sh): -DBFMM_PAIR_MINB / -DBFMM_PAIR_BATCH
+#ifdef BFMM_PAIR_MINB
+template <int P>
+constexpr int pair_minb() { return BFMM_PAIR_MINB; }
+#else
 template <int P>
 constexpr int pair_minb() { return P == 5 ? 4 : 2; }  // <= 128 registers for C5 (p = 5)
+#endif
+#ifdef BFMM_PAIR_BATCH
+template <int P>
+constexpr int pair_batch() { return BFMM_PAIR_BATCH; }
+#else
 template <int P>
 constexpr int pair_batch() { return P <= 6 ? 64 : 32; }  // points staged per pass
+#endif
 template <int P>
 constexpr size_t p2m_pair_smem() {
   return sizeof(double) * pair_warps<P>() * pair_batch<P>() * (6 * P + 1);

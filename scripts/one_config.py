@@ -11,6 +11,10 @@ import paper_1903_02153_b200 as bf  # noqa: E402
 from paper_1903_02153_b200 import workloads  # noqa: E402
 from paper_1903_02153_b200.kernel import workload_kernel  # noqa: E402
 
+import os  # noqa: E402
+if os.environ.get("BFMM_LIB"):  # a variant build of libbfmm.so (tuning sweeps)
+    from paper_1903_02153_b200 import _native
+    _native.load(os.environ["BFMM_LIB"])
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"
 scale = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 wl = workloads.make(name, scale)
