@@ -63,16 +63,18 @@ template <int P, int G>
 struct FftShape {
   static constexpr int p = P, q = 2 * P - 1, h = q / 2 + 1, F = q * q * h;
   static constexpr int P3 = p * p * p, PPH = p * p * h, PQH = p * q * h;
-  // forward: {in [G][p^3] real, B [G][p][q][h]} and {A [G][p][p][h], stage [F][G]}
-  // share storage (in dies before B is written, A before stage)
+  // forward: {in [G][p^3] real, B [G][p][q][h]} share storage (in dies
+  // before B is written), then A [G][p][p][h]; the x pass writes its bins
+  // straight to the spectrum (no [F][G] staging tile: lanes run over the G
+  // cells of a bin first, so a bin's G values still leave as one G * 16-byte
+  // run -- and the 46 KB the tile took at p = 6 buys two more CTAs per SM)
   static constexpr size_t U1 = (sizeof(double) * G * P3 > sizeof(double2) * G * PQH)
                                    ? sizeof(double) * G * P3 : sizeof(double2) * G * PQH;
-  static constexpr size_t U2 = (sizeof(double2) * G * PPH > sizeof(double2) * F * G)
-                                   ? sizeof(double2) * G * PPH : sizeof(double2) * F * G;
+  static constexpr size_t U2 = sizeof(double2) * G * PPH;
   static constexpr size_t smem = U1 + U2;
-  // inverse: {stage [F][G], D [G][p][p][h]} (stage dies before D is
-  // written) and C [G][p][q][h]
-  static constexpr size_t V1 = (F > PPH ? F : PPH) * sizeof(double2) * G;
+  // inverse: D [G][p][p][h] and C [G][p][q][h]; the x pass reads its q
+  // bins straight from the spectrum into registers
+  static constexpr size_t V1 = PPH * sizeof(double2) * G;
   static constexpr size_t smem_inv = V1 + sizeof(double2) * G * PQH;
   static constexpr size_t most = smem > smem_inv ? smem : smem_inv;
 };
@@ -105,7 +107,6 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
   double *in = reinterpret_cast<double *>(smraw);            // [G][p^3]
   double2 *B = reinterpret_cast<double2 *>(smraw);           // [G][p][q][h]
   double2 *A = reinterpret_cast<double2 *>(smraw + Sh::U1);  // [G][p][p][h]
-  double2 *stage = A;                                        // [F][G]
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
   const int64_t ngroups = ncell / G;
@@ -168,9 +169,12 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
       }
     }
     __syncthreads();
-    // x: p inputs -> q bins, into the [f][cell] staging tile; line (gi, ky, kz)
+    // x: p inputs -> q bins, straight into the [f][cell] spectrum; line
+    // (ky, kz, gi) with the cell index fastest across lanes: the G cells of
+    // a bin are one G * 16-byte run in global memory
+    double2 *dst = X + (int64_t)crel * F * ncell + lex0;
     for (int l = threadIdx.x; l < G * q * h; l += blockDim.x) {
-      const int gi = l / (q * h), rem = l - gi * q * h;
+      const int rem = l / G, gi = l - rem * G;
       const double2 *b = B + gi * PQH + rem;
       double2 v[p];
 #pragma unroll
@@ -184,14 +188,8 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
           re = fma(v[i].x, g.c[r], fma(v[i].y, g.s[r], re));
           im = fma(v[i].y, g.c[r], fma(-v[i].x, g.s[r], im));
         }
-        stage[(kx * q * h + rem) * G + gi] = make_double2(re, im);
+        dst[(int64_t)(kx * q * h + rem) * ncell + gi] = make_double2(re, im);
       }
-    }
-    __syncthreads();
-    double2 *dst = X + (int64_t)crel * F * ncell + lex0;
-    for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
-      const int f = e / G, gi = e - f * G;
-      dst[(int64_t)f * ncell + gi] = stage[e];
     }
   }
 }
@@ -544,8 +542,7 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
   constexpr int p = Sh::p, q = Sh::q, h = Sh::h, F = Sh::F;
   constexpr int P3 = Sh::P3, PPH = Sh::PPH, PQH = Sh::PQH;
   extern __shared__ __align__(16) unsigned char smraw[];
-  double2 *stage = reinterpret_cast<double2 *>(smraw);           // [F][G]
-  double2 *D = stage;                                            // [G][p][p][h]  y inverted, j < p
+  double2 *D = reinterpret_cast<double2 *>(smraw);               // [G][p][p][h]  y inverted, j < p
   double2 *C = reinterpret_cast<double2 *>(smraw + Sh::V1);      // [G][p][q][h]  x inverted, i < p
   const int n = 1 << level;
   const int64_t ncell = int64_t(1) << (3 * level);
@@ -562,20 +559,16 @@ fft_inv_kernel(const double2 *__restrict__ Y, int level, int64_t cell_lo, int64_
       any |= id >= cell_lo && id < cell_hi;
     }
     if (!any) continue;  // uniform across the CTA
-    __syncthreads();
+    __syncthreads();  // the previous run's readers of C and D are done
     const double2 *src = Y + (int64_t)crel * F * ncell + lex0;
-    for (int e = threadIdx.x; e < F * G; e += blockDim.x) {
-      const int f = e / G, gi = e - f * G;
-      cp_async16z(stage + e, src + (int64_t)f * ncell + gi, true);
-    }
-    cp_async_all();
-    __syncthreads();
-    // x: q bins -> p outputs, e^{+2 pi i i kx / q}; line (gi, ky, kz)
+    // x: q bins -> p outputs, e^{+2 pi i i kx / q}; line (ky, kz, gi), the
+    // cell index fastest across lanes (G * 16-byte runs), its q bins loaded
+    // from the spectrum into registers (all in flight at once)
     for (int l = threadIdx.x; l < G * q * h; l += blockDim.x) {
-      const int gi = l / (q * h), rem = l - gi * q * h;
+      const int rem = l / G, gi = l - rem * G;
       double2 v[q];
 #pragma unroll
-      for (int kx = 0; kx < q; ++kx) v[kx] = stage[(kx * q * h + rem) * G + gi];
+      for (int kx = 0; kx < q; ++kx) v[kx] = src[(int64_t)(kx * q * h + rem) * ncell + gi];
       double2 *dst = C + gi * PQH + rem;
 #pragma unroll
       for (int i = 0; i < p; ++i) {
