@@ -85,7 +85,7 @@ struct KExponential {
   }
   template <class F>
   __device__ __forceinline__ static double eval_fast(double dx, double dy, double dz, F &bad) {
-    return bfmm_nf::bfmm_exp_fast(-sqrt(dx * dx + dy * dy + dz * dz), bad);
+    return bfmm_nf::bfmm_exp_fast(-bfmm_nf::bfmm_sqrt_fast(dx * dx + dy * dy + dz * dz, bad), bad);
   }
 };
 // log r, r = 0 -> 0
@@ -151,22 +151,29 @@ std::unordered_map<std::string, int> g_jit_cache;  // source -> handle
 constexpr int kFirstJit = 6;
 
 std::string functor_source(int kind, const char *expr) {
-  std::string body;
-  if (kind == 0)
-    body = "const double r = sqrt(dx * dx + dy * dy + dz * dz);\n return (" +
-           std::string(expr) + ");";
-  else if (kind == 1)
-    body = "const double r2 = dx * dx + dy * dy + dz * dz;\n return (" +
-           std::string(expr) + ");";
-  else
-    body = "return (" + std::string(expr) + ");";
+  // body(fast): the prologue that defines r / r2 for the expression; the fast
+  // body takes r from the branch-free bfmm_sqrt_fast
+  auto body = [&](bool fast) {
+    std::string b;
+    if (kind == 0)
+      b = std::string("const double r = ") +
+          (fast ? "bfmm_sqrt_fast(dx * dx + dy * dy + dz * dz, bfmm_bad_)"
+                : "sqrt(dx * dx + dy * dy + dz * dz)") +
+          ";\n return (" + std::string(expr) + ");";
+    else if (kind == 1)
+      b = "const double r2 = dx * dx + dy * dy + dz * dz;\n return (" + std::string(expr) + ");";
+    else
+      b = "return (" + std::string(expr) + ");";
+    return b;
+  };
   // exp() in user expressions maps to the branch-free bfmm_exp (p2p.cuh);
-  // eval_fast uses the flagged fast path (bfmm_exp_fast)
+  // eval_fast uses the flagged fast paths (bfmm_exp_fast, bfmm_sqrt_fast)
   return "#define exp(x) bfmm_exp(x)\nstruct KUser {\n __device__ __forceinline__ "
          "static double eval(double dx, double dy, double dz) {\n " +
-         body + "\n }\n#undef exp\n#define exp(x) bfmm_exp_fast(x, bfmm_bad_)\n"
+         body(false) + "\n }\n#undef exp\n#define exp(x) bfmm_exp_fast(x, bfmm_bad_)\n"
+         "#define sqrt(x) bfmm_sqrt_fast(x, bfmm_bad_)\n"
          " template <class F> __device__ __forceinline__ static double eval_fast(double dx, "
-         "double dy, double dz, F &bfmm_bad_) {\n " + body + "\n }\n#undef exp\n};\n";
+         "double dy, double dz, F &bfmm_bad_) {\n " + body(true) + "\n }\n#undef exp\n#undef sqrt\n};\n";
 }
 
 int jit_compile(int kind, const char *expr, int *handle) {
