@@ -725,9 +725,12 @@ template <int P>
 constexpr int pair_batch() { return BFMM_PAIR_BATCH; }
 #else
 template <int P>
-constexpr int pair_batch() { return P <= 6 ? 48 : 32; }  // points staged per pass (48: 47.6 KB per
-                                                          // CTA at p = 5 -> 4 CTAs per SM; C5 P2M
-                                                          // 11.8 -> 9.9 ms against 64)
+constexpr int pair_batch() {  // points staged per pass
+  // p = 5: 48 points = 47.6 KB per CTA -> 4 CTAs per SM (C5 P2M 11.8 -> 9.9 ms
+  // against 64); p = 6 keeps 64 (C4's crowded leaves take several passes, each
+  // a read-modify-write of the moments: 48 measured 6.8 -> 8.1 ms there)
+  return P == 5 ? 48 : P <= 6 ? 64 : 32;
+}
 #endif
 template <int P>
 constexpr size_t p2m_pair_smem() {
