@@ -200,12 +200,17 @@ fft_fwd_kernel(const double *__restrict__ moments, int level, int m, int c0,
 // run 3 % slower, the kernel being shared-memory-latency bound)
 constexpr int kTX = 8, kTY = 8, kTZ = 8, kR = kTZ / 2;
 constexpr int kHX = kTX + 6, kHY = kTY + 6, kHZ = kTZ + 6;
-// Bank layout: an LDS.128 is served 8 lanes (one quarter-warp phase) at a
-// time, and those 8 lanes must hit 8 distinct 16-byte slots (mod 8).  A
-// phase's lanes vary z parity (stride 1) and 4 same-parity x positions
-// (stride 2 * HYP * HZP), so the halo is padded to HYP = 15, HZP = 15:
-// 2 * 15 * 15 = 450 = 2 (mod 8) -> slots {0,2,4,6} + {0,1}, conflict-free
-// (the unpadded 14 x 14 layout is 2-way conflicted).
+// Bank layout (round-1 reasoning): an LDS.128 is served 8 lanes (one
+// quarter-warp phase) at a time, and those 8 lanes must hit 8 distinct
+// 16-byte slots (mod 8).  A phase's lanes vary z parity (stride 1) and 4
+// same-parity x positions (stride 2 * HYP * HZP), so the halo is padded to
+// HYP = 15, HZP = 15: 2 * 15 * 15 = 450 = 2 (mod 8) -> slots {0,2,4,6} +
+// {0,1} (the unpadded 14 x 14 layout is 2-way conflicted).  ncu on full C3
+// showed the rule is warp-wide, not per phase: a wavefront serves any lanes
+// with distinct slots, this kernel's 16 distinct source addresses per warp
+// all fall on even slots, and 40 % of its shared-memory wavefronts are
+// conflict replays (profiles/r02_ncu_c3_stencil_variants.txt) -- what
+// stencil3_kernel's skewed layout fixes.  Kept as the bitwise reference.
 constexpr int kHYP = kHY + 1, kHZP = kHZ + 1;
 
 // grid: (tiles, frequencies, columns); block (8, 8, 2): thread (ix, iy, pz)
