@@ -92,6 +92,8 @@ def run(name):
            "rel_l2_vs_direct_1000": rel(phi_idx, d), "direct_seconds_gpu": dsec,
            "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9}
     gp = os.path.join(GOLD, f"{name.lower()}_s0.npz")
+    if not os.path.exists(gp):  # full-size C3 / C4 fixtures
+        gp = os.path.join(GOLD, f"{name.lower()}_full.npz")
     if os.path.exists(gp):
         g = np.load(gp)
         out["reference_rel_l2_vs_direct"] = float(g["rel_l2_vs_direct"])
