@@ -176,6 +176,15 @@ int bfmm_rows_gemm_scatter(const double *A, int64_t rows, int K,
                            const double *B, int N, double *C, double alpha,
                            double beta, int a_splits, const int64_t *groups,
                            int64_t group_rows, bfmm_stream_t stream);
+/* Rows of listed cells only, in place in the level's arrays: for
+ * r < rows, with cell row R = groups[r / group_rows] * group_rows +
+ * r % group_rows, C[R] = alpha * A[R] @ B (A and C both indexed by R; the
+ * other rows of C are not written).  The V projection z = M V of a sparse
+ * cloud (engine.py:233): only the cells with sources below them have
+ * moments, the caller zero-fills z once. */
+int bfmm_rows_gemm_cells(const double *A, int64_t rows, int K, const double *B, int N,
+                         double *C, double alpha, const int64_t *groups,
+                         int64_t group_rows, bfmm_stream_t stream);
 
 /* M2L Chebyshev (engine.py:228-256): for every cell c at `level` and
  * column, lt[c][i] = sum over the valid far offsets t of

@@ -40,6 +40,7 @@ SIGNATURES = {
     "bfmm_rows_gemm_i8": (_I, [_P, _I64, _I, _P, _P, _I, _P, _D, _P, _P]),
     "bfmm_rows_gemm_max": (_I, [_P, _I64, _I, _P, _I, _P, _D, _P, _P]),
     "bfmm_rows_gemm_scatter": (_I, [_P, _I64, _I, _P, _I, _P, _D, _D, _I, _P, _I64, _P]),
+    "bfmm_rows_gemm_cells": (_I, [_P, _I64, _I, _P, _I, _P, _D, _P, _I64, _P]),
     "bfmm_m2l_cheb_cells": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "bfmm_octant_histogram": (_I, [_P, _P, _I64, _P, _P]),
     "bfmm_group_by_octant_scratch_bytes": (_SZ, [_I64]),

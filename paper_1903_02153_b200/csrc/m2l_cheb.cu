@@ -186,7 +186,8 @@ template <int WN>
 __global__ void __launch_bounds__(128 * WN)
 proj_gemm_kernel(const double *__restrict__ A, int64_t rows, int64_t lda, int K,
                  const double *__restrict__ B, int N, double *__restrict__ C, double alpha,
-                 double beta, const int64_t *__restrict__ groups, int64_t group_rows) {
+                 double beta, const int64_t *__restrict__ groups, int64_t group_rows,
+                 int gather_a) {
   constexpr int TN = 64 * WN, NT = 8, LDB = pj_ldb<WN>(), NTH = 128 * WN;
   constexpr int A_ELEMS = kPjTM * kPjLDA, STAGE = A_ELEMS + kPjKC * LDB;
   constexpr int AEPT = kPjTM * kPjKC / NTH;  // A slots per thread
@@ -214,7 +215,9 @@ proj_gemm_kernel(const double *__restrict__ A, int64_t rows, int64_t lda, int K,
     for (int u = 0; u < AEPT; ++u) {
       const int64_t r = row0 + ar + u * AR_STEP;
       const bool v = akv && r < rows;
-      cp_async8(As + (ar + u * AR_STEP) * kPjLDA + ak, v ? A + r * lda + k0 + ak : A, v);
+      // gather_a: A rows live at their cells too (row map as for C)
+      const int64_t ra = (gather_a && v) ? c_row(r, groups, group_rows) : r;
+      cp_async8(As + (ar + u * AR_STEP) * kPjLDA + ak, v ? A + ra * lda + k0 + ak : A, v);
     }
 #pragma unroll
     for (int u = 0; u < BEPT; ++u) {
@@ -575,7 +578,7 @@ static int rows_gemm_res(const double *A, int64_t rows, int64_t lda, int K, cons
 static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int N,
                      double *C, double alpha, double beta, int a_splits,
                      const int64_t *groups, int64_t group_rows,
-                     bfmm_stream_t stream) {
+                     bfmm_stream_t stream, int gather_a = 0) {
   if (rows <= 0 || N <= 0) return 0;
   if (a_splits < 1 || K < 1) {
     set_error("bfmm_rows_gemm: a_splits=%d K=%d", a_splits, K);
@@ -612,10 +615,10 @@ static int rows_gemm(const double *A, int64_t rows, int K, const double *B, int 
   }
   if (wn == 2)
     proj_gemm_kernel<2><<<grid, 256, pj_smem<2>(), st>>>(A, rows, lda, K, B, N, C, alpha,
-                                                        beta, groups, group_rows);
+                                                        beta, groups, group_rows, gather_a);
   else
     proj_gemm_kernel<1><<<grid, 128, pj_smem<1>(), st>>>(A, rows, lda, K, B, N, C, alpha,
-                                                        beta, groups, group_rows);
+                                                        beta, groups, group_rows, gather_a);
   return check_launch("proj_gemm_kernel");
 }
 
@@ -671,6 +674,17 @@ extern "C" int bfmm_rows_gemm_scatter(const double *A, int64_t rows, int K,
     return 2;
   }
   return rows_gemm(A, rows, K, B, N, C, alpha, beta, a_splits, groups, group_rows, stream);
+}
+
+extern "C" int bfmm_rows_gemm_cells(const double *A, int64_t rows, int K, const double *B,
+                                    int N, double *C, double alpha, const int64_t *groups,
+                                    int64_t group_rows, bfmm_stream_t stream) {
+  if (!groups || group_rows < 1) {
+    set_error("bfmm_rows_gemm_cells: groups=%p group_rows=%lld", (const void *)groups,
+              (long long)group_rows);
+    return 2;
+  }
+  return rows_gemm(A, rows, K, B, N, C, alpha, 0.0, 1, groups, group_rows, stream, 1);
 }
 
 extern "C" int bfmm_m2l_cheb_splits(int level, int m, int rp, int64_t nq) {

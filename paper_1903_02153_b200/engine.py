@@ -686,13 +686,16 @@ class FmmEvaluator:
             out[lev] = (grouped, off, nact)
         return out
 
-    def _far_field(self, moments, m, shard, active=None):
+    def _far_field(self, moments, m, shard, active=None, active_src=False):
         """Locals of every level 2..L (engine.py:228-292).  The levels are
         independent; with stream_levels the coarse ones (2..L-2, small and
         latency-bound) run on a side stream under the two finest."""
         torch = _torch()
         L = self.plan.levels
         active = active or {}
+        # active_src: the active target cells are also the cells with sources
+        # below them (shared source / target tree), see _far_level
+        self._active_src = bool(active_src)
         locs = {}
         coarse = list(range(2, L - self.main_levels + 1)) if (self.stream_levels and shard is None) else []
         if coarse:
@@ -735,13 +738,23 @@ class FmmEvaluator:
             rp = blk["rp"]
             longest = int(np.max(off[1:] - off[:-1]))
             ns = self._m2l_splits(lev, m, rp, max(longest, 1))
-            z = zalloc((ncell * m * rp,), dtype=torch.float64, device=self.device)
             lt = torch.empty((max(nact, 1) * m * ns * rp,), dtype=torch.float64,
                              device=self.device)
             out.zero_()
-            _native.check(self.lib.bfmm_rows_gemm(
-                moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
-                z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
+            if self._active_src:
+                # shared tree: the other cells have no sources below them, so
+                # their moments and z rows are zero -- project the listed
+                # cells only (C4 level 7: 82k of 2.1M cells)
+                z = torch.zeros((ncell * m * rp,), dtype=torch.float64, device=self.device)
+                if nact:
+                    _native.check(self.lib.bfmm_rows_gemm_cells(
+                        moments[lev].data_ptr(), nact * m, p3, blk["V"].data_ptr(), rp,
+                        z.data_ptr(), 1.0, cells.data_ptr(), m, st), "bfmm_rows_gemm_cells(V)")
+            else:
+                z = zalloc((ncell * m * rp,), dtype=torch.float64, device=self.device)
+                _native.check(self.lib.bfmm_rows_gemm(
+                    moments[lev][lo * m * p3:].data_ptr(), nloc * m, p3, blk["V"].data_ptr(), rp,
+                    z[lo * m * rp:].data_ptr(), 1.0, 0.0, 1, st), "bfmm_rows_gemm(V)")
             if shard is not None and not shard[0].full:
                 shard[1].exchange_level(z, m * rp, lev, shard[0])
             self._m2l_translate(z, lt, lev, m, rp, ns, blk, st, cells=cells, off=off, shard=shard)
@@ -1100,7 +1113,8 @@ class FmmEvaluator:
             if ev:
                 ev[3].record()
             if not self._disable_far_field:
-                locs = self._far_field(moments, m, shard, self._active_cells(ttree, shard))
+                locs = self._far_field(moments, m, shard, self._active_cells(ttree, shard),
+                                       active_src=stree is ttree)
                 if overlap and side is None:
                     # enqueued after the far field: the persistent P2P grid fills
                     # the SMs the M2L CTAs leave free instead of holding them all
