@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 session W (re-run as W2 after the FFT / P2M-batch changes): evidence of the current tree -- bench C5 (headline, with C2 secondary and the
 # reference cpu_baseline), bench C1..C4, the reference arm, the gpu suite, the C5 launch list.
-O=gpurun_out/r2w4
+O=gpurun_out/r2w6
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $O/smi.txt 2>&1
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err
