@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 session W (re-run as W2 after the FFT / P2M-batch changes): evidence of the current tree -- bench C5 (headline, with C2 secondary and the
+# Round-2 session W (final evidence run; last output directory r2w6): evidence of the current tree -- bench C5 (headline, with C2 secondary and the
 # reference cpu_baseline), bench C1..C4, the reference arm, the gpu suite, the C5 launch list.
 O=gpurun_out/r2w6
 mkdir -p $O
