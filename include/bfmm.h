@@ -246,6 +246,14 @@ int bfmm_m2l_i8_zmax(const double *z, int64_t rows, int m, int rp,
                      unsigned long long *zmax, bfmm_stream_t stream);
 int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int S,
                         int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream);
+/* Sparse clouds: the same for the m rows of each listed cell only (compact
+ * row r = array row cells[r / m] * m + r % m of z and zs; rows = listed
+ * cells x m).  The digit rows of the other cells are not written: the caller
+ * zero-fills zs once (their z is zero).  Without BFMM_I8_ZMAX_GIVEN the scale
+ * is taken over the listed rows. */
+int bfmm_m2l_i8_slice_z_cells(const double *z, int64_t rows, int m, int rp, int S,
+                              int8_t *zs, unsigned long long *zmax, const int64_t *cells,
+                              bfmm_stream_t stream);
 int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq);
 int bfmm_m2l_i8(const int8_t *zs, const unsigned long long *zmax, const int8_t *cs,
                 const double *cpow, double *lt, int level, int m, int rp, int S,

@@ -51,6 +51,7 @@ SIGNATURES = {
     "bfmm_m2l_cheb": (_I, [_P, _P, _I, _I, _I, _I, _I64, _I64, _P, _P]),
     "bfmm_m2l_i8_zs_bytes": (_SZ, [_I64, _I, _I]),
     "bfmm_m2l_i8_slice_z": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P]),
+    "bfmm_m2l_i8_slice_z_cells": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P, _P]),
     "bfmm_m2l_i8_zmax": (_I, [_P, _I64, _I, _I, _P, _P]),
     "bfmm_m2l_i8_splits": (_I, [_I, _I, _I, _I64]),
     "bfmm_m2l_i8": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _I64, _P]),

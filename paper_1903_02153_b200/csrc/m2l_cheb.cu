@@ -779,8 +779,8 @@ extern "C" size_t bfmm_m2l_i8_zs_bytes(int64_t rows, int rp, int Sarg) {
   return (size_t)rows * ceil_div(rp, 32) * (Sarg & 0xff) * 32;
 }
 
-extern "C" int bfmm_m2l_i8_zmax(const double *z, int64_t rows, int m, int rp,
-                                unsigned long long *zmax, bfmm_stream_t stream) {
+static int i8_zmax(const double *z, int64_t rows, int m, int rp, unsigned long long *zmax,
+                   const int64_t *groups, bfmm_stream_t stream) {
   if (rp <= 0 || rows < 0 || m < 1 || m > 65535 || rows % m) {
     set_error("bfmm_m2l_i8_zmax: rp=%d, m=%d, rows=%lld", rp, m, (long long)rows);
     return 2;
@@ -793,12 +793,17 @@ extern "C" int bfmm_m2l_i8_zmax(const double *z, int64_t rows, int m, int rp,
   if (rows == 0) return 0;
   const int64_t n = rows / m * rp;
   absmax_bits_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs), m), 256,
-                       0, st>>>(z, rows, rp, m, zmax);
+                       0, st>>>(z, rows, rp, m, zmax, groups);
   return check_launch("absmax_bits_kernel");
 }
 
-extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int Sarg,
-                                   int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream) {
+extern "C" int bfmm_m2l_i8_zmax(const double *z, int64_t rows, int m, int rp,
+                                unsigned long long *zmax, bfmm_stream_t stream) {
+  return i8_zmax(z, rows, m, rp, zmax, nullptr, stream);
+}
+
+static int i8_slice_z(const double *z, int64_t rows, int m, int rp, int Sarg, int8_t *zs,
+                      unsigned long long *zmax, const int64_t *groups, bfmm_stream_t stream) {
   int S, B;
   i8_digits(Sarg, &S, &B);
   if (rp <= 0 || rp > 256 || S < 5 || S > 8 || (B == 8 && S != 6) || rows < 0 || m < 1 ||
@@ -809,22 +814,37 @@ extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp,
   }
   cudaStream_t st = as_stream(stream);
   if (!(Sarg & BFMM_I8_ZMAX_GIVEN)) {
-    if (int rc = bfmm_m2l_i8_zmax(z, rows, m, rp, zmax, stream)) return rc;
+    if (int rc = i8_zmax(z, rows, m, rp, zmax, groups, stream)) return rc;
   }
   if (rows == 0) return 0;
   const int kc_n = (int)ceil_div(rp, 32);
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows * kc_n * 2, 256), 16 * kNumSMs);
   if (B == 8) {
-    z_slice_kernel<6, 8><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs);
+    z_slice_kernel<6, 8><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs, groups);
   } else {
     switch (S) {
-      case 5: z_slice_kernel<5, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
-      case 6: z_slice_kernel<6, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
-      case 7: z_slice_kernel<7, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
-      default: z_slice_kernel<8, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs); break;
+      case 5: z_slice_kernel<5, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs, groups); break;
+      case 6: z_slice_kernel<6, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs, groups); break;
+      case 7: z_slice_kernel<7, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs, groups); break;
+      default: z_slice_kernel<8, 7><<<grid, 256, 0, st>>>(z, rows, rp, kc_n, m, zmax, zs, groups); break;
     }
   }
   return check_launch("z_slice_kernel");
+}
+
+extern "C" int bfmm_m2l_i8_slice_z(const double *z, int64_t rows, int m, int rp, int Sarg,
+                                   int8_t *zs, unsigned long long *zmax, bfmm_stream_t stream) {
+  return i8_slice_z(z, rows, m, rp, Sarg, zs, zmax, nullptr, stream);
+}
+
+extern "C" int bfmm_m2l_i8_slice_z_cells(const double *z, int64_t rows, int m, int rp, int Sarg,
+                                         int8_t *zs, unsigned long long *zmax,
+                                         const int64_t *cells, bfmm_stream_t stream) {
+  if (!cells) {
+    set_error("bfmm_m2l_i8_slice_z_cells: cell list required");
+    return 2;
+  }
+  return i8_slice_z(z, rows, m, rp, Sarg, zs, zmax, cells, stream);
 }
 
 extern "C" int bfmm_m2l_i8_splits(int level, int m, int rp, int64_t nq) {

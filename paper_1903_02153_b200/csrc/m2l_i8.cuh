@@ -624,14 +624,17 @@ m2l_i8p_kernel(const int8_t *__restrict__ zs, const unsigned long long *__restri
 
 // max |z| over n doubles as the bit pattern of a non-negative double
 // (order-preserving as an unsigned integer, so atomicMax is exact).
+// groups (nullable): the rows are the m rows of each listed cell, compact row
+// r = array row groups[r / m] * m + r % m (sparse clouds: occupied cells).
 __global__ void absmax_bits_kernel(const double *__restrict__ z, int64_t rows, int rp, int m,
-                                   unsigned long long *__restrict__ out) {
+                                   unsigned long long *__restrict__ out,
+                                   const int64_t *__restrict__ groups = nullptr) {
   // block column blockIdx.y = weight column c: rows c, c + m, c + 2m, ...
   const int c = blockIdx.y;
   const int64_t nr = (rows - c + m - 1) / m;
   const int64_t n = nr * rp;
   unsigned long long mx = 0;
-  if (m == 1) {  // one column: the whole array, no index arithmetic
+  if (m == 1 && !groups) {  // one column: the whole array, no index arithmetic
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
          e += int64_t(gridDim.x) * blockDim.x) {
       const unsigned long long b =
@@ -643,9 +646,9 @@ __global__ void absmax_bits_kernel(const double *__restrict__ z, int64_t rows, i
          e += int64_t(gridDim.x) * blockDim.x) {
       const int64_t i = e / rp;
       const int k = (int)(e - i * rp);
+      const int64_t R = groups ? groups[i] * m + c : c + i * m;
       const unsigned long long b =
-          (unsigned long long)__double_as_longlong(z[(c + i * m) * rp + k]) &
-          0x7fffffffffffffffull;
+          (unsigned long long)__double_as_longlong(z[R * rp + k]) & 0x7fffffffffffffffull;
       mx = b > mx ? b : mx;
     }
   }
@@ -666,14 +669,17 @@ __global__ void absmax_bits_kernel(const double *__restrict__ z, int64_t rows, i
 template <int S, int B>
 __global__ void z_slice_kernel(const double *__restrict__ z, int64_t rows, int rp, int kc_n,
                                int m, const unsigned long long *__restrict__ zmax,
-                               int8_t *__restrict__ zs) {
+                               int8_t *__restrict__ zs,
+                               const int64_t *__restrict__ groups = nullptr) {
   const int64_t total = rows * kc_n * 2;
   const unsigned per_row = (unsigned)(kc_n * 2);
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     // 32-bit division when the index fits (every level up to 2^31 chunks)
-    const int64_t row = total <= 0xffffffffll ? (int64_t)((unsigned)e / per_row) : e / per_row;
-    const int rem = (int)(e - row * per_row);
+    const int64_t crow = total <= 0xffffffffll ? (int64_t)((unsigned)e / per_row) : e / per_row;
+    const int rem = (int)(e - crow * per_row);
+    // listed cells: compact row -> the cell's row of the level's arrays
+    const int64_t row = groups ? groups[crow / m] * m + crow % m : crow;
     const int kc = rem >> 1, h = rem & 1;
     const int k0 = kc * 32 + h * 16;
     const double amax = __longlong_as_double((long long)zmax[m == 1 ? 0 : row % m]);

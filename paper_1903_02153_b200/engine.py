@@ -385,8 +385,14 @@ class FmmEvaluator:
             cs, cpow = self._i8_tables(blk, S, bits)
             Sarg = S | (_native.I8_BASE256 if bits == 8 else 0)
             rows = z.numel() // rp
-            zs = torch.empty(int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, Sarg)), dtype=torch.int8,
-                             device=self.device)
+            # sparse cloud on a shared tree, unsharded: z is non-zero in the
+            # listed cells only, so only their rows are scanned and cut (the
+            # other digit rows stay zero)
+            listed = (cells is not None and getattr(self, "_active_src", False)
+                      and (shard is None or shard[0].full) and zmax is None)
+            zs = (torch.zeros if listed else torch.empty)(
+                int(self.lib.bfmm_m2l_i8_zs_bytes(rows, rp, Sarg)), dtype=torch.int8,
+                device=self.device)
             if zmax is not None:
                 # max |z| from the int8 projection's epilogue (one column)
                 if shard is not None and not shard[0].full:
@@ -401,9 +407,17 @@ class FmmEvaluator:
                                                         zmax.data_ptr(), st), "bfmm_m2l_i8_zmax")
                 shard[1].allreduce_max(zmax)
                 Sarg |= _native.I8_ZMAX_GIVEN
-            _native.check(self.lib.bfmm_m2l_i8_slice_z(z.data_ptr(), rows, m, rp, Sarg,
-                                                       zs.data_ptr(), zmax.data_ptr(), st),
-                          "bfmm_m2l_i8_slice_z")
+            if listed:
+                if cells.numel() and off[8] > 0:
+                    _native.check(self.lib.bfmm_m2l_i8_slice_z_cells(
+                        z.data_ptr(), int(off[8]) * m, m, rp, Sarg, zs.data_ptr(),
+                        zmax.data_ptr(), cells.data_ptr(), st), "bfmm_m2l_i8_slice_z_cells")
+                else:
+                    zmax.zero_()
+            else:
+                _native.check(self.lib.bfmm_m2l_i8_slice_z(z.data_ptr(), rows, m, rp, Sarg,
+                                                           zs.data_ptr(), zmax.data_ptr(), st),
+                              "bfmm_m2l_i8_slice_z")
             e0 = self._kevent()
             if cells is not None:
                 _native.check(self.lib.bfmm_m2l_i8_cells(
