@@ -65,6 +65,49 @@ def _run_both(level, rp, m, S, ns, seed=0, gather=False, bits=7):
     return got, ref.view(rows, rp).cpu().numpy(), outs[0]
 
 
+@pytest.mark.parametrize("ncell,nact,p3,rp,m,bits", [(4096, 300, 216, 168, 1, 7), (512, 40, 125, 61, 3, 8),
+                                                      (4096, 1, 64, 37, 1, 8)])
+def test_listed_cell_projection_and_slicing_equal_dense(ncell, nact, p3, rp, m, bits):
+    """Sparse clouds (C ABI): bfmm_rows_gemm_cells and
+    bfmm_m2l_i8_slice_z_cells over the listed (occupied) cells against the
+    dense bfmm_rows_gemm / bfmm_m2l_i8_slice_z over every cell, the other
+    cells' moments being zero: z rows, digit scale and digit planes bitwise
+    equal (engine.py:233; the evaluator's active far field on a shared tree)."""
+    lib = _native.load()
+    st = _native.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    g = np.random.default_rng(ncell + nact)
+    cells = np.sort(g.choice(ncell, nact, replace=False)).astype(np.int64)
+    mom = np.zeros((ncell * m, p3))
+    for c in cells:
+        mom[c * m:(c + 1) * m] = g.standard_normal((m, p3)) * np.exp(g.uniform(-6, 2))
+    V = g.standard_normal((p3, rp))
+    dm, dV, dc = torch.from_numpy(mom).cuda(), torch.from_numpy(V).cuda(), torch.from_numpy(cells).cuda()
+    z_dense = torch.full((ncell * m, rp), float("nan"), dtype=torch.float64, device="cuda")
+    _native.check(lib.bfmm_rows_gemm(dm.data_ptr(), ncell * m, p3, dV.data_ptr(), rp,
+                                     z_dense.data_ptr(), 1.0, 0.0, 1, st), "rows_gemm")
+    z_list = torch.zeros((ncell * m, rp), dtype=torch.float64, device="cuda")
+    _native.check(lib.bfmm_rows_gemm_cells(dm.data_ptr(), nact * m, p3, dV.data_ptr(), rp,
+                                           z_list.data_ptr(), 1.0, dc.data_ptr(), m, st),
+                  "rows_gemm_cells")
+    torch.cuda.synchronize()
+    assert torch.equal(z_dense, z_list)
+    S = 6 if bits == 8 else 7
+    Sarg = S | (_native.I8_BASE256 if bits == 8 else 0)
+    nbytes = int(lib.bfmm_m2l_i8_zs_bytes(ncell * m, rp, Sarg))
+    zs_d = torch.full((nbytes,), 55, dtype=torch.int8, device="cuda")
+    zs_l = torch.zeros(nbytes, dtype=torch.int8, device="cuda")
+    zm_d = torch.empty(m, dtype=torch.int64, device="cuda")
+    zm_l = torch.empty(m, dtype=torch.int64, device="cuda")
+    _native.check(lib.bfmm_m2l_i8_slice_z(z_dense.data_ptr(), ncell * m, m, rp, Sarg,
+                                          zs_d.data_ptr(), zm_d.data_ptr(), st), "slice")
+    _native.check(lib.bfmm_m2l_i8_slice_z_cells(z_list.data_ptr(), nact * m, m, rp, Sarg,
+                                                zs_l.data_ptr(), zm_l.data_ptr(), dc.data_ptr(),
+                                                st), "slice_cells")
+    torch.cuda.synchronize()
+    assert torch.equal(zm_d, zm_l)
+    assert torch.equal(zs_d, zs_l)
+
+
 @pytest.mark.parametrize("level,rp,m,S,ns", [(3, 56, 1, 7, 1), (3, 104, 1, 7, 3),
                                              (3, 64, 3, 6, 2), (2, 168, 1, 8, 1),
                                              (4, 56, 1, 5, 4), (2, 8, 2, 7, 189),
