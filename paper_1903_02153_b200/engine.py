@@ -14,6 +14,7 @@ skip every host<->device copy).
 from __future__ import annotations
 
 import contextlib
+import os
 import time
 from dataclasses import dataclass
 
@@ -251,6 +252,9 @@ class FmmEvaluator:
         self.kernel_ms = {}
         self._kpending = []
         # replay the device step from a CUDA graph when possible (_graph_ok)
+        # NVTX ranges around the stages and the far-field levels (for Nsight
+        # timelines; the reference's tracing is its `timings` dict, engine.py:505-533)
+        self.nvtx = bool(os.environ.get("BFMM_NVTX"))
         self.use_graph = False
         self._graphs = {}
         self.graph_launches = 0  # kernels of ours run by graph replays (bench accounting)
@@ -450,6 +454,14 @@ class FmmEvaluator:
         return self._dev_blocks[0] if self.table.single_level else self._dev_blocks[level]
 
     # -- helpers --------------------------------------------------------------
+    def _nv_push(self, name):
+        if self.nvtx:
+            _torch().cuda.nvtx.range_push("bfmm." + name)
+
+    def _nv_pop(self):
+        if self.nvtx:
+            _torch().cuda.nvtx.range_pop()
+
     @staticmethod
     def _stream():
         torch = _torch()
@@ -729,6 +741,13 @@ class FmmEvaluator:
         return locs
 
     def _far_level(self, lev, moments, m, shard, active):
+        self._nv_push(f"m2l_level_{lev}")
+        try:
+            return self._far_level_impl(lev, moments, m, shard, active)
+        finally:
+            self._nv_pop()
+
+    def _far_level_impl(self, lev, moments, m, shard, active):
         torch = _torch()
         p = self.plan.order
         p3 = p ** 3
@@ -887,6 +906,13 @@ class FmmEvaluator:
             locs[L].data_ptr(), phi_far.data_ptr(), status[_ST_REF:].data_ptr(), st), "bfmm_l2p")
 
     def _near_field(self, ttree, stree, ws, m, near, shard):
+        self._nv_push("near_field")
+        try:
+            return self._near_field_impl(ttree, stree, ws, m, near, shard)
+        finally:
+            self._nv_pop()
+
+    def _near_field_impl(self, ttree, stree, ws, m, near, shard):
         torch = _torch()
         st = self._stream()
         sb = self.lib.bfmm_p2p_scratch_bytes(max(ttree.max_leaves, 1), ttree.n)
@@ -1062,6 +1088,7 @@ class FmmEvaluator:
         st = self._stream()
         if ev:
             ev[1].record()
+        self._nv_push("distribute")
         stree = self._build_tree(src, status, _ST_DOMAIN_SRC)
         ttree = stree if shared else self._build_tree(tgt, status, _ST_DOMAIN_TGT)
         if w_event is not None:
@@ -1071,6 +1098,7 @@ class FmmEvaluator:
                                                    ws.data_ptr(), stree.pts4.data_ptr(),
                                                    status[_ST_WEIGHTS:].data_ptr(), st),
                       "bfmm_gather_weights")
+        self._nv_pop()
         if ev:
             ev[2].record()
         shard = _shard if sharded else None
@@ -1123,19 +1151,25 @@ class FmmEvaluator:
             hi.wait_stream(main)
         phi_far = alloc((max(n_tgt, 1), m), dtype=torch.float64, device=self.device)
         with (torch.cuda.stream(hi) if hi is not None else contextlib.nullcontext()):
+            self._nv_push("upward")
             moments, leaf_geom = self._upward(stree, ws, m, status, shard)
+            self._nv_pop()
             if ev:
                 ev[3].record()
             if not self._disable_far_field:
+                self._nv_push("far_field")
                 locs = self._far_field(moments, m, shard, self._active_cells(ttree, shard),
                                        active_src=stree is ttree)
+                self._nv_pop()
                 if overlap and side is None:
                     # enqueued after the far field: the persistent P2P grid fills
                     # the SMs the M2L CTAs leave free instead of holding them all
                     side = near_on_side()
                 if ev:
                     ev[4].record()
+                self._nv_push("downward")
                 self._downward(locs, ttree, m, leaf_geom, status, phi_far, shard)
+                self._nv_pop()
             else:
                 locs = None
                 phi_far = None

@@ -395,6 +395,18 @@ def test_laplace_subnormal_distances_take_exact_path(cache_dir):
     assert np.max(np.abs(got[-4:])) > 1e150
 
 
+def test_nvtx_ranges_do_not_change_results(cache_dir):
+    """ev.nvtx (or BFMM_NVTX=1) wraps the stages and far-field levels in NVTX
+    ranges for Nsight timelines; the matvec itself is untouched."""
+    pts, w = unit_cloud(5000, seed=33)
+    ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(levels=3, order=4), cache_dir=cache_dir)
+    a = ev.evaluate(pts, weights=w)
+    ev.nvtx = True
+    b = ev.evaluate(pts, weights=w)
+    assert np.array_equal(a, b)
+    assert set(ev.timings) >= {"distribute", "upward", "far_field", "downward", "near_field"}
+
+
 def test_rejects_bad_inputs(cache_dir):
     pts, w = unit_cloud(100, seed=0)
     ev = bf.FmmEvaluator(bf.LAPLACIAN, small_plan(), cache_dir=cache_dir)
